@@ -1,0 +1,145 @@
+/* turnstile_b200.h - C ABI of the B200-native iterative NUTS engine.
+ *
+ * The reference (turnstile, pure Python + numba) has no native boundary: its
+ * hot path is the Python call chain
+ *   chains.run -> run_chain -> nuts_transition_from -> build_tree_iterative
+ *   -> integrator.leapfrog -> model.potential / model.gradient -> kernels.*
+ * Each entry point below replaces one link of that chain; the Python package
+ * paper_1912_11554_b200 binds them with ctypes (INTEGRATION.md shows the
+ * binding) and keeps the reference's Python API on top.
+ *
+ * Conventions:
+ *  - every pointer argument named *_dev is device memory owned by the caller
+ *    (torch tensors); the library owns only ts_model handles and transient
+ *    workspaces;
+ *  - return 0 on success; TS_EINVAL for contract violations (the Python layer
+ *    raises ValueError, as the reference does), TS_ECUDA / TS_EUNSUPPORTED
+ *    otherwise (RuntimeError); ts_last_error() describes the last failure of
+ *    the calling thread;
+ *  - numerical events are data, never errors: +inf energies, divergence
+ *    flags and -inf log weights are returned in the outputs;
+ *  - calls are ordered on the given CUDA stream (NULL = legacy stream).
+ */
+#ifndef TURNSTILE_B200_H
+#define TURNSTILE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TS_ABI_VERSION 1
+
+enum { TS_OK = 0, TS_EINVAL = 1, TS_ECUDA = 2, TS_EUNSUPPORTED = 3 };
+
+/* Model kinds.  Reference constructors: models.py:67-144 (std_normal,
+ * gaussian, logistic_regression, funnel); eight_schools is the SURVEY 8(d)
+ * config-3 model (no reference built-in; oracle twin in oracle/). */
+enum { TS_STD_NORMAL = 0, TS_GAUSSIAN = 1, TS_LOGISTIC = 2, TS_FUNNEL = 3, TS_EIGHT_SCHOOLS = 4 };
+
+/* Arithmetic policy of the logistic data pass (ts_logistic.cuh). */
+enum { TS_PREC_FP64 = 0, TS_PREC_FP32 = 1 };
+
+/* U-turn criterion (tree.py:36-37). */
+enum { TS_GENERALIZED = 0, TS_CLASSIC = 1 };
+
+/* Team layout for small models: one chain per thread (default) or per CTA. */
+typedef enum { TS_EXEC_THREAD = 0, TS_EXEC_BLOCK = 1 } ts_exec_mode;
+
+/* SamplerConfig (sampler.py:38-59). */
+typedef struct {
+  double step_size;
+  int32_t max_tree_depth;
+  int32_t criterion;
+  double divergence_threshold;
+} ts_sampler_cfg;
+
+/* RunConfig (chains.py:36-57) minus model/mode/seed, which the host resolves. */
+typedef struct {
+  int32_t num_warmup;
+  int32_t num_samples;
+  double target_accept;
+  int32_t has_sampler; /* RunConfig.sampler is not None (chains.py:137-143) */
+  int32_t pad_;
+  ts_sampler_cfg sampler;
+} ts_run_cfg;
+
+typedef struct ts_model ts_model;
+
+const char* ts_last_error(void);
+int ts_abi_version(void);
+
+/* Replaces models.py:67-144 + LogisticRegressionData (models.py:43-64): builds
+ * a device model.  params (host): gaussian inv_var[dim]; eight_schools
+ * y[J], sigma[J] (dim = J + 2).  Logistic: x_dev row-major fp32 (n_rows x
+ * n_feat), y_dev uint8 in {0,1}; the library re-tiles X into its own HBM
+ * layout. */
+int ts_model_create(int kind, int dim, const double* params, int n_params, const float* x_dev, const uint8_t* y_dev,
+                    int64_t n_rows, int n_feat, int precision, ts_model** out);
+int ts_model_destroy(ts_model* m);
+int ts_model_dim(const ts_model* m);
+/* Cap the number of CTAs of the persistent logistic grid (0 = one per SM). */
+int ts_model_set_grid(ts_model* m, int grid);
+
+/* Replaces model.potential + model.gradient (models.py:110-118 ->
+ * kernels.py:90-123): one fused pass per point.  q_dev [n][dim];
+ * out_dev [n][1 + dim] = (U, gradient).  U is returned raw (may be inf/nan). */
+int ts_potential_grad(const ts_model* m, const double* q_dev, int n_points, double* out_dev, void* stream);
+
+/* Benchmark helper: `repeats` evaluations of the same point inside one
+ * persistent launch (the per-leapfrog model cost of the device loop). */
+int ts_eval_bench(const ts_model* m, const double* q_dev, int repeats, double* out_dev, void* stream);
+
+/* Replaces integrator.leapfrog (integrator.py:90-103).
+ * z = [q dim | r dim | grad dim | U]; z_out same layout. */
+int ts_leapfrog(const ts_model* m, const double* inv_dev, const double* z_in, double eps, double* z_out, int exec_mode,
+                void* stream);
+
+/* Replaces tree.build_tree_iterative (tree.py:344-453).  z_in as above; the
+ * tree's uniforms come from the device Philox stream of key (== numpy's
+ * RngKey(key).generator()).  tree_out [8*dim + 10]:
+ *   left.q, left.r, right.q, right.r, right.grad, proposal.q, proposal.grad,
+ *   momentum_sum, then lw, sum_metropolis, leapfrog_count, turning,
+ *   diverging, proposal.U, proposal.H, proposal leaf index, left.U, right.U.
+ * Optional trace (TreeTrace, tree.py:165-187): events int32[cap][5], leaf
+ * log weights, counts int32[3] = (events, leaf weights, max occupied). */
+int ts_build_tree(const ts_model* m, const ts_sampler_cfg* cfg, const double* inv_dev, const double* z_in, int depth,
+                  double eps, double h_ref, uint64_t key_hi, uint64_t key_lo, double* tree_out, int32_t* trace_ev,
+                  int trace_cap, double* leaf_lw, int lw_cap, int32_t* trace_counts, int exec_mode, void* stream);
+
+/* Replaces sampler.nuts_transition_from (sampler.py:83-148).  z_in as above
+ * (momentum ignored).  normals_or_null: injected standard normals for the
+ * momentum refresh, else drawn on device from fold(key, 0) exactly as numpy
+ * does.  out [2*dim + 8]: q, grad, U, depth, leapfrogs, diverged,
+ * accept_stat, energy, proposal tree, proposal leaf. */
+int ts_transition(const ts_model* m, const ts_sampler_cfg* cfg, const double* inv_dev, const double* z_in,
+                  const double* normals_or_null, uint64_t key_hi, uint64_t key_lo, double* out, int32_t* trace_ev,
+                  int trace_cap, int32_t* trace_counts, int exec_mode, void* stream);
+
+/* Replaces adapt.find_reasonable_step_size (adapt.py:172-204). out[1]. */
+int ts_find_step_size(const ts_model* m, const double* inv_dev, const double* z_in, const double* normals_or_null,
+                      uint64_t key_hi, uint64_t key_lo, double init, double* out, int exec_mode, void* stream);
+
+/* Replaces chains.run_chain for every chain (chains.py:98-163, adapt.py:207-236):
+ * warmup adaptation and sampling entirely on device, one launch.
+ * chain_keys_dev [C][2] (hi, lo); inv0_dev [dim]; schedule_dev [W] (bit0 in a
+ * covariance window, bit1 window end: WarmupSchedule.window_steps,
+ * adapt.py:119-127); da_weight_dev [W] = t^-kappa.  Outputs: samples
+ * [C][S][dim], stats [C][W+S][5] (depth, leapfrogs, diverged, accept_stat,
+ * energy), adapt [C][2+W+dim] (initial step, final step, step trace,
+ * inverse mass), status [C] (0 ok, 1 invalid mass install). */
+int ts_run_chains(const ts_model* m, const ts_run_cfg* rc, const uint64_t* chain_keys_dev, int n_chains,
+                  const double* inv0_dev, const uint8_t* schedule_dev, const double* da_weight_dev, double* samples,
+                  double* stats, double* adapt, int32_t* status, int exec_mode, void* stream);
+
+/* Parity probe of the device randomness (csrc/ts_rng.cuh): kind 0 writes n
+ * Generator.random() doubles of RngKey(key).generator(), kind 1 n
+ * standard_normal() values, kind 2 the keys fold(0..n-1) as raw 64-bit
+ * words [n][2].  Replaces nothing in the reference; used by tests. */
+int ts_rng_probe(uint64_t key_hi, uint64_t key_lo, int kind, int n, double* out_dev, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,325 @@
+// C-ABI of the B200 turnstile engine (declared in include/turnstile_b200.h).
+//
+// Kernels:
+//   k_thread_op  - ThreadTeam: one chain (or one parity op) per thread, small
+//                  models, vectors in a chain-interleaved global workspace.
+//   k_block_op   - BlockTeam: one replica of the chain per CTA; with the
+//                  logistic model the CTAs form a cooperative persistent grid
+//                  that evaluates each potential together (one grid barrier
+//                  per leapfrog) and run the tree logic redundantly.
+#include <stdio.h>
+#include "ts_internal.cuh"
+
+using namespace ts;
+using namespace ts_internal;
+
+// ------------------------------------------------------------------ errors
+static thread_local std::string g_last_error;
+namespace ts_internal {
+int set_err(int code, const char* msg) {
+  g_last_error = msg;
+  return code;
+}
+}  // namespace ts_internal
+
+extern "C" const char* ts_last_error(void) { return g_last_error.c_str(); }
+extern "C" int ts_abi_version(void) { return TS_ABI_VERSION; }
+
+__global__ void k_retile(const float* __restrict__ x, const uint8_t* __restrict__ y, int64_t n, int p, int64_t ntiles,
+                         float* __restrict__ xt, uint8_t* __restrict__ yt) {
+  const int64_t total = ntiles * 32 * (int64_t)p;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = i / p;
+    const int j = (int)(i % p);
+    const int64_t t = row >> 5;
+    const int lane = (int)(row & 31);
+    const int g = j >> 2;
+    const int w = (p - 4 * g) < 4 ? (p - 4 * g) : 4;
+    const int64_t dst = t * 32 * (int64_t)p + 128 * (int64_t)g + (int64_t)lane * w + (j & 3);
+    xt[dst] = row < n ? x[row * p + j] : 0.f;
+    if (j == 0) yt[row] = row < n ? y[row] : 0;
+  }
+}
+
+static int pick_pmax(int p) {
+  if (p <= 8) return 8;
+  if (p <= 32) return 32;
+  if (p <= 56) return 56;
+  if (p <= 64) return 64;
+  return 0;
+}
+
+// ------------------------------------------------------------------ helpers
+static int check_cfg(const ts_sampler_cfg* c) {
+  if (!c) return set_err(TS_EINVAL, "null sampler config");
+  if (!(c->step_size > 0) || !isfinite(c->step_size)) return set_err(TS_EINVAL, "step_size must be positive and finite");
+  if (c->max_tree_depth < 1 || c->max_tree_depth > 30) return set_err(TS_EINVAL, "max_tree_depth must be in [1, 30]");
+  if (c->criterion != TS_GENERALIZED && c->criterion != TS_CLASSIC) return set_err(TS_EINVAL, "unknown criterion");
+  if (!(c->divergence_threshold > 0)) return set_err(TS_EINVAL, "divergence_threshold must be positive");
+  return TS_OK;
+}
+
+static SamplerCfg to_cfg(const ts_sampler_cfg* c) {
+  SamplerCfg s;
+  s.step = c->step_size;
+  s.max_depth = c->max_tree_depth;
+  s.generalized = c->criterion == TS_GENERALIZED;
+  s.threshold = c->divergence_threshold;
+  return s;
+}
+
+static int launch(const ts_model* m, int nslots, OpArgs& A, int n_threads_chains, ts_exec_mode mode, cudaStream_t st) {
+  if (nslots < 1) nslots = 1;
+  if (nslots > kMaxSlots) return set_err(TS_EINVAL, "tree depth exceeds device slot limit (30)");
+  if (m->kind == TS_LOGISTIC) {
+    if (!m->pmax) return set_err(TS_EUNSUPPORTED, "logistic feature count > 64 not supported on this path");
+    return launch_block_logistic(m, nslots, A, st);
+  }
+  SmallModel sm;
+  sm.kind = m->kind;
+  sm.dim = m->dim;
+  sm.params = m->params;
+  const int D = m->dim;
+  if (mode == TS_EXEC_BLOCK) return launch_block_small(sm, D, nslots, A, st);
+  return launch_thread(sm, D, n_threads_chains, nslots, A, st);
+}
+
+// ------------------------------------------------------------------ C ABI
+extern "C" int ts_model_create(int kind, int dim, const double* params, int n_params, const float* x_dev,
+                               const uint8_t* y_dev, int64_t n_rows, int n_feat, int precision, ts_model** out) {
+  if (!out) return set_err(TS_EINVAL, "null output handle");
+  *out = nullptr;
+  if (dim < 1) return set_err(TS_EINVAL, "model dimension must be positive");
+  ts_model* m = new ts_model();
+  memset(m, 0, sizeof(*m));
+  m->kind = kind;
+  m->dim = dim;
+  cudaGetDevice(&m->device);
+  auto fail = [&](int code, const char* msg) {
+    if (m->params) cudaFree(m->params);
+    if (m->xt) cudaFree(m->xt);
+    if (m->yt) cudaFree(m->yt);
+    if (m->pbuf) cudaFree(m->pbuf);
+    if (m->bar) cudaFree(m->bar);
+    delete m;
+    return set_err(code, msg);
+  };
+  switch (kind) {
+    case TS_STD_NORMAL:
+      break;
+    case TS_GAUSSIAN:
+      if (n_params != dim || !params) return fail(TS_EINVAL, "gaussian needs dim inverse variances");
+      break;
+    case TS_FUNNEL:
+      if (dim < 2) return fail(TS_EINVAL, "funnel needs the scale coordinate plus at least one other");
+      break;
+    case TS_EIGHT_SCHOOLS:
+      if (dim < 3 || n_params != 2 * (dim - 2) || !params) return fail(TS_EINVAL, "eight_schools needs y[J], sigma[J] with dim = J + 2");
+      break;
+    case TS_LOGISTIC: {
+      if (n_feat < 1 || dim != n_feat + 1) return fail(TS_EINVAL, "logistic dim must equal num_features + 1");
+      if (n_rows < 1 || !x_dev || !y_dev) return fail(TS_EINVAL, "logistic needs at least one data row");
+      m->pmax = pick_pmax(n_feat);
+      if (!m->pmax) return fail(TS_EUNSUPPORTED, "logistic feature count > 64 not supported on this path");
+      m->n_rows = n_rows;
+      m->p = n_feat;
+      m->ntiles = (n_rows + 31) / 32;
+      m->fp64 = precision == TS_PREC_FP64;
+      const size_t nx = (size_t)m->ntiles * 32 * n_feat;
+      if (cudaMalloc((void**)&m->xt, nx * sizeof(float)) != cudaSuccess) return fail(TS_ECUDA, "cudaMalloc X failed");
+      if (cudaMalloc((void**)&m->yt, (size_t)m->ntiles * 32) != cudaSuccess) return fail(TS_ECUDA, "cudaMalloc y failed");
+      k_retile<<<1184, 256>>>(x_dev, y_dev, n_rows, n_feat, m->ntiles, m->xt, m->yt);
+      if (cudaGetLastError() != cudaSuccess) return fail(TS_ECUDA, "retile launch failed");
+      int nsm = 148;
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, m->device);
+      const size_t pb = 2 * (size_t)nsm * 2 * (n_feat + 2);  // room for up to 2 CTAs per SM
+      if (cudaMalloc((void**)&m->pbuf, pb * sizeof(double)) != cudaSuccess) return fail(TS_ECUDA, "cudaMalloc partials failed");
+      if (cudaMalloc((void**)&m->bar, sizeof(unsigned long long)) != cudaSuccess) return fail(TS_ECUDA, "cudaMalloc barrier failed");
+      if (cudaDeviceSynchronize() != cudaSuccess) return fail(TS_ECUDA, "retile failed");
+      break;
+    }
+    default:
+      return fail(TS_EINVAL, "unknown model kind");
+  }
+  if (n_params > 0 && params && kind != TS_LOGISTIC) {
+    if (cudaMalloc((void**)&m->params, n_params * sizeof(double)) != cudaSuccess) return fail(TS_ECUDA, "cudaMalloc params failed");
+    if (cudaMemcpy(m->params, params, n_params * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess)
+      return fail(TS_ECUDA, "params upload failed");
+    m->n_params = n_params;
+  }
+  *out = m;
+  return TS_OK;
+}
+
+extern "C" int ts_model_destroy(ts_model* m) {
+  if (!m) return TS_OK;
+  if (m->params) cudaFree(m->params);
+  if (m->xt) cudaFree(m->xt);
+  if (m->yt) cudaFree(m->yt);
+  if (m->pbuf) cudaFree(m->pbuf);
+  if (m->bar) cudaFree(m->bar);
+  delete m;
+  return TS_OK;
+}
+
+extern "C" int ts_model_set_grid(ts_model* m, int grid) {
+  if (!m) return set_err(TS_EINVAL, "null model");
+  m->grid = grid;
+  return TS_OK;
+}
+
+extern "C" int ts_model_dim(const ts_model* m) { return m ? m->dim : -1; }
+
+static OpArgs base_args(int op) {
+  OpArgs A;
+  memset(&A, 0, sizeof A);
+  A.op = op;
+  return A;
+}
+
+extern "C" int ts_potential_grad(const ts_model* m, const double* q_dev, int n_points, double* out_dev, void* stream) {
+  if (!m || !q_dev || !out_dev) return set_err(TS_EINVAL, "null argument");
+  if (n_points < 1) return TS_OK;
+  OpArgs A = base_args(OP_POTGRAD);
+  A.z_in = q_dev; A.z_out = out_dev; A.n_points = n_points;
+  // inv is read by do_op; use a dummy ones vector
+  double* ones = nullptr;
+  cudaStream_t st = (cudaStream_t)stream;
+  TS_CUDA(cudaMallocAsync((void**)&ones, m->dim * sizeof(double), st));
+  TS_CUDA(cudaMemsetAsync(ones, 0, m->dim * sizeof(double), st));
+  A.inv = ones;
+  int rc = launch(m, 1, A, 1, TS_EXEC_THREAD, st);
+  cudaFreeAsync(ones, st);
+  return rc;
+}
+
+extern "C" int ts_eval_bench(const ts_model* m, const double* q_dev, int repeats, double* out_dev, void* stream) {
+  if (!m || !q_dev || !out_dev) return set_err(TS_EINVAL, "null argument");
+  OpArgs A = base_args(OP_EVALBENCH);
+  A.z_in = q_dev; A.z_out = out_dev; A.n_points = repeats;
+  double* ones = nullptr;
+  cudaStream_t st = (cudaStream_t)stream;
+  TS_CUDA(cudaMallocAsync((void**)&ones, m->dim * sizeof(double), st));
+  TS_CUDA(cudaMemsetAsync(ones, 0, m->dim * sizeof(double), st));
+  A.inv = ones;
+  int rc = launch(m, 1, A, 1, TS_EXEC_BLOCK, st);
+  cudaFreeAsync(ones, st);
+  return rc;
+}
+
+extern "C" int ts_leapfrog(const ts_model* m, const double* inv_dev, const double* z_in, double eps, double* z_out,
+                           int exec_mode, void* stream) {
+  if (!m || !inv_dev || !z_in || !z_out) return set_err(TS_EINVAL, "null argument");
+  OpArgs A = base_args(OP_LEAPFROG);
+  A.z_in = z_in; A.z_out = z_out; A.inv = inv_dev; A.eps = eps;
+  return launch(m, 1, A, 1, (ts_exec_mode)exec_mode, (cudaStream_t)stream);
+}
+
+extern "C" int ts_build_tree(const ts_model* m, const ts_sampler_cfg* cfg, const double* inv_dev, const double* z_in,
+                             int depth, double eps, double h_ref, uint64_t key_hi, uint64_t key_lo, double* tree_out,
+                             int32_t* trace_ev, int trace_cap, double* leaf_lw, int lw_cap, int32_t* trace_counts,
+                             int exec_mode, void* stream) {
+  if (!m || !inv_dev || !z_in || !tree_out) return set_err(TS_EINVAL, "null argument");
+  int rc = check_cfg(cfg);
+  if (rc) return rc;
+  if (depth < 0) return set_err(TS_EINVAL, "depth must be non-negative");
+  if (depth > cfg->max_tree_depth) return set_err(TS_EINVAL, "depth exceeds max_tree_depth");
+  if (depth > 30) return set_err(TS_EINVAL, "depth exceeds the hard limit 30");
+  OpArgs A = base_args(OP_TREE);
+  A.z_in = z_in; A.z_out = tree_out; A.inv = inv_dev; A.cfg = to_cfg(cfg);
+  A.depth = depth; A.eps = eps; A.h_ref = h_ref; A.key_hi = key_hi; A.key_lo = key_lo;
+  if (trace_ev && trace_counts) {
+    A.has_trace = 1;
+    A.trace.ev = trace_ev; A.trace.cap = trace_cap; A.trace.leaf_lw = leaf_lw; A.trace.lw_cap = leaf_lw ? lw_cap : 0;
+    A.trace.counts = trace_counts;
+  }
+  return launch(m, depth, A, 1, (ts_exec_mode)exec_mode, (cudaStream_t)stream);
+}
+
+extern "C" int ts_transition(const ts_model* m, const ts_sampler_cfg* cfg, const double* inv_dev, const double* z_in,
+                             const double* normals_or_null, uint64_t key_hi, uint64_t key_lo, double* out,
+                             int32_t* trace_ev, int trace_cap, int32_t* trace_counts, int exec_mode, void* stream) {
+  if (!m || !inv_dev || !z_in || !out) return set_err(TS_EINVAL, "null argument");
+  int rc = check_cfg(cfg);
+  if (rc) return rc;
+  OpArgs A = base_args(OP_TRANSITION);
+  A.z_in = z_in; A.z_out = out; A.inv = inv_dev; A.cfg = to_cfg(cfg);
+  A.key_hi = key_hi; A.key_lo = key_lo; A.inj = normals_or_null;
+  if (trace_ev && trace_counts) {
+    A.has_trace = 1;
+    A.trace.ev = trace_ev; A.trace.cap = trace_cap; A.trace.counts = trace_counts;
+  }
+  return launch(m, cfg->max_tree_depth - 1, A, 1, (ts_exec_mode)exec_mode, (cudaStream_t)stream);
+}
+
+extern "C" int ts_find_step_size(const ts_model* m, const double* inv_dev, const double* z_in, const double* normals_or_null,
+                                 uint64_t key_hi, uint64_t key_lo, double init, double* out, int exec_mode, void* stream) {
+  if (!m || !inv_dev || !z_in || !out) return set_err(TS_EINVAL, "null argument");
+  OpArgs A = base_args(OP_STEPSEARCH);
+  A.z_in = z_in; A.z_out = out; A.inv = inv_dev; A.eps = init;
+  A.key_hi = key_hi; A.key_lo = key_lo; A.inj = normals_or_null;
+  return launch(m, 1, A, 1, (ts_exec_mode)exec_mode, (cudaStream_t)stream);
+}
+
+extern "C" int ts_run_chains(const ts_model* m, const ts_run_cfg* rc, const uint64_t* chain_keys_dev, int n_chains,
+                             const double* inv0_dev, const uint8_t* schedule_dev, const double* da_weight_dev,
+                             double* samples, double* stats, double* adapt, int32_t* status, int exec_mode, void* stream) {
+  if (!m || !rc || !chain_keys_dev || !inv0_dev || !samples || !stats || !adapt || !status)
+    return set_err(TS_EINVAL, "null argument");
+  int r = check_cfg(&rc->sampler);
+  if (r) return r;
+  if (n_chains < 1) return set_err(TS_EINVAL, "num_chains must be >= 1");
+  if (rc->num_samples < 1) return set_err(TS_EINVAL, "num_samples must be >= 1");
+  if (rc->num_warmup != 0 && rc->num_warmup < 20) return set_err(TS_EINVAL, "num_warmup must be 0 (off) or at least 20");
+  if (rc->num_warmup > 0 && (!schedule_dev || !da_weight_dev)) return set_err(TS_EINVAL, "warmup needs schedule and weights");
+  OpArgs A = base_args(OP_RUN);
+  A.inv = inv0_dev;
+  A.cfg = to_cfg(&rc->sampler);
+  A.rc.num_warmup = rc->num_warmup;
+  A.rc.num_samples = rc->num_samples;
+  A.rc.target_accept = rc->target_accept;
+  A.rc.base_step = rc->sampler.step_size;
+  A.rc.has_sampler = rc->has_sampler;
+  A.rc.sampler = A.cfg;
+  A.rc.schedule = schedule_dev;
+  A.rc.da_weight = da_weight_dev;
+  A.chain_keys = chain_keys_dev;
+  A.n_chains = n_chains;
+  A.samples = samples; A.stats = stats; A.adapt = adapt; A.status = status;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int nslots = rc->sampler.max_tree_depth - 1;
+  if (m->kind == TS_LOGISTIC) {
+    for (int c = 0; c < n_chains; ++c) {
+      A.n_points = c;
+      int e = launch(m, nslots, A, 1, TS_EXEC_BLOCK, st);
+      if (e) return e;
+    }
+    return TS_OK;
+  }
+  return launch(m, nslots, A, n_chains, (ts_exec_mode)exec_mode, st);
+}
+
+// ------------------------------------------------------------------ rng probe
+// Device streams for parity tests: kind 0 = random() doubles, 1 = standard
+// normals, 2 = fold(i) keys for i = 0..n-1 (hi, lo as raw bits in doubles).
+__global__ void k_rng_probe(uint64_t hi, uint64_t lo, int kind, int n, double* out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  Stream s;
+  s.init(Key{hi, lo});
+  for (int i = 0; i < n; ++i) {
+    if (kind == 0) out[i] = s.next_double();
+    else if (kind == 1) out[i] = s.normal();
+    else {
+      Key k = key_fold(Key{hi, lo}, (uint64_t)i);
+      out[2 * i] = __longlong_as_double((long long)k.hi);
+      out[2 * i + 1] = __longlong_as_double((long long)k.lo);
+    }
+  }
+}
+
+extern "C" int ts_rng_probe(uint64_t key_hi, uint64_t key_lo, int kind, int n, double* out_dev, void* stream) {
+  if (!out_dev || n < 0 || kind < 0 || kind > 2) return set_err(TS_EINVAL, "bad rng probe arguments");
+  k_rng_probe<<<1, 32, 0, (cudaStream_t)stream>>>(key_hi, key_lo, kind, n, out_dev);
+  TS_CUDA(cudaGetLastError());
+  return TS_OK;
+}

@@ -1,0 +1,631 @@
+// Device NUTS engine: leapfrog, iterative tree builder, doubling transition,
+// step-size search, warmup adaptation and the whole per-chain run loop.
+//
+// Every function restates a reference routine (file:line in turnstile/):
+//   leapfrog              integrator.py:90-103, kernels.py:148-165
+//   hamiltonian           integrator.py:82-87,  kernels.py:125-130
+//   build_tree            tree.py:344-453 (+ _merge 140-156, _logaddexp 131-137,
+//                         merge_out 395-400, _leaf_summary 262-280)
+//   transition            sampler.py:83-148 (biased progressive, outer U-turn)
+//   find_step_size        adapt.py:172-204
+//   dual averaging        adapt.py:28-70, Welford adapt.py:73-108,
+//   warmup driver         adapt.py:207-236, chains.py:98-163
+// Floating-point expressions keep the reference's association and use
+// explicit _rn intrinsics (the file is also compiled with -fmad=false), so
+// a ThreadTeam chain of a small model reproduces the reference bit for bit
+// up to the last-ulp behaviour of exp/log1p.
+#pragma once
+#include <math.h>
+#include <stdint.h>
+#include "ts_rng.cuh"
+#include "ts_team.cuh"
+
+namespace ts {
+
+enum Vid : int {
+  V_INV = 0, V_Q0, V_G0, V_R0,        // current state z0 (position, gradient), momentum
+  V_LQ, V_LR, V_LG,                   // trajectory left end (earliest in time)
+  V_RQ, V_RR, V_RG,                   // trajectory right end (latest in time)
+  V_PQ, V_PG,                         // transition proposal
+  V_RHO,                              // transition momentum sum
+  V_CQ, V_CR, V_CG, V_CUM,            // current leaf z_cur, running momentum prefix sum
+  V_FQ, V_FR, V_CUMF,                 // running subtree: first leaf and its prefix sum
+  V_TPQ, V_TPG,                       // running subtree proposal
+  V_MSUM,                             // tree momentum sum (output of build_tree)
+  V_WMEAN, V_WM2,                     // Welford accumulator
+  V_SLOT0                             // NodeStore slots: 5 vectors each
+};
+constexpr int kSlotVecs = 5;  // FQ, FR, CUMF, PQ, PG
+constexpr int kMaxSlots = 30;  // treemath.MAX_TREE_DEPTH_LIMIT
+__host__ __device__ inline int num_vecs(int nslots) { return V_SLOT0 + kSlotVecs * nslots; }
+__device__ __forceinline__ int slot_vec(int s, int k) { return V_SLOT0 + kSlotVecs * s + k; }
+
+enum Stop : int { kStopNone = 0, kStopTurn = 1, kStopDiv = 2 };
+
+// trace event kinds (int32 x5 per event: kind, a, b, c, e)
+enum TraceKind : int {
+  kEvWrite = 1,      // (n, slot, -)
+  kEvCheck = 2,      // (n, slot, stored leaf)
+  kEvTreeEnd = 3,    // (depth j, leapfrogs, stop*16 + go_right, max occupied slots)
+  kEvProposal = 4,   // (tree j, leaf index, accepted by outer step)
+  kEvOuter = 5,      // (j, turned, -)
+};
+
+struct TraceBuf {
+  int32_t* ev;      // [cap][5]
+  int cap;
+  double* leaf_lw;  // [lw_cap]
+  int lw_cap;
+  int32_t* counts;  // [0] = events written, [1] = leaf lws written, [2] = max occupied slots
+};
+
+struct SamplerCfg {
+  double step;
+  int max_depth;
+  int generalized;
+  double threshold;
+};
+
+struct SlotScalars {
+  double lw, metro, pU, pH, fU;
+  int count, pidx, leaf;
+};
+
+struct TreeOut {
+  double lw, sum_metro, pU, pH, fU;
+  int count, stop, pidx;
+};
+
+struct Stats {
+  int depth, leapfrogs, diverged;
+  double accept, energy;
+};
+
+__device__ __forceinline__ double kInf() { return __longlong_as_double(0x7ff0000000000000LL); }
+
+// tree._logaddexp (tree.py:131-137)
+__device__ __forceinline__ double logaddexp_inner(double a, double b) {
+  if (a == -kInf()) return b;
+  if (b == -kInf()) return a;
+  double hi = a, lo = b;
+  if (!(a >= b)) { hi = b; lo = a; }
+  return __dadd_rn(hi, log1p(exp(__dsub_rn(lo, hi))));
+}
+// numpy npy_logaddexp (used at sampler.py:129)
+__device__ __forceinline__ double logaddexp_np(double x, double y) {
+  if (x == y) return __dadd_rn(x, 0.693147180559945309417232121458176568);
+  const double tmp = __dsub_rn(x, y);
+  if (tmp > 0) return __dadd_rn(x, log1p(exp(-tmp)));
+  if (tmp <= 0) return __dadd_rn(y, log1p(exp(tmp)));
+  return tmp;
+}
+
+template <class Team, class Model>
+struct Engine {
+  Team T;
+  Model M;
+  VecStore S;
+  int D;
+  SamplerCfg cfg;
+  TraceBuf* tr;  // null unless tracing (leader writes)
+  int occupied_mask;
+
+  // replicated scalars
+  double U0;            // potential at z0
+  double cur_U;         // potential at z_cur
+  double LU, RU;        // potentials at the trajectory ends
+  double pU, pH;        // transition proposal potential / energy
+  int p_tree, p_leaf;   // transition proposal provenance (trace only)
+  // running subtree scalars
+  double r_lw, r_metro, r_pU, r_pH, r_fU;
+  int r_count, r_pidx;
+  SlotScalars ss[kMaxSlots];
+  unsigned long long n_evals;
+
+  __device__ __forceinline__ double* v(int id) const { return S.v(id); }
+  __device__ __forceinline__ int64_t ds() const { return S.dstride; }
+
+  // ---------------------------------------------------------------- trace
+  __device__ void ev(int kind, int a, int b, int c, int e = 0) {
+    if (tr == nullptr || !T.leader()) return;
+    int n = tr->counts[0];
+    if (n < tr->cap) {
+      int32_t* p = tr->ev + 5 * n;
+      p[0] = kind; p[1] = a; p[2] = b; p[3] = c; p[4] = e;
+    }
+    tr->counts[0] = n + 1;
+  }
+  __device__ void ev_lw(double lw) {
+    if (tr == nullptr || !T.leader()) return;
+    int n = tr->counts[1];
+    if (n < tr->lw_cap) tr->leaf_lw[n] = lw;
+    tr->counts[1] = n + 1;
+  }
+
+  // ------------------------------------------------------- vector helpers
+  __device__ __forceinline__ void copy(int dst, int src) {
+    double* a = v(dst);
+    const double* b = v(src);
+    const int64_t s = ds();
+    for (int d = T.rank(); d < D; d += T.size()) a[d * s] = b[d * s];
+  }
+  __device__ __forceinline__ void fill(int dst, double x) {
+    double* a = v(dst);
+    const int64_t s = ds();
+    for (int d = T.rank(); d < D; d += T.size()) a[d * s] = x;
+  }
+
+  // model evaluation at vector qid -> U (non-finite -> +inf), gradient -> gid
+  __device__ double eval(int qid, int gid) {
+    T.sync();
+    double u = M.eval(T, S, qid, gid);
+    T.sync();
+    n_evals += 1;
+    return isfinite(u) ? u : kInf();
+  }
+
+  // kinetic_energy_impl (kernels.py:125-130): sum 0.5 r r inv, left to right
+  __device__ double kinetic(int rid) {
+    const double* r = v(rid);
+    const double* inv = v(V_INV);
+    const int64_t s = ds();
+    double acc = 0.0;
+    for (int d = T.rank(); d < D; d += T.size()) {
+      const double x = r[d * s];
+      acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(__dmul_rn(0.5, x), x), inv[d * s]));
+    }
+    return T.sum(acc);
+  }
+  // hamiltonian (integrator.py:82-87)
+  __device__ double hamiltonian(double U, int rid) {
+    if (!isfinite(U)) return kInf();
+    const double h = __dadd_rn(U, kinetic(rid));
+    return isfinite(h) ? h : kInf();
+  }
+
+  // uturn_dots (kernels.py:132-139): (sum rho inv rl < 0) or (sum rho inv rr < 0)
+  __device__ bool uturn_dots(int rho_id, int rl_id, int rr_id) {
+    const double* rho = v(rho_id);
+    const double* inv = v(V_INV);
+    const double* rl = v(rl_id);
+    const double* rr = v(rr_id);
+    const int64_t s = ds();
+    double a = 0.0, b = 0.0;
+    for (int d = T.rank(); d < D; d += T.size()) {
+      const double w = __dmul_rn(rho[d * s], inv[d * s]);
+      a = __dadd_rn(a, __dmul_rn(w, rl[d * s]));
+      b = __dadd_rn(b, __dmul_rn(w, rr[d * s]));
+    }
+    T.sum2(a, b);
+    return a < 0.0 || b < 0.0;
+  }
+
+  // leapfrog on (CQ, CR, CG, cur_U) in place (integrator.py:90-103)
+  __device__ void leapfrog(double eps) {
+    const double half = __dmul_rn(0.5, eps);
+    double* q = v(V_CQ);
+    double* r = v(V_CR);
+    const double* g = v(V_CG);
+    const double* inv = v(V_INV);
+    const int64_t s = ds();
+    for (int d = T.rank(); d < D; d += T.size()) {
+      const double rh = __dsub_rn(r[d * s], __dmul_rn(half, g[d * s]));
+      r[d * s] = rh;
+      q[d * s] = __dadd_rn(q[d * s], __dmul_rn(eps, __dmul_rn(inv[d * s], rh)));
+    }
+    cur_U = eval(V_CQ, V_CG);
+    for (int d = T.rank(); d < D; d += T.size()) r[d * s] = __dsub_rn(r[d * s], __dmul_rn(half, g[d * s]));
+  }
+
+  // ------------------------------------------------------- tree builder
+  __device__ void running_from_leaf(int n, double lw, double metro, double h) {
+    copy(V_FQ, V_CQ); copy(V_FR, V_CR); copy(V_CUMF, V_CUM);
+    copy(V_TPQ, V_CQ); copy(V_TPG, V_CG);
+    r_lw = lw; r_metro = metro; r_count = 1; r_pU = cur_U; r_pH = h; r_pidx = n; r_fU = cur_U;
+  }
+
+  // running = _merge(summaries[s], running, u)   (tree.py:140-156)
+  __device__ void merge_slot(int s, double u) {
+    const SlotScalars& L = ss[s];
+    const double lw = logaddexp_inner(L.lw, r_lw);
+    const double p_right = (r_lw == -kInf()) ? 0.0 : exp(__dsub_rn(r_lw, lw));
+    if (!(u < p_right)) {
+      copy(V_TPQ, slot_vec(s, 3)); copy(V_TPG, slot_vec(s, 4));
+      r_pU = L.pU; r_pH = L.pH; r_pidx = L.pidx;
+    }
+    copy(V_FQ, slot_vec(s, 0)); copy(V_FR, slot_vec(s, 1)); copy(V_CUMF, slot_vec(s, 2));
+    r_fU = L.fU;
+    r_lw = lw;
+    r_count = L.count + r_count;
+    r_metro = __dadd_rn(L.metro, r_metro);
+  }
+
+  __device__ void merge_out(int start, Stream& draws) {
+    for (int s = start - 1; s >= 0; --s) merge_slot(s, draws.next_double());
+  }
+
+  // U-turn test of the running subtree (tree.py:436-446)
+  __device__ bool running_turning(bool forward) {
+    const int64_t s = ds();
+    if (cfg.generalized) {
+      // rho = (cum_last - cum_first) + first.r  -> V_MSUM as scratch
+      double* rho = v(V_MSUM);
+      const double* cum = v(V_CUM);
+      const double* cf = v(V_CUMF);
+      const double* fr = v(V_FR);
+      for (int d = T.rank(); d < D; d += T.size()) rho[d * s] = __dadd_rn(__dsub_rn(cum[d * s], cf[d * s]), fr[d * s]);
+      return uturn_dots(V_MSUM, V_FR, V_CR);
+    }
+    double* dq = v(V_MSUM);
+    const double* lq = v(V_CQ);
+    const double* fq = v(V_FQ);
+    if (forward) {
+      for (int d = T.rank(); d < D; d += T.size()) dq[d * s] = __dsub_rn(lq[d * s], fq[d * s]);
+      return uturn_dots(V_MSUM, V_FR, V_CR);
+    }
+    for (int d = T.rank(); d < D; d += T.size()) dq[d * s] = __dsub_rn(fq[d * s], lq[d * s]);
+    return uturn_dots(V_MSUM, V_CR, V_FR);
+  }
+
+  // leaf energy bookkeeping shared by both branches
+  __device__ void leaf_energy(double h_ref, double& h, double& delta) {
+    h = hamiltonian(cur_U, V_CR);
+    delta = __dsub_rn(h, h_ref);
+  }
+
+  __device__ void add_cum() {
+    double* c = v(V_CUM);
+    const double* r = v(V_CR);
+    const int64_t s = ds();
+    for (int d = T.rank(); d < D; d += T.size()) c[d * s] = __dadd_rn(c[d * s], r[d * s]);
+  }
+
+  // build_tree_iterative (tree.py:344-453).  Input: frontier in CQ/CR/CG/cur_U.
+  // Output: running subtree (FQ/FR/CUMF + TPQ/TPG + r_* scalars), last leaf in
+  // CQ/CR/CG/cur_U, momentum sum in V_MSUM.
+  __device__ TreeOut build_tree(int depth, double eps, double h_ref, Key key) {
+    Stream draws;
+    draws.init(key);
+    occupied_mask = 0;
+    fill(V_CUM, 0.0);
+    const double thr = cfg.threshold;
+    const bool forward = eps > 0;
+    int stop = kStopNone;
+    if (depth == 0) {
+      leapfrog(eps);
+      add_cum();
+      double h, delta;
+      leaf_energy(h_ref, h, delta);
+      const bool div = !isfinite(delta) || delta > thr;
+      const double lw = div ? -kInf() : -h;
+      const double metro = !isfinite(delta) ? 0.0 : (delta > 0 ? exp(-delta) : 1.0);
+      ev_lw(lw);
+      running_from_leaf(0, lw, metro, h);
+      stop = div ? kStopDiv : kStopNone;
+    } else {
+      const unsigned long long nleaves = 1ULL << depth;
+      for (unsigned long long n = 0; n < nleaves; ++n) {
+        leapfrog(eps);
+        add_cum();
+        double h, delta;
+        leaf_energy(h_ref, h, delta);
+        const int pc = __popcll(n);
+        if (!(isfinite(delta) && delta <= thr)) {
+          const double metro = isfinite(delta) ? exp(-delta) : 0.0;
+          ev_lw(-kInf());
+          running_from_leaf((int)n, -kInf(), metro, h);
+          merge_out(pc, draws);
+          stop = kStopDiv;
+          break;
+        }
+        const double lw = -h;
+        const double metro = delta > 0 ? exp(-delta) : 1.0;
+        ev_lw(lw);
+        if ((n & 1ULL) == 0) {
+          const int slot = pc;
+          copy(slot_vec(slot, 0), V_CQ); copy(slot_vec(slot, 1), V_CR); copy(slot_vec(slot, 2), V_CUM);
+          copy(slot_vec(slot, 3), V_CQ); copy(slot_vec(slot, 4), V_CG);
+          SlotScalars& L = ss[slot];
+          L.lw = lw; L.metro = metro; L.pU = cur_U; L.pH = h; L.fU = cur_U;
+          L.count = 1; L.pidx = (int)n; L.leaf = (int)n;
+          occupied_mask |= 1 << slot;
+          ev(kEvWrite, (int)n, slot, 0);
+        } else {
+          int slot = pc - 1;
+          const int i_min = slot - __popcll(((n + 1) & ~n) - 1) + 1;
+          running_from_leaf((int)n, lw, metro, h);
+          bool turned = false;
+          while (slot >= i_min) {
+            ev(kEvCheck, (int)n, slot, ss[slot].leaf);
+            merge_slot(slot, draws.next_double());
+            if (running_turning(forward)) {
+              merge_out(slot, draws);
+              turned = true;
+              break;
+            }
+            --slot;
+          }
+          if (turned) { stop = kStopTurn; break; }
+          // summaries[i_min] = running: first/cum_first already equal slot i_min's
+          copy(slot_vec(i_min, 3), V_TPQ); copy(slot_vec(i_min, 4), V_TPG);
+          SlotScalars& L = ss[i_min];
+          L.lw = r_lw; L.metro = r_metro; L.pU = r_pU; L.pH = r_pH; L.count = r_count; L.pidx = r_pidx;
+        }
+      }
+    }
+    // momentum_sum = (cum_last - cum_first) + first.r   (tree.py:283-294)
+    {
+      double* ms = v(V_MSUM);
+      const double* cum = v(V_CUM);
+      const double* cf = v(V_CUMF);
+      const double* fr = v(V_FR);
+      const int64_t s = ds();
+      for (int d = T.rank(); d < D; d += T.size()) ms[d * s] = __dadd_rn(__dsub_rn(cum[d * s], cf[d * s]), fr[d * s]);
+    }
+    if (tr != nullptr && T.leader()) tr->counts[2] = __popc(occupied_mask);
+    TreeOut o;
+    o.lw = r_lw; o.sum_metro = r_metro; o.pU = r_pU; o.pH = r_pH; o.fU = r_fU;
+    o.count = r_count; o.stop = stop; o.pidx = r_pidx;
+    return o;
+  }
+
+  // ------------------------------------------------------- transition
+  // Momentum refresh r0 = N(0,1) * momentum_std (sampler.py:95); normals from
+  // fold(key, 0) (or injected, std normal, component-major with stride inj_ds).
+  __device__ void draw_momentum(int rid, Key nkey, const double* inj, int64_t inj_ds) {
+    double* r = v(rid);
+    const double* inv = v(V_INV);
+    const int64_t s = ds();
+    if (inj != nullptr) {
+      for (int d = T.rank(); d < D; d += T.size())
+        r[d * s] = __dmul_rn(inj[d * inj_ds], __ddiv_rn(1.0, __dsqrt_rn(inv[d * s])));
+      return;
+    }
+    Stream ns;
+    ns.init(nkey);
+    for (int d = 0; d < D; ++d) {
+      const double z = ns.normal();
+      if ((d % T.size()) == T.rank()) r[d * s] = __dmul_rn(z, __ddiv_rn(1.0, __dsqrt_rn(inv[d * s])));
+    }
+  }
+
+  // nuts_transition_from (sampler.py:83-148): z0 = (Q0, G0, U0) -> proposal
+  __device__ Stats transition(Key key, const double* inj, int64_t inj_ds) {
+    draw_momentum(V_R0, key_fold(key, 0), inj, inj_ds);
+    const double h0 = hamiltonian(U0, V_R0);
+    Stream gen;
+    gen.init(key_fold(key, 1));
+    copy(V_LQ, V_Q0); copy(V_LR, V_R0); copy(V_LG, V_G0); LU = U0;
+    copy(V_RQ, V_Q0); copy(V_RR, V_R0); copy(V_RG, V_G0); RU = U0;
+    copy(V_PQ, V_Q0); copy(V_PG, V_G0); pU = U0; pH = h0; p_tree = -1; p_leaf = -1;
+    copy(V_RHO, V_R0);
+    double lw = -h0;
+    int leapfrogs = 0;
+    double sum_metro = 0.0;
+    bool diverged = false;
+    int depth_reached = 0;
+    for (int j = 0; j < cfg.max_depth; ++j) {
+      const bool go_right = gen.next_double() < 0.5;
+      const double eps = go_right ? cfg.step : -cfg.step;
+      if (go_right) { copy(V_CQ, V_RQ); copy(V_CR, V_RR); copy(V_CG, V_RG); cur_U = RU; }
+      else { copy(V_CQ, V_LQ); copy(V_CR, V_LR); copy(V_CG, V_LG); cur_U = LU; }
+      const TreeOut t = build_tree(j, eps, h0, key_fold(key, 2 + (uint64_t)j));
+      leapfrogs += t.count;
+      sum_metro = __dadd_rn(sum_metro, t.sum_metro);
+      ev(kEvTreeEnd, j, t.count, t.stop * 16 + (go_right ? 1 : 0), __popc(occupied_mask));
+      if (t.stop != kStopNone) {
+        diverged = diverged || (t.stop == kStopDiv);
+        depth_reached = j;
+        break;
+      }
+      const double u = gen.next_double();
+      const bool take = (t.lw >= lw) || (u < exp(__dsub_rn(t.lw, lw)));
+      if (take) {
+        copy(V_PQ, V_TPQ); copy(V_PG, V_TPG); pU = t.pU; pH = t.pH; p_tree = j; p_leaf = t.pidx;
+      }
+      ev(kEvProposal, j, t.pidx, take ? 1 : 0);
+      lw = logaddexp_np(lw, t.lw);
+      {
+        double* rho = v(V_RHO);
+        const double* ms = v(V_MSUM);
+        const int64_t s = ds();
+        for (int d = T.rank(); d < D; d += T.size()) rho[d * s] = __dadd_rn(rho[d * s], ms[d * s]);
+      }
+      if (go_right) { copy(V_RQ, V_CQ); copy(V_RR, V_CR); copy(V_RG, V_CG); RU = cur_U; }
+      else { copy(V_LQ, V_CQ); copy(V_LR, V_CR); copy(V_LG, V_CG); LU = cur_U; }
+      depth_reached = j + 1;
+      bool turned;
+      if (cfg.generalized) {
+        turned = uturn_dots(V_RHO, V_LR, V_RR);
+      } else {
+        double* dq = v(V_MSUM);
+        const double* rq = v(V_RQ);
+        const double* lq = v(V_LQ);
+        const int64_t s = ds();
+        for (int d = T.rank(); d < D; d += T.size()) dq[d * s] = __dsub_rn(rq[d * s], lq[d * s]);
+        turned = uturn_dots(V_MSUM, V_LR, V_RR);
+      }
+      ev(kEvOuter, j, turned ? 1 : 0, 0);
+      if (turned) break;
+    }
+    Stats st;
+    st.depth = depth_reached;
+    st.leapfrogs = leapfrogs;
+    st.diverged = diverged ? 1 : 0;
+    st.accept = leapfrogs ? __ddiv_rn(sum_metro, (double)leapfrogs) : 0.0;
+    st.energy = pH;
+    copy(V_Q0, V_PQ); copy(V_G0, V_PG); U0 = pU;
+    return st;
+  }
+
+  // ------------------------------------------------------- step-size search
+  __device__ double accept_prob(double h0, double eps) {
+    copy(V_CQ, V_Q0); copy(V_CR, V_R0); copy(V_CG, V_G0); cur_U = U0;
+    leapfrog(eps);
+    const double h1 = hamiltonian(cur_U, V_CR);
+    if (!isfinite(h1)) return 0.0;
+    const double x = __dsub_rn(h0, h1);
+    return exp(x < 0.0 ? x : 0.0);
+  }
+  // find_reasonable_step_size (adapt.py:172-204); z0 in Q0/G0/U0
+  __device__ double find_step_size(Key key, double init, const double* inj, int64_t inj_ds) {
+    const double target = 0.5;
+    // rng.generator() of the given key directly (not a fold)
+    {
+      double* r = v(V_R0);
+      const double* inv = v(V_INV);
+      const int64_t s = ds();
+      if (inj != nullptr) {
+        for (int d = T.rank(); d < D; d += T.size())
+          r[d * s] = __dmul_rn(inj[d * inj_ds], __ddiv_rn(1.0, __dsqrt_rn(inv[d * s])));
+      } else {
+        Stream ns;
+        ns.init(key);
+        for (int d = 0; d < D; ++d) {
+          const double z = ns.normal();
+          if ((d % T.size()) == T.rank()) r[d * s] = __dmul_rn(z, __ddiv_rn(1.0, __dsqrt_rn(inv[d * s])));
+        }
+      }
+    }
+    const double h0 = hamiltonian(U0, V_R0);
+    double eps = init;
+    const int direction = accept_prob(h0, eps) > target ? 1 : -1;
+    for (int it = 0; it < 64; ++it) {
+      const double eps_next = __dmul_rn(eps, direction == 1 ? 2.0 : 0.5);
+      if (!(1e-10 < eps_next && eps_next < 1e7)) break;
+      const double prob = accept_prob(h0, eps_next);
+      if ((direction == 1 && prob <= target) || (direction == -1 && prob > target))
+        return direction == -1 ? eps_next : eps;
+      eps = eps_next;
+    }
+    return eps;
+  }
+};
+
+// ------------------------------------------------------------------- run
+struct RunCfg {
+  int num_warmup;
+  int num_samples;
+  double target_accept;
+  double base_step;
+  int has_sampler;  // RunConfig.sampler is not None (chains.py:137-143)
+  SamplerCfg sampler;
+  const uint8_t* schedule;    // [W]: bit0 in a covariance window, bit1 window end
+  const double* da_weight;    // [W]: t ** -kappa for t = 1..W
+};
+
+struct RunOut {
+  double* samples;   // [S][D] for this chain (component stride ds_out)
+  int64_t s_stride;  // stride between draws
+  int64_t d_stride;  // stride between components
+  double* stats;     // [(W+S)][5]
+  double* adapt;     // [2 + W + D]: eps0, final step, step trace, inv mass
+  int32_t* status;   // 0 ok, 1 invalid mass matrix install
+};
+
+// run_chain (chains.py:98-163) for the chain owning key `ck`.
+template <class Team, class Model>
+__device__ void run_chain(Engine<Team, Model>& E, Key ck, const RunCfg& rc, const RunOut& out, bool writer) {
+  const int D = E.D;
+  const int W = rc.num_warmup, S = rc.num_samples;
+  const int64_t s = E.ds();
+  // q0 ~ U(-2, 2)^D from fold(0) (chains.py:107)
+  {
+    Stream us;
+    us.init(key_fold(ck, 0));
+    double* q = E.v(V_Q0);
+    for (int d = 0; d < D; ++d) {
+      const double u = us.next_double();
+      if ((d % E.T.size()) == E.T.rank()) q[d * s] = __dadd_rn(-2.0, __dmul_rn(4.0, u));
+    }
+  }
+  E.U0 = E.eval(V_Q0, V_G0);
+  int status = 0;
+  double step;
+  if (W > 0) {
+    const double eps0 = E.find_step_size(key_fold(ck, 1), rc.base_step, nullptr, 0);
+    if (writer && E.T.leader()) out.adapt[0] = eps0;
+    // DualAveragingState.init (adapt.py:44-50)
+    const double mu = log(__dmul_rn(10.0, eps0));
+    double log_eps = log(eps0), log_eps_bar = 0.0, h_bar = 0.0;
+    const double gamma = 0.05, t0 = 10.0, delta = rc.target_accept;
+    int wcount = 0;
+    E.fill(V_WMEAN, 0.0);
+    E.fill(V_WM2, 0.0);
+    for (int i = 0; i < W; ++i) {
+      E.cfg.step = exp(log_eps);
+      if (writer && E.T.leader()) out.adapt[2 + i] = E.cfg.step;
+      const Stats st = E.transition(key_fold(ck, 10 + (uint64_t)i), nullptr, 0);
+      if (writer && E.T.leader()) {
+        double* o = out.stats + (int64_t)i * 5;
+        o[0] = st.depth; o[1] = st.leapfrogs; o[2] = st.diverged; o[3] = st.accept; o[4] = st.energy;
+      }
+      // da_update (adapt.py:60-70) with the clipped acceptance (adapt.py:227)
+      {
+        const double a = fmin(1.0, fmax(0.0, st.accept));
+        const int t = i + 1;
+        const double frac = __ddiv_rn(1.0, __dadd_rn((double)t, t0));
+        h_bar = __dadd_rn(__dmul_rn(__dsub_rn(1.0, frac), h_bar), __dmul_rn(frac, __dsub_rn(delta, a)));
+        log_eps = __dsub_rn(mu, __dmul_rn(__ddiv_rn(__dsqrt_rn((double)t), gamma), h_bar));
+        const double w = rc.da_weight[i];
+        log_eps_bar = __dadd_rn(__dmul_rn(w, log_eps), __dmul_rn(__dsub_rn(1.0, w), log_eps_bar));
+      }
+      const uint8_t flag = rc.schedule[i];
+      if (flag & 1) {  // welford_update (adapt.py:86-94)
+        wcount += 1;
+        double* mean = E.v(V_WMEAN);
+        double* m2 = E.v(V_WM2);
+        const double* x = E.v(V_Q0);
+        for (int d = E.T.rank(); d < D; d += E.T.size()) {
+          const double dl = __dsub_rn(x[d * s], mean[d * s]);
+          const double nm = __dadd_rn(mean[d * s], __ddiv_rn(dl, (double)wcount));
+          mean[d * s] = nm;
+          m2[d * s] = __dadd_rn(m2[d * s], __dmul_rn(dl, __dsub_rn(x[d * s], nm)));
+        }
+      }
+      if ((flag & 2) && wcount >= 2) {  // install regularized variance (adapt.py:104-108, 228-232)
+        double* inv = E.v(V_INV);
+        double* mean = E.v(V_WMEAN);
+        double* m2 = E.v(V_WM2);
+        const double n = (double)wcount;
+        double bad = 0.0;
+        for (int d = E.T.rank(); d < D; d += E.T.size()) {
+          const double var = __ddiv_rn(m2[d * s], (double)(wcount - 1));
+          const double nv = __dadd_rn(__dmul_rn(__ddiv_rn(n, __dadd_rn(n, 5.0)), var),
+                                      __dmul_rn(__ddiv_rn(5.0, __dadd_rn(n, 5.0)), 1e-3));
+          if (!(isfinite(nv) && nv > 0.0)) bad = 1.0;
+          inv[d * s] = nv;
+          mean[d * s] = 0.0;
+          m2[d * s] = 0.0;
+        }
+        wcount = 0;
+        if (E.T.sum(bad) != 0.0) { status = 1; break; }
+      }
+    }
+    step = exp(log_eps_bar);
+  } else {
+    step = rc.base_step;
+    if (!rc.has_sampler) step = E.find_step_size(key_fold(ck, 1), 1.0, nullptr, 0);
+    if (writer && E.T.leader()) out.adapt[0] = step;
+  }
+  if (writer && E.T.leader()) { out.adapt[1] = step; out.status[0] = status; }
+  if (status != 0) return;
+  E.cfg.step = step;
+  for (int i = 0; i < S; ++i) {
+    const Stats st = E.transition(key_fold(ck, 10 + (uint64_t)(W + i)), nullptr, 0);
+    if (writer) {
+      const double* q = E.v(V_Q0);
+      for (int d = E.T.rank(); d < D; d += E.T.size()) out.samples[(int64_t)i * out.s_stride + d * out.d_stride] = q[d * s];
+      if (E.T.leader()) {
+        double* o = out.stats + (int64_t)(W + i) * 5;
+        o[0] = st.depth; o[1] = st.leapfrogs; o[2] = st.diverged; o[3] = st.accept; o[4] = st.energy;
+      }
+    }
+  }
+  if (writer) {
+    const double* inv = E.v(V_INV);
+    for (int d = E.T.rank(); d < D; d += E.T.size()) out.adapt[2 + W + d] = inv[d * s];
+  }
+}
+
+}  // namespace ts

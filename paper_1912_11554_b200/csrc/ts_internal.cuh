@@ -1,0 +1,233 @@
+// Internal declarations shared by the translation units of the engine.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+#include <string>
+#include <type_traits>
+
+#include "ts_engine.cuh"
+#include "ts_logistic.cuh"
+#include "ts_models.cuh"
+#include "../../include/turnstile_b200.h"
+
+// Device model handle behind the opaque ts_model of the C ABI.
+struct ts_model {
+  int kind;
+  int dim;
+  int device;
+  double* params;  // device
+  int n_params;
+  // logistic
+  float* xt;
+  uint8_t* yt;
+  int64_t n_rows;
+  int p;
+  int64_t ntiles;
+  double* pbuf;
+  unsigned long long* bar;
+  int fp64;
+  int grid;
+  int pmax;
+};
+
+namespace ts_internal {
+using namespace ts;
+
+int set_err(int code, const char* msg);
+
+
+// ------------------------------------------------------------------ op args
+enum OpCode : int { OP_POTGRAD = 0, OP_LEAPFROG = 1, OP_TREE = 2, OP_TRANSITION = 3, OP_STEPSEARCH = 4, OP_RUN = 5, OP_EVALBENCH = 6 };
+
+struct OpArgs {
+  int op;
+  const double* z_in;
+  double* z_out;
+  const double* inv;
+  SamplerCfg cfg;
+  int depth;
+  double eps;
+  double h_ref;
+  uint64_t key_hi, key_lo;
+  const double* inj;
+  TraceBuf trace;
+  int has_trace;
+  int n_points;
+  // run
+  RunCfg rc;
+  const uint64_t* chain_keys;  // [C][2]
+  int n_chains;
+  double* samples;  // [C][S][D]
+  double* stats;    // [C][W+S][5]
+  double* adapt;    // [C][2+W+D]
+  int32_t* status;  // [C]
+};
+
+struct SmallW {
+  SmallModel m;
+  template <class Team>
+  __device__ double eval(const Team& T, const VecStore& S, int q, int g) { return small_model_eval(T, m, S, q, g); }
+};
+
+struct LogisticW {
+  LogisticArgs a;
+  double* wred;
+  double* red_s;
+  unsigned long long epoch;
+  __device__ double eval(const BlockTeam& T, const VecStore& S, int q, int g) {
+    return logistic_eval_grid(T, a, S, q, g, wred, red_s, epoch);
+  }
+};
+
+// Run one parity/production op for the engine E (vectors already allocated).
+template <class Team, class Model>
+__device__ void do_op(Engine<Team, Model>& E, const OpArgs& A, int chain, bool writer) {
+  const int D = E.D;
+  const int64_t s = E.ds();
+  const int rk = E.T.rank(), sz = E.T.size();
+  // mass matrix
+  {
+    double* inv = E.v(V_INV);
+    for (int d = rk; d < D; d += sz) inv[d * s] = A.inv[d];
+  }
+  E.tr = (A.has_trace && writer) ? const_cast<TraceBuf*>(&A.trace) : nullptr;
+  E.n_evals = 0;
+  E.cfg = A.cfg;
+  switch (A.op) {
+    case OP_POTGRAD: {
+      for (int k = 0; k < A.n_points; ++k) {
+        double* q = E.v(V_CQ);
+        for (int d = rk; d < D; d += sz) q[d * s] = A.z_in[(int64_t)k * D + d];
+        E.T.sync();
+        const double u = E.M.eval(E.T, E.S, V_CQ, V_CG);
+        E.T.sync();
+        if (writer) {
+          const double* g = E.v(V_CG);
+          double* o = A.z_out + (int64_t)k * (D + 1);
+          if (E.T.leader()) o[0] = u;
+          for (int d = rk; d < D; d += sz) o[1 + d] = g[d * s];
+        }
+      }
+      break;
+    }
+    case OP_EVALBENCH: {
+      double* q = E.v(V_CQ);
+      for (int d = rk; d < D; d += sz) q[d * s] = A.z_in[d];
+      double u = 0.0;
+      for (int k = 0; k < A.n_points; ++k) u = E.eval(V_CQ, V_CG);
+      if (writer && E.T.leader()) A.z_out[0] = u;
+      break;
+    }
+    case OP_LEAPFROG: {
+      double* q = E.v(V_CQ); double* r = E.v(V_CR); double* g = E.v(V_CG);
+      for (int d = rk; d < D; d += sz) { q[d * s] = A.z_in[d]; r[d * s] = A.z_in[D + d]; g[d * s] = A.z_in[2 * D + d]; }
+      E.cur_U = A.z_in[3 * D];
+      E.leapfrog(A.eps);
+      if (writer) {
+        for (int d = rk; d < D; d += sz) { A.z_out[d] = q[d * s]; A.z_out[D + d] = r[d * s]; A.z_out[2 * D + d] = g[d * s]; }
+        if (E.T.leader()) A.z_out[3 * D] = E.cur_U;
+      }
+      break;
+    }
+    case OP_TREE: {
+      double* q = E.v(V_CQ); double* r = E.v(V_CR); double* g = E.v(V_CG);
+      for (int d = rk; d < D; d += sz) { q[d * s] = A.z_in[d]; r[d * s] = A.z_in[D + d]; g[d * s] = A.z_in[2 * D + d]; }
+      E.cur_U = A.z_in[3 * D];
+      double h_ref = A.h_ref;
+      const TreeOut t = E.build_tree(A.depth, A.eps, h_ref, Key{A.key_hi, A.key_lo});
+      if (writer) {
+        const int ids[8] = {V_FQ, V_FR, V_CQ, V_CR, V_CG, V_TPQ, V_TPG, V_MSUM};
+        for (int k = 0; k < 8; ++k) {
+          const double* vv = E.v(ids[k]);
+          for (int d = rk; d < D; d += sz) A.z_out[(int64_t)k * D + d] = vv[d * s];
+        }
+        if (E.T.leader()) {
+          double* o = A.z_out + 8 * (int64_t)D;
+          o[0] = t.lw; o[1] = t.sum_metro; o[2] = t.count; o[3] = t.stop == kStopTurn; o[4] = t.stop == kStopDiv;
+          o[5] = t.pU; o[6] = t.pH; o[7] = t.pidx; o[8] = t.fU; o[9] = E.cur_U;
+        }
+      }
+      break;
+    }
+    case OP_TRANSITION: {
+      double* q = E.v(V_Q0); double* g = E.v(V_G0);
+      for (int d = rk; d < D; d += sz) { q[d * s] = A.z_in[d]; g[d * s] = A.z_in[2 * D + d]; }
+      E.U0 = A.z_in[3 * D];
+      const Stats st = E.transition(Key{A.key_hi, A.key_lo}, A.inj, 1);
+      if (writer) {
+        for (int d = rk; d < D; d += sz) { A.z_out[d] = q[d * s]; A.z_out[D + d] = g[d * s]; }
+        if (E.T.leader()) {
+          double* o = A.z_out + 2 * (int64_t)D;
+          o[0] = E.U0; o[1] = st.depth; o[2] = st.leapfrogs; o[3] = st.diverged; o[4] = st.accept; o[5] = st.energy;
+          o[6] = E.p_tree; o[7] = E.p_leaf;
+        }
+      }
+      break;
+    }
+    case OP_STEPSEARCH: {
+      double* q = E.v(V_Q0); double* g = E.v(V_G0);
+      for (int d = rk; d < D; d += sz) { q[d * s] = A.z_in[d]; g[d * s] = A.z_in[2 * D + d]; }
+      E.U0 = A.z_in[3 * D];
+      const double eps = E.find_step_size(Key{A.key_hi, A.key_lo}, A.eps, A.inj, 1);
+      if (writer && E.T.leader()) A.z_out[0] = eps;
+      break;
+    }
+    case OP_RUN: {
+      const int W = A.rc.num_warmup, S = A.rc.num_samples;
+      RunOut ro;
+      ro.samples = A.samples + (int64_t)chain * S * D;
+      ro.s_stride = D;
+      ro.d_stride = 1;
+      ro.stats = A.stats + (int64_t)chain * (W + S) * 5;
+      ro.adapt = A.adapt + (int64_t)chain * (2 + W + D);
+      ro.status = A.status + chain;
+      const Key ck{A.chain_keys[2 * chain], A.chain_keys[2 * chain + 1]};
+      run_chain(E, ck, A.rc, ro, writer);
+      break;
+    }
+  }
+}
+
+// BlockTeam: vectors in shared memory.  smem = vecs | team scratch(64) | model scratch
+template <class MW>
+__global__ void __launch_bounds__(256, 1) k_block_op(MW mw, int D, int nslots, int model_scratch, OpArgs A) {
+  extern __shared__ double smem[];
+  const int nv = num_vecs(nslots);
+  Engine<BlockTeam, MW> E;
+  E.T.scratch = smem + (int64_t)nv * D;
+  E.M = mw;
+  E.D = D;
+  E.S.base = smem;
+  E.S.vstride = D;
+  E.S.dstride = 1;
+  if constexpr (!std::is_same<MW, SmallW>::value) {
+    E.M.wred = smem + (int64_t)nv * D + 64;
+    E.M.red_s = E.M.wred + model_scratch;
+    E.M.epoch = 0;
+  }
+  const bool writer = blockIdx.x == 0;
+  if (A.op == OP_RUN) {
+    // one chain per launch in grid mode; chain index passed via n_points
+    do_op(E, A, A.n_points, writer);
+  } else {
+    do_op(E, A, 0, writer);
+  }
+}
+
+
+int launch_thread(const SmallModel& sm, int D, int C, int nslots, OpArgs& A, cudaStream_t st);
+int launch_block_small(const SmallModel& sm, int D, int nslots, OpArgs& A, cudaStream_t st);
+int launch_block_logistic(const ts_model* m, int nslots, OpArgs& A, cudaStream_t st);
+
+}  // namespace ts_internal
+
+#define TS_CUDA(call)                                                              \
+  do {                                                                             \
+    cudaError_t e_ = (call);                                                       \
+    if (e_ != cudaSuccess) {                                                       \
+      char b_[512];                                                                \
+      snprintf(b_, sizeof b_, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__); \
+      return ts_internal::set_err(TS_ECUDA, b_);                                   \
+    }                                                                              \
+  } while (0)

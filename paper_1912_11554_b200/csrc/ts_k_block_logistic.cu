@@ -1,0 +1,40 @@
+// BlockTeam kernel for the logistic model: cooperative persistent grid.
+#include <stdio.h>
+#include "ts_internal.cuh"
+
+namespace ts_internal {
+
+int launch_block_logistic(const ts_model* m, int nslots, OpArgs& A, cudaStream_t st) {
+  const int PMAX = m->pmax;
+  LogisticW mw;
+  mw.a.xt = m->xt; mw.a.yt = m->yt; mw.a.n_rows = m->n_rows; mw.a.p = m->p; mw.a.ntiles = m->ntiles;
+  mw.a.pbuf = m->pbuf; mw.a.bar = m->bar; mw.a.fp64 = m->fp64; mw.a.pmax = m->pmax;
+  mw.wred = nullptr; mw.red_s = nullptr; mw.epoch = 0;
+  const int threads = 256;
+  const int nwarps = threads / 32;
+  int scratch = nwarps * (PMAX + 2);
+  if (scratch < threads) scratch = threads;
+  if (scratch < m->p + 2) scratch = m->p + 2;
+  const int D = m->dim;
+  const size_t smem = ((size_t)num_vecs(nslots) * D + 64 + scratch + (m->p + 2)) * sizeof(double);
+  auto kern = k_block_op<LogisticW>;
+  TS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int occ = 0;
+  TS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem));
+  if (occ < 1) return set_err(TS_EUNSUPPORTED, "logistic kernel cannot be resident (shared memory / registers)");
+  int dev = 0, nsm = 0;
+  TS_CUDA(cudaGetDevice(&dev));
+  TS_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  int64_t grid = (int64_t)nsm * occ;
+  if (m->grid > 0 && m->grid < grid) grid = m->grid;
+  if (grid > m->ntiles) grid = m->ntiles;
+  if (grid < 1) grid = 1;
+  TS_CUDA(cudaMemsetAsync(m->bar, 0, sizeof(unsigned long long), st));
+  int Dv = D, ns = nslots, sc = scratch;
+  void* args[] = {&mw, &Dv, &ns, &sc, &A};
+  TS_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3((unsigned)grid), dim3(threads), args, smem, st));
+  return TS_OK;
+}
+
+
+}  // namespace ts_internal

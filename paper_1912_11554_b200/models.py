@@ -1,0 +1,308 @@
+"""Target densities, executed on the device.
+
+Reference: turnstile/models.py.  ``TargetModel`` keeps the reference's
+fields (name, dim, potential, gradient, params) so code written against the
+reference plugin API still reads the same.  Built-in constructors return
+models whose ``potential``/``gradient`` callables evaluate on the GPU through
+``ts_potential_grad`` and which carry a ``device_spec`` describing the
+device-resident data (the reference hides X and y in closures,
+models.py:107-118; here they are uploaded once and re-tiled in HBM).
+
+A ``TargetModel`` built from arbitrary Python callables has no device
+counterpart: the samplers reject it with ``ValueError`` (there is no CPU
+fallback, BASELINE.json north star).
+"""
+
+from __future__ import annotations
+
+import csv
+import json
+from dataclasses import dataclass, field
+from pathlib import Path
+from typing import Callable, Optional
+
+import numpy as np
+
+from . import _lib
+
+PRECISIONS = ("fp64", "fp32")
+
+
+class DeviceSpec:
+    """Device description of a built-in model; owns per-GPU ts_model handles."""
+
+    def __init__(self, kind: int, dim: int, params=None, x=None, y=None, precision: str = "fp64"):
+        if precision not in PRECISIONS:
+            raise ValueError(f"precision must be one of {PRECISIONS}")
+        self.kind = kind
+        self.dim = dim
+        self.params = None if params is None else np.ascontiguousarray(params, dtype=np.float64)
+        self.x = x  # fp32 (N, p) C-contiguous, logistic only
+        self.y = y  # uint8 (N,)
+        self.precision = precision
+        self._handles: dict = {}
+        self._grid = 0
+
+    def handle(self, device=None):
+        """ts_model* for the given CUDA device (created on first use)."""
+        torch = _lib.torch_cuda()
+        dev = _lib.cuda_device(torch, device)
+        key = dev.index
+        h = self._handles.get(key)
+        if h is not None:
+            return h
+        lib = _lib.load_library()
+        out = _lib._P()
+        with torch.cuda.device(dev):
+            xd = yd = None
+            n_rows = n_feat = 0
+            if self.kind == _lib.TS_LOGISTIC:
+                xd = torch.from_numpy(self.x).to(dev)
+                yd = torch.from_numpy(self.y).to(dev)
+                n_rows, n_feat = self.x.shape
+            params = self.params
+            pp = params.ctypes.data if params is not None else 0
+            npar = 0 if params is None else params.size
+            prec = _lib.TS_PREC_FP64 if self.precision == "fp64" else _lib.TS_PREC_FP32
+            _lib.check(lib.ts_model_create(self.kind, self.dim, pp, npar, _lib.ptr(xd), _lib.ptr(yd), n_rows, n_feat, prec,
+                                           ctypes_byref(out)))
+            if self._grid:
+                _lib.check(lib.ts_model_set_grid(out, self._grid))
+            torch.cuda.synchronize(dev)
+        self._handles[key] = out
+        return out
+
+    def set_grid(self, grid: int) -> None:
+        """Cap the persistent grid size (testing / multi-tenant use)."""
+        self._grid = int(grid)
+        lib = _lib.load_library()
+        for h in self._handles.values():
+            _lib.check(lib.ts_model_set_grid(h, self._grid))
+
+    def __del__(self):
+        try:
+            lib = _lib._lib
+            if lib is not None:
+                for h in self._handles.values():
+                    lib.ts_model_destroy(h)
+        except Exception:  # pragma: no cover - interpreter shutdown
+            pass
+
+
+def ctypes_byref(x):
+    import ctypes
+
+    return ctypes.byref(x)
+
+
+def potential_and_gradient(spec: DeviceSpec, qs: np.ndarray, device=None) -> np.ndarray:
+    """Fused U and gradient at each row of ``qs`` -> array (n, 1 + dim)."""
+    torch = _lib.torch_cuda()
+    qs = np.atleast_2d(np.asarray(qs, dtype=np.float64))
+    if qs.shape[1] != spec.dim:
+        raise ValueError(f"expected parameter vector of length {spec.dim}, got {qs.shape[1]}")
+    h = spec.handle(device)
+    dev = _lib.cuda_device(torch, device)
+    qd = torch.from_numpy(np.ascontiguousarray(qs)).to(dev)
+    out = torch.empty((qs.shape[0], spec.dim + 1), dtype=torch.float64, device=dev)
+    lib = _lib.load_library()
+    with torch.cuda.device(dev):
+        _lib.check(lib.ts_potential_grad(h, _lib.ptr(qd), qs.shape[0], _lib.ptr(out), _lib.stream_ptr(torch)))
+    return out.cpu().numpy()
+
+
+@dataclass(frozen=True)
+class TargetModel:
+    """A target distribution seen through its potential energy surface."""
+
+    name: str
+    dim: int
+    potential: Callable[[np.ndarray], float]
+    gradient: Callable[[np.ndarray], np.ndarray]
+    params: dict = field(default_factory=dict)
+    device_spec: Optional[DeviceSpec] = field(default=None, compare=False, repr=False)
+
+    def __post_init__(self):
+        if self.dim < 1:
+            raise ValueError("model dimension must be positive")
+
+    def descriptor(self) -> dict:
+        return {"model": self.name, "params": self.params}
+
+
+def require_device(model: TargetModel) -> DeviceSpec:
+    if model.device_spec is None:
+        raise ValueError(
+            f"model {model.name!r} has no device implementation; only the built-in models "
+            f"{BUILTIN_MODELS} run on the B200 path (no CPU fallback)"
+        )
+    return model.device_spec
+
+
+def _device_model(name: str, spec: DeviceSpec, params: dict) -> TargetModel:
+    dim = spec.dim
+
+    def potential(q: np.ndarray) -> float:
+        return float(potential_and_gradient(spec, np.asarray(q, dtype=np.float64).reshape(1, -1))[0, 0])
+
+    def gradient(q: np.ndarray) -> np.ndarray:
+        return potential_and_gradient(spec, np.asarray(q, dtype=np.float64).reshape(1, -1))[0, 1:].copy()
+
+    return TargetModel(name, dim, potential, gradient, params, spec)
+
+
+@dataclass(frozen=True)
+class LogisticRegressionData:
+    """Covariates and binary labels (models.py:43-64).
+
+    The device streams X in fp32: values are rounded to fp32 once here (the
+    benchmark data are generated fp32-exact, so nothing changes for them).
+    """
+
+    x: np.ndarray
+    y: np.ndarray
+
+    def __post_init__(self):
+        x = np.atleast_2d(np.asarray(self.x, dtype=np.float64))
+        y = np.asarray(self.y, dtype=np.float64).ravel()
+        if x.shape[0] != y.shape[0]:
+            raise ValueError("covariate rows and labels disagree in length")
+        if not np.isfinite(x).all() or not np.isfinite(y).all():
+            raise ValueError("logistic data must be free of NaN/Inf")
+        if not np.isin(y, (0.0, 1.0)).all():
+            raise ValueError("labels must be 0 or 1")
+        object.__setattr__(self, "x", np.ascontiguousarray(x))
+        object.__setattr__(self, "y", np.ascontiguousarray(y))
+
+    @property
+    def num_features(self) -> int:
+        return self.x.shape[1]
+
+
+def std_normal_model(dim: int) -> TargetModel:
+    if dim < 1:
+        raise ValueError("dim must be >= 1")
+    return _device_model("std_normal", DeviceSpec(_lib.TS_STD_NORMAL, dim), {"dim": dim})
+
+
+def gaussian_model(cov_diag) -> TargetModel:
+    var = np.asarray(cov_diag, dtype=np.float64).ravel()
+    if var.size < 1:
+        raise ValueError("cov_diag must be non-empty")
+    if not (np.isfinite(var).all() and (var > 0).all()):
+        raise ValueError("variances must be positive and finite")
+    inv_var = np.ascontiguousarray(1.0 / var)
+    return _device_model("gaussian", DeviceSpec(_lib.TS_GAUSSIAN, var.size, params=inv_var), {"cov_diag": var.tolist()})
+
+
+def logistic_regression_model(data: LogisticRegressionData, precision: str = "fp64") -> TargetModel:
+    """Bayesian logistic regression with unit-normal priors (models.py:101-126).
+
+    ``precision`` selects the arithmetic of the fused data pass:
+    ``"fp64"`` (parity mode, differs from the reference only in summation
+    order) or ``"fp32"`` (per-row math in float, accumulation in double).
+    """
+    x32 = np.ascontiguousarray(data.x, dtype=np.float32)
+    y8 = np.ascontiguousarray(data.y, dtype=np.uint8)
+    dim = data.num_features + 1
+    spec = DeviceSpec(_lib.TS_LOGISTIC, dim, x=x32, y=y8, precision=precision)
+    return _device_model(
+        "logistic_regression",
+        spec,
+        {"num_data": int(x32.shape[0]), "num_features": int(x32.shape[1])},
+    )
+
+
+def funnel_model(dim: int = 10) -> TargetModel:
+    if dim < 2:
+        raise ValueError("funnel needs the scale coordinate plus at least one other")
+    return _device_model("funnel", DeviceSpec(_lib.TS_FUNNEL, dim), {"dim": dim})
+
+
+EIGHT_SCHOOLS_Y = (28.0, 8.0, -3.0, 7.0, -1.0, 1.0, 18.0, 12.0)
+EIGHT_SCHOOLS_SIGMA = (15.0, 10.0, 16.0, 11.0, 9.0, 11.0, 10.0, 18.0)
+
+
+def eight_schools_model(y=EIGHT_SCHOOLS_Y, sigma=EIGHT_SCHOOLS_SIGMA) -> TargetModel:
+    """Non-centred eight schools: q = (mu, log tau, theta~_1..J).
+
+    U = mu^2/50 + log1p((tau/5)^2) - log tau + sum_j [th_j^2/2 + ((y_j - mu - tau th_j)/sigma_j)^2/2]
+    (mu ~ N(0, 5^2), tau ~ HalfCauchy(5), theta~ ~ N(0, 1)).
+    """
+    y = np.asarray(y, dtype=np.float64).ravel()
+    s = np.asarray(sigma, dtype=np.float64).ravel()
+    if y.size != s.size or y.size < 1:
+        raise ValueError("y and sigma must be non-empty and of equal length")
+    if not (np.isfinite(s).all() and (s > 0).all()):
+        raise ValueError("sigma must be positive and finite")
+    spec = DeviceSpec(_lib.TS_EIGHT_SCHOOLS, y.size + 2, params=np.concatenate([y, s]))
+    return _device_model("eight_schools", spec, {"y": y.tolist(), "sigma": s.tolist()})
+
+
+def fd_gradient(model: TargetModel, q: np.ndarray, h: float = 1e-5) -> np.ndarray:
+    """Central-difference gradient oracle (models.py:147-160)."""
+    if h <= 0:
+        raise ValueError("step h must be positive")
+    q = np.asarray(q, dtype=np.float64)
+    out = np.empty_like(q)
+    for i in range(q.size):
+        bumped = q.copy()
+        bumped[i] = q[i] + h
+        up = model.potential(bumped)
+        bumped[i] = q[i] - h
+        down = model.potential(bumped)
+        out[i] = (up - down) / (2.0 * h)
+    return out
+
+
+def load_logistic_csv(path) -> LogisticRegressionData:
+    rows = []
+    with open(path, newline="") as fh:
+        reader = csv.reader(fh)
+        header = next(reader, None)
+        if header is None:
+            raise ValueError(f"{path}: empty CSV")
+        for row in reader:
+            if row:
+                rows.append([float(v) for v in row])
+    if not rows:
+        raise ValueError(f"{path}: no data rows")
+    mat = np.asarray(rows, dtype=np.float64)
+    return LogisticRegressionData(mat[:, :-1], mat[:, -1])
+
+
+def model_from_descriptor(descriptor, base_dir=None) -> TargetModel:
+    """Build a model from a JSON descriptor (models.py:180-215)."""
+    if isinstance(descriptor, (str, Path)):
+        p = Path(descriptor)
+        if p.exists():
+            desc = json.loads(p.read_text())
+            base_dir = p.parent if base_dir is None else base_dir
+        else:
+            desc = json.loads(str(descriptor))
+    else:
+        desc = dict(descriptor)
+    name = desc.get("model")
+    params = dict(desc.get("params") or {})
+    if name == "std_normal":
+        return std_normal_model(int(params.get("dim", 1)))
+    if name == "gaussian":
+        if "cov_diag" not in params:
+            raise ValueError("gaussian descriptor needs params.cov_diag")
+        return gaussian_model(params["cov_diag"])
+    if name == "funnel":
+        return funnel_model(int(params.get("dim", 10)))
+    if name == "eight_schools":
+        return eight_schools_model(params.get("y", EIGHT_SCHOOLS_Y), params.get("sigma", EIGHT_SCHOOLS_SIGMA))
+    if name == "logistic_regression":
+        data_path = desc.get("data_path")
+        if data_path is None:
+            raise ValueError("logistic_regression descriptor needs data_path")
+        data_path = Path(data_path)
+        if not data_path.is_absolute() and base_dir is not None:
+            data_path = Path(base_dir) / data_path
+        return logistic_regression_model(load_logistic_csv(data_path), precision=params.get("precision", "fp64"))
+    raise ValueError(f"unknown model name: {name!r}")
+
+
+BUILTIN_MODELS = ("std_normal", "gaussian", "logistic_regression", "funnel", "eight_schools")

@@ -1,0 +1,377 @@
+#!/usr/bin/env python
+"""Benchmark: covtype-shaped Bayesian logistic regression NUTS on B200.
+
+BASELINE.json metric: leapfrog steps/s (and ESS/s) of NUTS on synthetic
+covtype-shaped logistic regression (581,012 rows x 54 features, D = 55),
+1 chain per GPU, max_tree_depth 10 (configs[1]).
+
+One benchmark STEP = one complete run of that configuration through the
+device engine: step-size search, 1000 warmup draws with dual averaging and
+windowed mass adaptation, 1000 sampling draws.  All of it is ONE persistent
+cooperative kernel launch (ts_run_chains); the step's leapfrogs are counted
+on the device.  Multi-GPU (torchrun, one rank per GPU) runs independent
+replicas with different seeds (weak scaling, "replicas only": a 126 MB data
+pass is too small to amortise a per-leapfrog collective).
+
+Keys of the JSON line beyond the driver contract:
+  roofline     achieved GB/s of the persistent kernel = algorithmic bytes per
+               data pass (4*N*p + N) x passes / kernel time (CUDA events on
+               the launching stream); peak = MEASURED_PEAKS.json hbm_gbs
+  eval_only    the fused potential+gradient pass alone (ts_eval_bench)
+  cpu_baseline the oracle port (oracle/, fused OpenMP pass + Python tree
+               logic) on the host cores for a bounded sample
+  e2e          the public API (logistic_regression_model + run) from host
+               numpy data: H2D of X and y, re-tiling, run, D2H of results
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+N_ROWS, N_FEAT, DATA_SEED = 581012, 54, 20191222
+ALGO_BYTES_PER_PASS = 4 * N_ROWS * N_FEAT + N_ROWS  # fp32 X + uint8 y = 126,079,604 B
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--precision", choices=("fp64", "fp32"), default="fp64")
+    ap.add_argument("--num-warmup", type=int, default=1000)
+    ap.add_argument("--num-samples", type=int, default=1000)
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,utilization.gpu")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                vals = [v.strip() for v in out.stdout.strip().split(",")]
+                if len(vals) >= 7:
+                    self.samples.append(vals)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+
+        def num(v):
+            try:
+                return float(v)
+            except ValueError:
+                return None
+
+        loaded = [s for s in self.samples if (num(s[6]) or 0) > 0] or self.samples
+        sm = [num(s[0]) for s in loaded if num(s[0]) is not None]
+        reasons = set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for s in loaded:
+            for k, name in enumerate(names):
+                if s[2 + k].lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": num(loaded[0][1]),
+                "reasons": sorted(reasons), "samples": len(loaded)}
+
+
+def make_data():
+    from tests_data import logistic_data
+
+    x, y = logistic_data(N_ROWS, N_FEAT, DATA_SEED)
+    return np.ascontiguousarray(x, dtype=np.float32), np.ascontiguousarray(y, dtype=np.uint8)
+
+
+def cpu_baseline(x32, y8, seconds, start=None, step=None, inv=None, seed=1):
+    """Oracle port on the host cores: NUTS transitions of the same model
+    (fused OpenMP logistic pass + Python tree logic), bounded by `seconds`."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import turnstile_oracle as o
+
+    m = o.Model("logistic_regression", N_FEAT + 1, x=x32.astype(np.float64), y=y8.astype(np.float64), fused_omp=True)
+    m._x32, m._y8 = x32, y8
+    key = o.chain_keys(seed, 1)[0]
+    if start is None:
+        # bounded sample of the run itself: q0 ~ U(-2,2), step-size search, warmup draws
+        t0 = time.perf_counter()
+        lf = 0
+        out = None
+        budget = 64
+        while time.perf_counter() - t0 < seconds:
+            out = o.run_chain(m, key, 1000, 1, max_leapfrogs=budget)
+            lf += out["total_leapfrogs"]
+            budget *= 2
+        el = time.perf_counter() - t0
+        return lf, el, m.threads, "oracle run_chain warmup draws from q0 (leapfrog budget doubling)"
+    z = o.Point(list(start), [0.0] * (N_FEAT + 1), m.potential(list(start)), m.gradient(list(start)))
+    t0 = time.perf_counter()
+    lf = 0
+    i = 0
+    while time.perf_counter() - t0 < seconds:
+        z, st, _ = o.transition(z, step, inv, m, o.key_fold(key, 10 + i))
+        lf += st.leapfrogs
+        i += 1
+    el = time.perf_counter() - t0
+    return lf, el, m.threads, f"{i} oracle NUTS transitions from the device's adapted state"
+
+
+def run_reference(args):
+    """--impl reference: the CPU implementation of the path (oracle port), rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    x32, y8 = make_data()
+    times, lfs = [], []
+    threads = 1
+    per_step = max(1.0, min(20.0, 120.0 / max(1, args.steps + args.warmup)))
+    for s in range(args.warmup + args.steps):
+        lf, el, threads, sample = cpu_baseline(x32, y8, per_step, seed=args.seed + s)
+        if s >= args.warmup:
+            times.append(el)
+            lfs.append(lf)
+    value = sum(lfs) / sum(times)
+    line = {
+        "impl": "reference",
+        "metric": "leapfrog_steps_per_sec",
+        "value": value,
+        "unit": "leapfrog/s",
+        "n_gpus": args.gpus,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": 1000.0 * sum(times) / len(times),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": "covtype-shaped logistic NUTS, 581012x54 (D=55), 1 chain, max_tree_depth 10",
+                   "rows": N_ROWS, "features": N_FEAT},
+        "cpu_baseline": {"value": value, "unit": "leapfrog/s", "cores": threads, "kind": "port",
+                         "sample": f"{per_step:.0f} s per step: {sample}"},
+        "e2e": {"value": value, "unit": "leapfrog/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1912_11554_b200 as ts
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    x32, y8 = make_data()
+    model =ts.logistic_regression_model(ts.LogisticRegressionData(x32, y8), precision=args.precision)
+    model.device_spec.handle(dev)
+    cfg_for = lambda seed: ts.RunConfig(model={"model": "logistic_regression"}, num_chains=1,  # noqa: E731
+                                        num_warmup=args.num_warmup, num_samples=args.num_samples, seed=seed)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MB > L2
+
+    # ---------------------------------------------------------------- device-resident timed region
+    ms_list, lf_list, ev_list, ess_list = [], [], [], []
+    last = None
+    clocks = ClockSampler(local)
+    for s in range(args.warmup + args.steps):
+        seed = args.seed + 1000 * s + rank
+        keys = ts.chain_keys(seed, 1)
+        flush.fill_(float(s))
+        barrier()
+        if s == args.warmup:
+            clocks.__enter__()
+        r = ts.run_device(model, cfg_for(seed), keys, dev, sync=False)
+        r.event_ms[1].synchronize()
+        barrier()
+        if s >= args.warmup:
+            ms = r.event_ms[0].elapsed_time(r.event_ms[1])
+            st = r.stats.cpu().numpy()[0]
+            ms_list.append(ms)
+            lf_list.append(float(st[:, 1].sum()))
+            ev_list.append(float(r.evals.cpu().numpy()[0]))
+            samples = r.samples.cpu().numpy()[0]
+            ess_list.append(float(np.nanmin(ts.ess(samples[None]))))
+            last = r
+    clocks.__exit__(None, None, None)
+    t_total_ms = max_over_ranks(sum(ms_list))
+    lf_total = sum_over_ranks(sum(lf_list))
+    ev_total_local = sum(ev_list)
+    ess_total = sum_over_ranks(sum(ess_list))
+    value = lf_total / (t_total_ms / 1000.0)
+    ess_per_s = ess_total / (t_total_ms / 1000.0)
+
+    # roofline of the persistent kernel (this rank's own launches and clock)
+    peak, peak_kind = peaks()
+    achieved = ALGO_BYTES_PER_PASS * ev_total_local / (sum(ms_list) / 1000.0) / 1e9
+
+    # eval-only microbenchmark: the fused pass alone, 200 passes in one launch
+    q = torch.from_numpy(np.asarray(last.samples.cpu().numpy()[0, -1])).to(dev)
+    out = torch.empty(1, dtype=torch.float64, device=dev)
+    lib = ts._lib.load_library()
+    h = model.device_spec.handle(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for _ in range(2):
+        ts._lib.check(lib.ts_eval_bench(h, q.data_ptr(), 20, out.data_ptr(), ts._lib.stream_ptr(torch)))
+    flush.fill_(1.0)
+    e0.record()
+    ts._lib.check(lib.ts_eval_bench(h, q.data_ptr(), 200, out.data_ptr(), ts._lib.stream_ptr(torch)))
+    e1.record()
+    e1.synchronize()
+    eval_us = e0.elapsed_time(e1) * 1000.0 / 200
+    eval_gbs = ALGO_BYTES_PER_PASS / (eval_us * 1e-6) / 1e9
+
+    # ---------------------------------------------------------------- end to end through the public API
+    e2e = None
+    if not args.no_e2e:
+        xp = torch.from_numpy(x32).pin_memory()
+        yp = torch.from_numpy(y8).pin_memory()
+        e_ms, e_lf = [], []
+        h2d = x32.nbytes + y8.nbytes
+        d2h = 0
+        for s in range(max(1, args.steps)):
+            seed = args.seed + 7777 + 1000 * s + rank
+            barrier()
+            t0 = time.perf_counter()
+            # the user's calls: model from host arrays (pinned), then run()
+            m2 = ts.logistic_regression_model(ts.LogisticRegressionData(xp.numpy(), yp.numpy()),
+                                              precision=args.precision)
+            res = ts.run(cfg_for(seed), m2, devices=[local])
+            torch.cuda.synchronize()
+            el = time.perf_counter() - t0
+            barrier()
+            e_ms.append(max_over_ranks(el * 1000.0))
+            e_lf.append(sum_over_ranks(float(res[0].total_leapfrogs)))
+            d2h = (res[0].samples.nbytes + (args.num_warmup + args.num_samples) * 5 * 8
+                   + (2 + args.num_warmup + N_FEAT + 1) * 8)
+            del m2, res
+        e2e = {"value": sum(e_lf) / (sum(e_ms) / 1000.0), "unit": "leapfrog/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        samples = last.samples.cpu().numpy()[0]
+        adapt = last.adapt.cpu().numpy()[0]
+        W = args.num_warmup
+        lf, el, threads, sample = cpu_baseline(x32, y8, args.cpu_seconds, start=samples[-1], step=float(adapt[1]),
+                                               inv=adapt[2 + W:].tolist(), seed=args.seed)
+        cpu = {"value": lf / el, "unit": "leapfrog/s", "cores": threads, "kind": "port",
+               "sample": f"{sample}: {lf} leapfrogs in {el:.1f} s (fused OpenMP fp64 pass, {threads} threads)"}
+
+    if rank == 0:
+        line = {
+            "metric": "leapfrog_steps_per_sec",
+            "value": value,
+            "unit": "leapfrog/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": t_total_ms / args.steps,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f64" if args.precision == "fp64" else "f32-rows/f64-accum",
+            "data": "synthetic",
+            "config": {
+                "workload": "covtype-shaped logistic NUTS, 581012x54 (D=55), 1 chain per GPU, max_tree_depth 10",
+                "num_warmup": args.num_warmup, "num_samples": args.num_samples, "precision": args.precision,
+                "parallelism": f"replicas{world}", "l2": "256 MB buffer written between steps (X+y = 126 MB ~ L2)",
+                "step": "one full run (step-size search + warmup + sampling) = one persistent kernel launch",
+            },
+            "ess_per_sec": ess_per_s,
+            "leapfrogs_per_step": lf_total / args.steps,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                         "bytes_per_pass": ALGO_BYTES_PER_PASS, "passes": ev_total_local},
+            "eval_only": {"us_per_pass": eval_us, "achieved_gbs": eval_gbs, "frac": eval_gbs / peak},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": args.steps,
+            "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

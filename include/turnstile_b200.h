@@ -128,10 +128,11 @@ int ts_find_step_size(const ts_model* m, const double* inv_dev, const double* z_
  * adapt.py:119-127); da_weight_dev [W] = t^-kappa.  Outputs: samples
  * [C][S][dim], stats [C][W+S][5] (depth, leapfrogs, diverged, accept_stat,
  * energy), adapt [C][2+W+dim] (initial step, final step, step trace,
- * inverse mass), status [C] (0 ok, 1 invalid mass install). */
+ * inverse mass), status [C] (0 ok, 1 invalid mass install), evals [C] or NULL
+ * (model evaluations = passes over the data, incl. step-size search). */
 int ts_run_chains(const ts_model* m, const ts_run_cfg* rc, const uint64_t* chain_keys_dev, int n_chains,
                   const double* inv0_dev, const uint8_t* schedule_dev, const double* da_weight_dev, double* samples,
-                  double* stats, double* adapt, int32_t* status, int exec_mode, void* stream);
+                  double* stats, double* adapt, int32_t* status, int64_t* evals, int exec_mode, void* stream);
 
 /* Parity probe of the device randomness (csrc/ts_rng.cuh): kind 0 writes n
  * Generator.random() doubles of RngKey(key).generator(), kind 1 n

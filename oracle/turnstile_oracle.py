@@ -187,9 +187,30 @@ class Model:
     y: np.ndarray = None
     es_y: list = None
     es_s: list = None
+    fused_omp: bool = False  # logistic: one OpenMP pass computes U and gradient (CPU baseline)
     _clib: object = field(default=None, repr=False)
+    _cache: tuple = field(default=None, repr=False)
+    threads: int = 0
+
+    def _fused(self, q):
+        """U and gradient from ts_oracle_logistic_omp, cached for the pair of calls
+        integrator.leapfrog makes at the same point (integrator.py:98-101)."""
+        key = tuple(q)
+        if self._cache is None or self._cache[0] != key:
+            if getattr(self, "_x32", None) is None:
+                self._x32 = np.ascontiguousarray(self.x, dtype=np.float32)
+                self._y8 = np.ascontiguousarray(self.y, dtype=np.uint8)
+            th = np.ascontiguousarray(q, dtype=np.float64)
+            out = np.empty(self.dim + 1)
+            self.threads = self.clib().ts_oracle_logistic_omp(self._x32.ctypes.data, self._y8.ctypes.data,
+                                                              self.x.shape[0], self.x.shape[1], th.ctypes.data,
+                                                              out.ctypes.data)
+            self._cache = (key, float(out[0]), out[1:].tolist())
+        return self._cache[1], self._cache[2]
 
     def potential(self, q):
+        if self.fused_omp:
+            return self._fused(q)[0]
         k = self.kind
         if k == "std_normal":
             acc = 0.0
@@ -217,6 +238,8 @@ class Model:
         raise ValueError(k)
 
     def gradient(self, q):
+        if self.fused_omp:
+            return list(self._fused(q)[1])
         k = self.kind
         if k == "std_normal":
             return list(q)
@@ -595,9 +618,17 @@ def schedule_flags(W):
     return flags
 
 
+class Budget(Exception):
+    """Raised by run_chain when max_leapfrogs is exhausted (bounded CPU samples)."""
+
+
 def run_chain(model, key, W, S, step=1.0, inv0=None, has_sampler=False, target=0.8, max_depth=10, generalized=True,
-              threshold=1000.0):
-    """chains.run_chain (chains.py:98-163); returns dict of samples/stats/adaptation."""
+              threshold=1000.0, max_leapfrogs=None):
+    """chains.run_chain (chains.py:98-163); returns dict of samples/stats/adaptation.
+
+    ``max_leapfrogs`` bounds the work for CPU timing samples: the run stops
+    after the first transition that crosses the budget and returns what it has
+    (``"truncated": True``)."""
     D = model.dim
     us = Stream(key_fold(key, 0))
     q0 = [-2.0 + 4.0 * us.random() for _ in range(D)]
@@ -615,6 +646,9 @@ def run_chain(model, key, W, S, step=1.0, inv0=None, has_sampler=False, target=0
             trace.append(cur)
             z, st, _ = transition(z, cur, inv, model, key_fold(key, 10 + i), max_depth, generalized, threshold)
             stats.append(st)
+            if max_leapfrogs is not None and sum(s.leapfrogs for s in stats) >= max_leapfrogs:
+                return {"samples": [], "stats": stats, "adaptation": {}, "truncated": True,
+                        "total_leapfrogs": sum(s.leapfrogs for s in stats)}
             a = min(1.0, max(0.0, st.accept))
             t = i + 1
             frac = 1.0 / (t + 10.0)
@@ -643,6 +677,8 @@ def run_chain(model, key, W, S, step=1.0, inv0=None, has_sampler=False, target=0
         z, st, _ = transition(z, final, inv, model, key_fold(key, 10 + W + i), max_depth, generalized, threshold)
         samples.append(list(z.q))
         stats.append(st)
+        if max_leapfrogs is not None and sum(s.leapfrogs for s in stats) >= max_leapfrogs:
+            break
     return {"samples": samples, "stats": stats, "adaptation": adaptation,
             "total_leapfrogs": sum(s.leapfrogs for s in stats)}
 

@@ -88,7 +88,7 @@ def _declare(lib):
                                   _P, _I, _P]
     lib.ts_transition.argtypes = [_P, ctypes.POINTER(SamplerCfgC), _P, _P, _P, _U64, _U64, _P, _P, _I, _P, _I, _P]
     lib.ts_find_step_size.argtypes = [_P, _P, _P, _P, _U64, _U64, _D, _P, _I, _P]
-    lib.ts_run_chains.argtypes = [_P, ctypes.POINTER(RunCfgC), _P, _I, _P, _P, _P, _P, _P, _P, _P, _I, _P]
+    lib.ts_run_chains.argtypes = [_P, ctypes.POINTER(RunCfgC), _P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _I, _P]
     lib.ts_rng_probe.argtypes = [_U64, _U64, _I, _I, _P, _P]
     for name in EXPORTS:
         if name not in ("ts_last_error",):

@@ -104,11 +104,12 @@ class DeviceRun:
     """Raw device outputs of one run on one GPU (arrays stay on the device
     until ``fetch``)."""
 
-    def __init__(self, samples, stats, adapt, status, event_ms):
+    def __init__(self, samples, stats, adapt, status, evals, event_ms):
         self.samples = samples
         self.stats = stats
         self.adapt = adapt
         self.status = status
+        self.evals = evals
         self.event_ms = event_ms
 
 
@@ -137,6 +138,7 @@ def run_device(model: TargetModel, config: RunConfig, keys: Sequence[RngKey], de
         stats = torch.empty((C, W + S, 5), dtype=torch.float64, device=dev)
         adapt = torch.zeros((C, 2 + W + D), dtype=torch.float64, device=dev)
         status = torch.zeros(C, dtype=torch.int32, device=dev)
+        evals = torch.zeros(C, dtype=torch.int64, device=dev)
         rc = _lib.RunCfgC(W, S, float(config.target_accept), 1 if config.sampler is not None else 0, 0,
                           sampler_cfg_c(base))
         lib = _lib.load_library()
@@ -144,14 +146,14 @@ def run_device(model: TargetModel, config: RunConfig, keys: Sequence[RngKey], de
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record()
         _lib.check(lib.ts_run_chains(handle, rc, _lib.ptr(kd), C, _lib.ptr(inv0), _lib.ptr(sched), _lib.ptr(weights),
-                                     _lib.ptr(samples), _lib.ptr(stats), _lib.ptr(adapt), _lib.ptr(status),
+                                     _lib.ptr(samples), _lib.ptr(stats), _lib.ptr(adapt), _lib.ptr(status), _lib.ptr(evals),
                                      exec_mode_for(model, exec_mode), _lib.stream_ptr(torch)))
         t1.record()
         ms = None
         if sync:
             t1.synchronize()
             ms = t0.elapsed_time(t1)
-    return DeviceRun(samples, stats, adapt, status, ms if sync else (t0, t1))
+    return DeviceRun(samples, stats, adapt, status, evals, ms if sync else (t0, t1))
 
 
 def _results(chain_ids, run: DeviceRun, config: RunConfig, D: int, wall_ns: int) -> list[ChainResult]:

@@ -263,7 +263,8 @@ extern "C" int ts_find_step_size(const ts_model* m, const double* inv_dev, const
 
 extern "C" int ts_run_chains(const ts_model* m, const ts_run_cfg* rc, const uint64_t* chain_keys_dev, int n_chains,
                              const double* inv0_dev, const uint8_t* schedule_dev, const double* da_weight_dev,
-                             double* samples, double* stats, double* adapt, int32_t* status, int exec_mode, void* stream) {
+                             double* samples, double* stats, double* adapt, int32_t* status, int64_t* evals, int exec_mode,
+                             void* stream) {
   if (!m || !rc || !chain_keys_dev || !inv0_dev || !samples || !stats || !adapt || !status)
     return set_err(TS_EINVAL, "null argument");
   int r = check_cfg(&rc->sampler);
@@ -285,7 +286,7 @@ extern "C" int ts_run_chains(const ts_model* m, const ts_run_cfg* rc, const uint
   A.rc.da_weight = da_weight_dev;
   A.chain_keys = chain_keys_dev;
   A.n_chains = n_chains;
-  A.samples = samples; A.stats = stats; A.adapt = adapt; A.status = status;
+  A.samples = samples; A.stats = stats; A.adapt = adapt; A.status = status; A.evals = evals;
   cudaStream_t st = (cudaStream_t)stream;
   const int nslots = rc->sampler.max_tree_depth - 1;
   if (m->kind == TS_LOGISTIC) {

@@ -521,6 +521,7 @@ struct RunOut {
   double* stats;     // [(W+S)][5]
   double* adapt;     // [2 + W + D]: eps0, final step, step trace, inv mass
   int32_t* status;   // 0 ok, 1 invalid mass matrix install
+  int64_t* evals;    // model evaluations (passes over the data) of this chain
 };
 
 // run_chain (chains.py:98-163) for the chain owning key `ck`.
@@ -625,6 +626,7 @@ __device__ void run_chain(Engine<Team, Model>& E, Key ck, const RunCfg& rc, cons
   if (writer) {
     const double* inv = E.v(V_INV);
     for (int d = E.T.rank(); d < D; d += E.T.size()) out.adapt[2 + W + d] = inv[d * s];
+    if (E.T.leader() && out.evals) out.evals[0] = (int64_t)E.n_evals;
   }
 }
 

@@ -62,6 +62,7 @@ struct OpArgs {
   double* stats;    // [C][W+S][5]
   double* adapt;    // [C][2+W+D]
   int32_t* status;  // [C]
+  int64_t* evals;   // [C]
 };
 
 struct SmallW {
@@ -182,6 +183,7 @@ __device__ void do_op(Engine<Team, Model>& E, const OpArgs& A, int chain, bool w
       ro.stats = A.stats + (int64_t)chain * (W + S) * 5;
       ro.adapt = A.adapt + (int64_t)chain * (2 + W + D);
       ro.status = A.status + chain;
+      ro.evals = A.evals ? A.evals + chain : nullptr;
       const Key ck{A.chain_keys[2 * chain], A.chain_keys[2 * chain + 1]};
       run_chain(E, ck, A.rc, ro, writer);
       break;
@@ -205,6 +207,14 @@ __global__ void __launch_bounds__(256, 1) k_block_op(MW mw, int D, int nslots, i
     E.M.wred = smem + (int64_t)nv * D + 64;
     E.M.red_s = E.M.wred + model_scratch;
     E.M.epoch = 0;
+    // TMA pipeline region: stages (128-B aligned) | mbarriers | per-warp counters
+    const int nwarps = blockDim.x >> 5;
+    uintptr_t pb = reinterpret_cast<uintptr_t>(E.M.red_s + E.M.a.p + 2);
+    pb = (pb + 127) & ~(uintptr_t)127;
+    E.M.a.stages = reinterpret_cast<unsigned char*>(pb);
+    E.M.a.mbar = reinterpret_cast<uint64_t*>(pb + (size_t)nwarps * E.M.a.nstage * E.M.a.stage_bytes);
+    E.M.a.pipe = reinterpret_cast<WarpPipe*>(E.M.a.mbar + nwarps * E.M.a.nstage);
+    logistic_pipeline_init(E.M.a);
   }
   const bool writer = blockIdx.x == 0;
   if (A.op == OP_RUN) {
@@ -213,6 +223,7 @@ __global__ void __launch_bounds__(256, 1) k_block_op(MW mw, int D, int nslots, i
   } else {
     do_op(E, A, 0, writer);
   }
+  if constexpr (!std::is_same<MW, SmallW>::value) logistic_pipeline_drain(E.M.a);
 }
 
 

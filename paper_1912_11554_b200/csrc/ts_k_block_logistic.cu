@@ -1,5 +1,6 @@
 // BlockTeam kernel for the logistic model: cooperative persistent grid.
 #include <stdio.h>
+#include <stdlib.h>
 #include "ts_internal.cuh"
 
 namespace ts_internal {
@@ -16,15 +17,28 @@ int launch_block_logistic(const ts_model* m, int nslots, OpArgs& A, cudaStream_t
   if (scratch < threads) scratch = threads;
   if (scratch < m->p + 2) scratch = m->p + 2;
   const int D = m->dim;
-  const size_t smem = ((size_t)num_vecs(nslots) * D + 64 + scratch + (m->p + 2)) * sizeof(double);
+  const size_t base = ((size_t)num_vecs(nslots) * D + 64 + scratch + (m->p + 2)) * sizeof(double) + 128;
+  int dev = 0, nsm = 0, smem_max = 0;
+  TS_CUDA(cudaGetDevice(&dev));
+  TS_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  TS_CUDA(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  // per-warp TMA ring: as many stages (<= 4) as shared memory allows
+  const int stage_bytes = ((128 * m->p + 32) + 127) / 128 * 128;
+  int nstage = 4;
+  auto need = [&](int ns) { return base + (size_t)nwarps * ns * (stage_bytes + 8) + nwarps * 16; };
+  while (nstage > 1 && need(nstage) > (size_t)smem_max) --nstage;
+  if (need(nstage) > (size_t)smem_max)
+    return set_err(TS_EUNSUPPORTED, "logistic model: shared memory too small for D / max_tree_depth");
+  mw.a.nstage = nstage;
+  mw.a.stage_bytes = stage_bytes;
+  mw.a.l2_keep_tiles = 0;
+  if (const char* e = getenv("TS_L2_KEEP_FRAC")) mw.a.l2_keep_tiles = (int)(atof(e) * (double)m->ntiles);
+  const size_t smem = need(nstage);
   auto kern = k_block_op<LogisticW>;
   TS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 0;
   TS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem));
   if (occ < 1) return set_err(TS_EUNSUPPORTED, "logistic kernel cannot be resident (shared memory / registers)");
-  int dev = 0, nsm = 0;
-  TS_CUDA(cudaGetDevice(&dev));
-  TS_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
   int64_t grid = (int64_t)nsm * occ;
   if (m->grid > 0 && m->grid < grid) grid = m->grid;
   if (grid > m->ntiles) grid = m->ntiles;

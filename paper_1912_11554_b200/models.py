@@ -163,16 +163,19 @@ class LogisticRegressionData:
     y: np.ndarray
 
     def __post_init__(self):
-        x = np.atleast_2d(np.asarray(self.x, dtype=np.float64))
-        y = np.asarray(self.y, dtype=np.float64).ravel()
+        # Kept in the device's storage types: X float32 (C order), y uint8.
+        x = np.atleast_2d(np.asarray(self.x))
+        y = np.asarray(self.y).ravel()
         if x.shape[0] != y.shape[0]:
             raise ValueError("covariate rows and labels disagree in length")
-        if not np.isfinite(x).all() or not np.isfinite(y).all():
+        x32 = np.ascontiguousarray(x, dtype=np.float32)
+        if not np.isfinite(x32).all() or (y.dtype.kind == "f" and not np.isfinite(y).all()):
             raise ValueError("logistic data must be free of NaN/Inf")
-        if not np.isin(y, (0.0, 1.0)).all():
+        y8 = y.astype(np.uint8)
+        if not np.array_equal(y8, y) or (y8 > 1).any():
             raise ValueError("labels must be 0 or 1")
-        object.__setattr__(self, "x", np.ascontiguousarray(x))
-        object.__setattr__(self, "y", np.ascontiguousarray(y))
+        object.__setattr__(self, "x", x32)
+        object.__setattr__(self, "y", np.ascontiguousarray(y8))
 
     @property
     def num_features(self) -> int:
@@ -202,8 +205,7 @@ def logistic_regression_model(data: LogisticRegressionData, precision: str = "fp
     ``"fp64"`` (parity mode, differs from the reference only in summation
     order) or ``"fp32"`` (per-row math in float, accumulation in double).
     """
-    x32 = np.ascontiguousarray(data.x, dtype=np.float32)
-    y8 = np.ascontiguousarray(data.y, dtype=np.uint8)
+    x32, y8 = data.x, data.y
     dim = data.num_features + 1
     spec = DeviceSpec(_lib.TS_LOGISTIC, dim, x=x32, y=y8, precision=precision)
     return _device_model(

@@ -220,6 +220,12 @@ def test_trees_match_reference(mode):
         # block teams reduce dot products in a shuffle-tree order: ulp-level
         # differences that a leapfrog chain of up to 2^8 steps may amplify
         rel = (SMALL_REL if mode == "thread" else BLOCK_REL) if small else FP64_REL
+        if not small:
+            x = np.asarray([nums(r) for r in case["model"]["x"]])
+            if not np.array_equal(x.astype(np.float32).astype(np.float64), x):
+                # crosscheck.build_case draws X in fp64; the device stores X in
+                # fp32, so these cases see data rounded by <= 2^-24
+                rel = FP32_REL
         ints_ok, floats_ok = _check_tree(case, tree, trace, rel)
         if not ints_ok:
             bad_int.append(i)

@@ -88,7 +88,9 @@ int ts_model_set_grid(ts_model* m, int grid);
 int ts_potential_grad(const ts_model* m, const double* q_dev, int n_points, double* out_dev, void* stream);
 
 /* Benchmark helper: `repeats` evaluations of the same point inside one
- * persistent launch (the per-leapfrog model cost of the device loop). */
+ * persistent launch (the per-leapfrog model cost of the device loop).
+ * out_dev[6]: U, kernel-internal ns (globaltimer, CTA 0), then 4 uint64
+ * CTA-0 cycle counters (prior, data pass, barrier, cross-CTA reduce). */
 int ts_eval_bench(const ts_model* m, const double* q_dev, int repeats, double* out_dev, void* stream);
 
 /* Replaces integrator.leapfrog (integrator.py:90-103).

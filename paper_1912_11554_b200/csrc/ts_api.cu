@@ -8,6 +8,7 @@
 //                  that evaluates each potential together (one grid barrier
 //                  per leapfrog) and run the tree logic redundantly.
 #include <stdio.h>
+#include <stdlib.h>
 #include "ts_internal.cuh"
 
 using namespace ts;
@@ -134,6 +135,7 @@ extern "C" int ts_model_create(int kind, int dim, const double* params, int n_pa
       cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, m->device);
       const size_t pb = 2 * (size_t)nsm * 2 * (n_feat + 2);  // room for up to 2 CTAs per SM
       if (cudaMalloc((void**)&m->pbuf, pb * sizeof(double)) != cudaSuccess) return fail(TS_ECUDA, "cudaMalloc partials failed");
+      if (cudaMemset(m->pbuf, 0, pb * sizeof(double)) != cudaSuccess) return fail(TS_ECUDA, "memset partials failed");
       if (cudaMalloc((void**)&m->bar, sizeof(unsigned long long)) != cudaSuccess) return fail(TS_ECUDA, "cudaMalloc barrier failed");
       if (cudaDeviceSynchronize() != cudaSuccess) return fail(TS_ECUDA, "retile failed");
       break;
@@ -202,7 +204,11 @@ extern "C" int ts_eval_bench(const ts_model* m, const double* q_dev, int repeats
   TS_CUDA(cudaMallocAsync((void**)&ones, m->dim * sizeof(double), st));
   TS_CUDA(cudaMemsetAsync(ones, 0, m->dim * sizeof(double), st));
   A.inv = ones;
+  // out_dev[2..5] (as u64): CTA-0 cycle counters of the logistic pass phases
+  TS_CUDA(cudaMemsetAsync(out_dev, 0, 10 * sizeof(double), st));
+  const_cast<ts_model*>(m)->prof = reinterpret_cast<unsigned long long*>(out_dev + 2);
   int rc = launch(m, 1, A, 1, TS_EXEC_BLOCK, st);
+  const_cast<ts_model*>(m)->prof = nullptr;
   cudaFreeAsync(ones, st);
   return rc;
 }
@@ -290,10 +296,29 @@ extern "C" int ts_run_chains(const ts_model* m, const ts_run_cfg* rc, const uint
   cudaStream_t st = (cudaStream_t)stream;
   const int nslots = rc->sampler.max_tree_depth - 1;
   if (m->kind == TS_LOGISTIC) {
+    // TS_PROF=1: CTA-0 cycle counters of the run, printed to stderr (profiling aid)
+    static unsigned long long* prof_buf = nullptr;
+    const bool prof = getenv("TS_PROF") != nullptr;
+    if (prof) {
+      if (!prof_buf) TS_CUDA(cudaMalloc((void**)&prof_buf, 16 * sizeof(unsigned long long)));
+      TS_CUDA(cudaMemsetAsync(prof_buf, 0, 16 * sizeof(unsigned long long), st));
+      const_cast<ts_model*>(m)->prof = prof_buf;
+    }
     for (int c = 0; c < n_chains; ++c) {
       A.n_points = c;
       int e = launch(m, nslots, A, 1, TS_EXEC_BLOCK, st);
-      if (e) return e;
+      if (e) { const_cast<ts_model*>(m)->prof = nullptr; return e; }
+    }
+    if (prof) {
+      const_cast<ts_model*>(m)->prof = nullptr;
+      unsigned long long h[16];
+      TS_CUDA(cudaMemcpyAsync(h, prof_buf, sizeof h, cudaMemcpyDeviceToHost, st));
+      TS_CUDA(cudaStreamSynchronize(st));
+      const double n = h[10] ? (double)h[10] : 1.0;
+      fprintf(stderr,
+              "TS_PROF evals=%llu cycles/eval: in-eval %.0f (pass %.0f [entry %.0f loop %.0f warpred %.0f ctared %.0f] "
+              "barrier %.0f reduce %.0f) between-evals %.0f\n",
+              h[10], h[8] / n, h[1] / n, h[4] / n, h[5] / n, h[6] / n, h[7] / n, h[2] / n, h[3] / n, h[9] / n);
     }
     return TS_OK;
   }

@@ -38,6 +38,11 @@ enum Vid : int {
 constexpr int kSlotVecs = 5;  // FQ, FR, CUMF, PQ, PG
 constexpr int kMaxSlots = 30;  // treemath.MAX_TREE_DEPTH_LIMIT
 __host__ __device__ inline int num_vecs(int nslots) { return V_SLOT0 + kSlotVecs * nslots; }
+// shared-memory scratch of a team (doubles): 64 for reductions / commands,
+// then the NodeStore scalars (kMaxSlots SlotScalars)
+constexpr int kTeamScratch = 64 + (kMaxSlots * 56 + 7) / 8;
+// shared-memory slot per driver-warp lane for its Engine object (grid mode)
+constexpr int kEngineSlotBytes = 1024;
 __device__ __forceinline__ int slot_vec(int s, int k) { return V_SLOT0 + kSlotVecs * s + k; }
 
 enum Stop : int { kStopNone = 0, kStopTurn = 1, kStopDiv = 2 };
@@ -70,6 +75,7 @@ struct SlotScalars {
   double lw, metro, pU, pH, fU;
   int count, pidx, leaf;
 };
+static_assert(sizeof(SlotScalars) == 56, "kTeamScratch assumes 56-byte slot records");
 
 struct TreeOut {
   double lw, sum_metro, pU, pH, fU;
@@ -119,8 +125,13 @@ struct Engine {
   // running subtree scalars
   double r_lw, r_metro, r_pU, r_pH, r_fU;
   int r_count, r_pidx;
-  SlotScalars ss[kMaxSlots];
+  // NodeStore scalars: per-thread local array for ThreadTeam; shared memory
+  // for CTA/warp teams (every team thread writes the identical value), which
+  // keeps them out of the local-memory path when shared memory crowds L1.
+  SlotScalars* ss;
   unsigned long long n_evals;
+  unsigned long long* prof = nullptr;  // CTA 0 / thread 0 only (profiling builds of a run)
+  long long prof_last = 0;
 
   __device__ __forceinline__ double* v(int id) const { return S.v(id); }
   __device__ __forceinline__ int64_t ds() const { return S.dstride; }
@@ -158,8 +169,20 @@ struct Engine {
   // model evaluation at vector qid -> U (non-finite -> +inf), gradient -> gid
   __device__ double eval(int qid, int gid) {
     T.sync();
+    long long c0 = 0;
+    const bool pr = prof != nullptr && T.leader();
+    if (pr) {  // profiling: [8] cycles inside model evaluations, [9] between them
+      c0 = clock64();
+      if (prof_last) prof[9] += c0 - prof_last;
+    }
     double u = M.eval(T, S, qid, gid);
     T.sync();
+    if (pr) {
+      const long long c1 = clock64();
+      prof[8] += c1 - c0;
+      prof[10] += 1;
+      prof_last = c1;
+    }
     n_evals += 1;
     return isfinite(u) ? u : kInf();
   }
@@ -283,7 +306,9 @@ struct Engine {
   // build_tree_iterative (tree.py:344-453).  Input: frontier in CQ/CR/CG/cur_U.
   // Output: running subtree (FQ/FR/CUMF + TPQ/TPG + r_* scalars), last leaf in
   // CQ/CR/CG/cur_U, momentum sum in V_MSUM.
-  __device__ TreeOut build_tree(int depth, double eps, double h_ref, Key key) {
+  // (noinline: separate register allocation per phase keeps the chain state
+  // out of local memory, which shares the L1 left over by the TMA stages)
+  __device__ __noinline__ TreeOut build_tree(int depth, double eps, double h_ref, Key key) {
     Stream draws;
     draws.init(key);
     occupied_mask = 0;
@@ -390,7 +415,7 @@ struct Engine {
   }
 
   // nuts_transition_from (sampler.py:83-148): z0 = (Q0, G0, U0) -> proposal
-  __device__ Stats transition(Key key, const double* inj, int64_t inj_ds) {
+  __device__ __noinline__ Stats transition(Key key, const double* inj, int64_t inj_ds) {
     draw_momentum(V_R0, key_fold(key, 0), inj, inj_ds);
     const double h0 = hamiltonian(U0, V_R0);
     Stream gen;
@@ -468,7 +493,7 @@ struct Engine {
     return exp(x < 0.0 ? x : 0.0);
   }
   // find_reasonable_step_size (adapt.py:172-204); z0 in Q0/G0/U0
-  __device__ double find_step_size(Key key, double init, const double* inj, int64_t inj_ds) {
+  __device__ __noinline__ double find_step_size(Key key, double init, const double* inj, int64_t inj_ds) {
     const double target = 0.5;
     // rng.generator() of the given key directly (not a fold)
     {

@@ -29,6 +29,7 @@ struct ts_model {
   int fp64;
   int grid;
   int pmax;
+  unsigned long long* prof;  // transient: phase counters for ts_eval_bench
 };
 
 namespace ts_internal {
@@ -71,13 +72,31 @@ struct SmallW {
   __device__ double eval(const Team& T, const VecStore& S, int q, int g) { return small_model_eval(T, m, S, q, g); }
 };
 
+// Logistic model on a persistent grid.  In each CTA the driver warp runs the
+// chain (WarpTeam) and the other warps serve data passes: eval() posts a
+// command word in shared memory and joins the pass with them.
 struct LogisticW {
   LogisticArgs a;
   double* wred;
   double* red_s;
+  int* cmd;  // smem: [0] 1 = evaluate / 0 = exit, [1] q vector id, [2] gradient vector id
   unsigned long long epoch;
-  __device__ double eval(const BlockTeam& T, const VecStore& S, int q, int g) {
-    return logistic_eval_grid(T, a, S, q, g, wred, red_s, epoch);
+  template <class Team>
+  __device__ double eval(const Team&, const VecStore& S, int q, int g) {
+    if (threadIdx.x == 0) { cmd[0] = 1; cmd[1] = q; cmd[2] = g; }
+    __syncthreads();  // wakes the worker warps (and publishes q)
+    return logistic_eval_grid(a, S, q, g, wred, red_s, epoch);
+  }
+  __device__ void serve(const VecStore& S) {  // worker warps
+    for (;;) {
+      __syncthreads();
+      if (cmd[0] == 0) break;
+      logistic_eval_grid(a, S, cmd[1], cmd[2], wred, red_s, epoch);
+    }
+  }
+  __device__ void release_workers() {  // driver warp, once at the end
+    if (threadIdx.x == 0) cmd[0] = 0;
+    __syncthreads();
   }
 };
 
@@ -116,8 +135,15 @@ __device__ void do_op(Engine<Team, Model>& E, const OpArgs& A, int chain, bool w
       double* q = E.v(V_CQ);
       for (int d = rk; d < D; d += sz) q[d * s] = A.z_in[d];
       double u = 0.0;
+      unsigned long long t0 = 0, t1 = 0;
+      E.T.sync();
+      if (writer && E.T.leader()) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
       for (int k = 0; k < A.n_points; ++k) u = E.eval(V_CQ, V_CG);
-      if (writer && E.T.leader()) A.z_out[0] = u;
+      if (writer && E.T.leader()) {
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        A.z_out[0] = u;
+        A.z_out[1] = (double)(t1 - t0);
+      }
       break;
     }
     case OP_LEAPFROG: {
@@ -196,34 +222,53 @@ template <class MW>
 __global__ void __launch_bounds__(256, 1) k_block_op(MW mw, int D, int nslots, int model_scratch, OpArgs A) {
   extern __shared__ double smem[];
   const int nv = num_vecs(nslots);
-  Engine<BlockTeam, MW> E;
-  E.T.scratch = smem + (int64_t)nv * D;
-  E.M = mw;
-  E.D = D;
-  E.S.base = smem;
-  E.S.vstride = D;
-  E.S.dstride = 1;
-  if constexpr (!std::is_same<MW, SmallW>::value) {
-    E.M.wred = smem + (int64_t)nv * D + 64;
-    E.M.red_s = E.M.wred + model_scratch;
-    E.M.epoch = 0;
+  const bool writer = blockIdx.x == 0;
+  const int chain = (A.op == OP_RUN) ? A.n_points : 0;  // grid mode: one chain per launch
+  VecStore S;
+  S.base = smem;
+  S.vstride = D;
+  S.dstride = 1;
+  if constexpr (std::is_same<MW, SmallW>::value) {
+    Engine<BlockTeam, MW> E;
+    E.T.scratch = smem + (int64_t)nv * D;
+    E.ss = reinterpret_cast<SlotScalars*>(smem + (int64_t)nv * D + 64);
+    E.M = mw;
+    E.D = D;
+    E.S = S;
+    do_op(E, A, chain, writer);
+  } else {
+    mw.wred = smem + (((int64_t)nv * D + kTeamScratch + 1) & ~(int64_t)1);  // 16-byte aligned
+    mw.red_s = mw.wred + model_scratch;
+    mw.cmd = reinterpret_cast<int*>(smem + (int64_t)nv * D);   // team scratch area
+    mw.epoch = 0;
     // TMA pipeline region: stages (128-B aligned) | mbarriers | per-warp counters
     const int nwarps = blockDim.x >> 5;
-    uintptr_t pb = reinterpret_cast<uintptr_t>(E.M.red_s + E.M.a.p + 2);
+    uintptr_t pb = reinterpret_cast<uintptr_t>(mw.red_s + mw.a.p + 2);
     pb = (pb + 127) & ~(uintptr_t)127;
-    E.M.a.stages = reinterpret_cast<unsigned char*>(pb);
-    E.M.a.mbar = reinterpret_cast<uint64_t*>(pb + (size_t)nwarps * E.M.a.nstage * E.M.a.stage_bytes);
-    E.M.a.pipe = reinterpret_cast<WarpPipe*>(E.M.a.mbar + nwarps * E.M.a.nstage);
-    logistic_pipeline_init(E.M.a);
+    mw.a.stages = reinterpret_cast<unsigned char*>(pb);
+    mw.a.mbar = reinterpret_cast<uint64_t*>(pb + (size_t)nwarps * mw.a.nstage * mw.a.stage_bytes);
+    mw.a.pipe = reinterpret_cast<WarpPipe*>(mw.a.mbar + nwarps * mw.a.nstage);
+    logistic_pipeline_init(mw.a);
+    if ((threadIdx.x >> 5) == 0) {
+      // driver warp: the whole NUTS state machine, warp-synchronous.  The
+      // engine is a local object whose member functions are all inlined, so
+      // its scalar state can live in registers.
+      Engine<WarpTeam, MW> E;
+      E.M = mw;
+      E.D = D;
+      E.S = S;
+      E.prof = (blockIdx.x == 0) ? mw.a.prof : nullptr;
+      E.prof_last = 0;
+      E.tr = nullptr;
+      E.ss = reinterpret_cast<SlotScalars*>(smem + (int64_t)nv * D + 64);
+      __syncwarp();
+      do_op(E, A, chain, writer);
+      E.M.release_workers();
+    } else {
+      mw.serve(S);
+    }
+    logistic_pipeline_drain(mw.a);
   }
-  const bool writer = blockIdx.x == 0;
-  if (A.op == OP_RUN) {
-    // one chain per launch in grid mode; chain index passed via n_points
-    do_op(E, A, A.n_points, writer);
-  } else {
-    do_op(E, A, 0, writer);
-  }
-  if constexpr (!std::is_same<MW, SmallW>::value) logistic_pipeline_drain(E.M.a);
 }
 
 

@@ -13,11 +13,11 @@ int launch_block_logistic(const ts_model* m, int nslots, OpArgs& A, cudaStream_t
   mw.wred = nullptr; mw.red_s = nullptr; mw.epoch = 0;
   const int threads = 256;
   const int nwarps = threads / 32;
-  int scratch = nwarps * (PMAX + 2);
+  int scratch = (nwarps * (PMAX + 2) + 1) & ~1;
   if (scratch < threads) scratch = threads;
   if (scratch < m->p + 2) scratch = m->p + 2;
   const int D = m->dim;
-  const size_t base = ((size_t)num_vecs(nslots) * D + 64 + scratch + (m->p + 2)) * sizeof(double) + 128;
+  const size_t base = ((size_t)num_vecs(nslots) * D + kTeamScratch + 2 + scratch + (m->p + 2)) * sizeof(double) + 128;
   int dev = 0, nsm = 0, smem_max = 0;
   TS_CUDA(cudaGetDevice(&dev));
   TS_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
@@ -25,6 +25,7 @@ int launch_block_logistic(const ts_model* m, int nslots, OpArgs& A, cudaStream_t
   // per-warp TMA ring: as many stages (<= 4) as shared memory allows
   const int stage_bytes = ((128 * m->p + 32) + 127) / 128 * 128;
   int nstage = 4;
+  if (const char* e = getenv("TS_NSTAGE")) nstage = atoi(e) < 1 ? 1 : (atoi(e) > 4 ? 4 : atoi(e));  // profiling
   auto need = [&](int ns) { return base + (size_t)nwarps * ns * (stage_bytes + 8) + nwarps * 16; };
   while (nstage > 1 && need(nstage) > (size_t)smem_max) --nstage;
   if (need(nstage) > (size_t)smem_max)
@@ -32,6 +33,9 @@ int launch_block_logistic(const ts_model* m, int nslots, OpArgs& A, cudaStream_t
   mw.a.nstage = nstage;
   mw.a.stage_bytes = stage_bytes;
   mw.a.l2_keep_tiles = 0;
+  mw.a.prof = m->prof;
+  mw.a.l2_prefetch = 0;
+  if (const char* e = getenv("TS_L2_PREFETCH")) mw.a.l2_prefetch = atoi(e);
   if (const char* e = getenv("TS_L2_KEEP_FRAC")) mw.a.l2_keep_tiles = (int)(atof(e) * (double)m->ntiles);
   const size_t smem = need(nstage);
   auto kern = k_block_op<LogisticW>;
@@ -44,6 +48,9 @@ int launch_block_logistic(const ts_model* m, int nslots, OpArgs& A, cudaStream_t
   if (grid > m->ntiles) grid = m->ntiles;
   if (grid < 1) grid = 1;
   TS_CUDA(cudaMemsetAsync(m->bar, 0, sizeof(unsigned long long), st));
+  // component-major partial slots are padded to 16 CTAs; padding must read 0
+  const size_t gpad = ((size_t)grid + 15) / 16 * 16;
+  TS_CUDA(cudaMemsetAsync(m->pbuf, 0, 2 * gpad * (m->p + 2) * sizeof(double), st));
   int Dv = D, ns = nslots, sc = scratch;
   void* args[] = {&mw, &Dv, &ns, &sc, &A};
   TS_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3((unsigned)grid), dim3(threads), args, smem, st));

@@ -9,6 +9,8 @@ __global__ void __launch_bounds__(128) k_thread_op(SmallModel m, int D, int C, d
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= C) return;
   Engine<ThreadTeam, SmallW> E;
+  SlotScalars ss_local[kMaxSlots];
+  E.ss = ss_local;
   E.M.m = m;
   E.D = D;
   E.S.base = ws + c;

@@ -60,6 +60,8 @@ struct LogisticArgs {
   int nstage;
   int stage_bytes;
   int l2_keep_tiles;        // tiles [0, l2_keep_tiles) loaded with L2::evict_last, rest evict_first
+  int l2_prefetch;          // tiles per warp prefetched into L2 at the end of a pass
+  unsigned long long* prof; // optional: CTA-0 cycle counters [prior, pass, barrier, reduce] (profiling)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -107,8 +109,35 @@ __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long
   asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ void red_release_add_u64(unsigned long long* p, unsigned long long v) {
   asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ void red_add_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Exact split of a double into two int64 fixed-point words,
+//   v = hi * 2^-10 + lo * 2^-63,   hi = floor(v * 2^10),  0 <= lo < 2^53,
+// valid for |v| < 2^43 (false otherwise or if v is not finite).  Sums of up
+// to 2^8 such pairs cannot overflow, and v - hi*2^-10 is computed exactly
+// (both are multiples of ulp(v) and differ by less than 2^-10).  Truncation
+// of bits below 2^-63 is the only error.
+__device__ __forceinline__ bool fx_split(double v, long long& hi, long long& lo) {
+  if (!(fabs(v) < 8796093022208.0)) { hi = 0; lo = 0; return false; }
+  const double a = floor(v * 1024.0);
+  hi = (long long)a;
+  const double rem = v - a * (1.0 / 1024.0);
+  lo = (long long)(rem * 9223372036854775808.0);
+  return true;
+}
+__device__ __forceinline__ double fx_join(long long hi, long long lo) {
+  return (double)hi * (1.0 / 1024.0) + (double)lo * (1.0 / 9223372036854775808.0);
 }
 
 // Grid barrier #epoch (0-based) over gridDim.x co-resident CTAs.
@@ -117,8 +146,9 @@ __device__ __forceinline__ void grid_barrier(unsigned long long* bar, unsigned l
   if (threadIdx.x == 0) {
     const unsigned long long target = (epoch + 1) * (unsigned long long)gridDim.x;
     red_release_add_u64(bar, 1ULL);
-    while (ld_acquire_u64(bar) < target) {
+    while (ld_relaxed_u64(bar) < target) {
     }
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
   }
   __syncthreads();
 }
@@ -143,19 +173,50 @@ __device__ __forceinline__ WarpTiles warp_tiles(const LogisticArgs& a) {
   return w;
 }
 
-// lane 0: issue periodic-sequence tile `seq` of this warp into its stage
-__device__ __forceinline__ void issue_tile(const LogisticArgs& a, const WarpTiles& wt, unsigned long long seq) {
-  const int warp = threadIdx.x >> 5;
-  const int s = (int)(seq % (unsigned long long)a.nstage);
-  const int64_t tile = wt.first + (int64_t)(seq % (unsigned long long)wt.count) * wt.nwarps;
-  unsigned char* dst = a.stages + ((int64_t)warp * a.nstage + s) * a.stage_bytes;
-  uint64_t* bar = a.mbar + warp * a.nstage + s;
-  const uint32_t xb = 128u * (uint32_t)a.p;
-  const uint64_t pol = tile < a.l2_keep_tiles ? policy_evict_last() : policy_evict_first();
-  mbar_expect_tx(bar, xb + 32u);
-  bulk_g2s(dst, a.xt + tile * 32 * (int64_t)a.p, xb, bar, pol);
-  bulk_g2s(dst + xb, a.yt + tile * 32, 32u, bar, pol);
-}
+// Producer side of a warp's ring (lane 0): position of the next issue,
+// advanced incrementally (no 64-bit division on the per-tile path).
+struct Producer {
+  unsigned char* ring;
+  uint64_t* bars;
+  const float* xsrc;     // X of the next tile to issue
+  const uint8_t* ysrc;   // y of the next tile
+  int64_t xstep, ystep;  // advance per issue (nwarps tiles)
+  int64_t tj, count;     // periodic tile index of the next issue
+  const float* xfirst;
+  const uint8_t* yfirst;
+  int s, nstage, stage_bytes;
+  uint32_t xb;
+  uint64_t pol;
+
+  __device__ __forceinline__ void init(const LogisticArgs& a, const WarpTiles& wt, unsigned long long issued) {
+    const int warp = threadIdx.x >> 5;
+    nstage = a.nstage;
+    stage_bytes = a.stage_bytes;
+    ring = a.stages + (int64_t)warp * nstage * stage_bytes;
+    bars = a.mbar + warp * nstage;
+    s = (int)(issued % (unsigned long long)nstage);
+    count = wt.count;
+    tj = (int64_t)(issued % (unsigned long long)count);
+    xb = 128u * (uint32_t)a.p;
+    xfirst = a.xt + wt.first * 32 * (int64_t)a.p;
+    yfirst = a.yt + wt.first * 32;
+    xstep = (int64_t)wt.nwarps * 32 * a.p;
+    ystep = (int64_t)wt.nwarps * 32;
+    xsrc = xfirst + tj * xstep;
+    ysrc = yfirst + tj * ystep;
+    pol = policy_evict_first();
+  }
+  __device__ __forceinline__ void issue() {
+    uint64_t* bar = bars + s;
+    unsigned char* dst = ring + (int64_t)s * stage_bytes;
+    mbar_expect_tx(bar, xb + 32u);
+    bulk_g2s(dst, xsrc, xb, bar, pol);
+    bulk_g2s(dst + xb, ysrc, 32u, bar, pol);
+    if (++s == nstage) s = 0;
+    if (++tj == count) { tj = 0; xsrc = xfirst; ysrc = yfirst; }
+    else { xsrc += xstep; ysrc += ystep; }
+  }
+};
 
 // Kernel prologue (all threads of the CTA): mbarriers and pipe counters.
 static __device__ void logistic_pipeline_init(const LogisticArgs& a) {
@@ -180,8 +241,10 @@ static __device__ void logistic_pipeline_drain(const LogisticArgs& a) {
 }
 
 // Lane's row of a tile in shared memory -> x[0..PMAX) (zeros past p), y.
-template <int PMAX>
-__device__ __forceinline__ void row_from_stage(const unsigned char* sb, int p, int lane, float (&x)[PMAX], uint8_t& y) {
+// PE > 0 fixes p at compile time (branch-free body for the benchmark shape).
+template <int PMAX, int PE>
+__device__ __forceinline__ void row_from_stage(const unsigned char* sb, int p_rt, int lane, float (&x)[PMAX], uint8_t& y) {
+  const int p = PE > 0 ? PE : p_rt;
   const float* f = reinterpret_cast<const float*>(sb);
 #pragma unroll
   for (int g = 0; g < PMAX / 4; ++g) {
@@ -210,13 +273,15 @@ __device__ __forceinline__ void row_from_stage(const unsigned char* sb, int p, i
 // Per-CTA streaming pass.  Writes this CTA's partial sums
 // red_out[0..p) = sum resid*x_j, red_out[p] = sum resid, red_out[p+1] = sum (y eta - log1pexp)
 // (wred: >= nwarps*(PMAX+2) doubles of scratch).
-template <int PMAX, bool FP64>
+template <int PMAX, bool FP64, int PE>
 __device__ __noinline__ void logistic_cta_pass(const LogisticArgs& a, const double* __restrict__ theta_s, double* wred,
                                                double* red_out) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  const int p = a.p;
+  const int p = PE > 0 ? PE : a.p;
   constexpr int NA = PMAX + 2;
   const WarpTiles wt = warp_tiles(a);
+  const bool prof = a.prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
+  long long pc0 = prof ? clock64() : 0, pc1;
 
   using acc_t = typename std::conditional<FP64, double, float>::type;
   acc_t acc[PMAX + 1];
@@ -227,32 +292,50 @@ __device__ __noinline__ void logistic_cta_pass(const LogisticArgs& a, const doub
   float th32[PMAX];
   float thb32 = 0.f;
   if constexpr (!FP64) {
+    // theta rounded to float once per pass (PMAX+1 conversions per CTA, not
+    // per thread), then broadcast with LDS.128 (wred is free until the end)
+    float* t32 = reinterpret_cast<float*>(wred);
+    for (int j = threadIdx.x; j <= PMAX; j += blockDim.x) t32[j] = (j < p) ? (float)theta_s[j] : (j == PMAX ? (float)theta_s[p] : 0.f);
+    __syncthreads();
 #pragma unroll
-    for (int j = 0; j < PMAX; ++j) th32[j] = (j < p) ? (float)theta_s[j] : 0.f;
-    thb32 = (float)theta_s[p];
+    for (int j = 0; j < PMAX; j += 4) {
+      const float4 v = reinterpret_cast<const float4*>(t32)[j / 4];
+      th32[j] = v.x; th32[j + 1] = v.y; th32[j + 2] = v.z; th32[j + 3] = v.w;
+    }
+    thb32 = t32[PMAX];
+    __syncthreads();
   }
 
   if (wt.count > 0) {
     WarpPipe& pipe = a.pipe[warp];
     const unsigned long long c0 = pipe.consumed;
     unsigned long long issued = pipe.issued;
+    Producer prod;
     if (lane == 0) {
-      while (issued < c0 + (unsigned long long)a.nstage) issue_tile(a, wt, issued++);
+      prod.init(a, wt, issued);
+      while (issued < c0 + (unsigned long long)a.nstage) { prod.issue(); ++issued; }
     }
+    // ring position and periodic tile index, advanced incrementally
+    int s = (int)(c0 % (unsigned long long)a.nstage);
+    uint32_t parity = (uint32_t)((c0 / a.nstage) & 1ULL);
+    int64_t tj = (int64_t)(c0 % (unsigned long long)wt.count);
+    const unsigned char* ring = a.stages + (int64_t)warp * a.nstage * a.stage_bytes;
+    uint64_t* bars = a.mbar + warp * a.nstage;
+    if (prof) { pc1 = clock64(); a.prof[4] += pc1 - pc0; pc0 = pc1; }
     for (int64_t j = 0; j < wt.count; ++j) {
-      const unsigned long long seq = c0 + (unsigned long long)j;
-      const int s = (int)(seq % (unsigned long long)a.nstage);
-      mbar_wait(a.mbar + warp * a.nstage + s, (uint32_t)((seq / a.nstage) & 1ULL));
-      const unsigned char* sb = a.stages + ((int64_t)warp * a.nstage + s) * a.stage_bytes;
+      mbar_wait(bars + s, parity);
+      const unsigned char* sb = ring + (int64_t)s * a.stage_bytes;
       float x[PMAX];
       uint8_t yb;
-      row_from_stage<PMAX>(sb, p, lane, x, yb);
+      row_from_stage<PMAX, PE>(sb, p, lane, x, yb);
       __syncwarp();
       // stage s is free again: keep the producer NSTAGE tiles ahead (wrapping
       // into the next pass; X is read-only for the whole kernel)
-      if (lane == 0) issue_tile(a, wt, issued++);
-      const int64_t row = (wt.first + (int64_t)(seq % (unsigned long long)wt.count) * wt.nwarps) * 32 + lane;
+      if (lane == 0) { prod.issue(); ++issued; }
+      const int64_t row = (wt.first + tj * wt.nwarps) * 32 + lane;
       const bool valid = row < a.n_rows;
+      if (++s == a.nstage) { s = 0; parity ^= 1u; }
+      if (++tj == wt.count) tj = 0;
       if constexpr (FP64) {
         double e0 = theta_s[p], e1 = 0.0, e2 = 0.0, e3 = 0.0;
 #pragma unroll
@@ -294,20 +377,47 @@ __device__ __noinline__ void logistic_cta_pass(const LogisticArgs& a, const doub
       }
     }
     __syncwarp();
-    if (lane == 0) { pipe.consumed = c0 + (unsigned long long)wt.count; pipe.issued = issued; }
+    if (lane == 0) {
+      pipe.consumed = c0 + (unsigned long long)wt.count;
+      pipe.issued = issued;
+    }
     __syncwarp();
   }
 
-  // warp reduction in double, fixed shuffle tree
+  if (prof) { pc1 = clock64(); a.prof[5] += pc1 - pc0; pc0 = pc1; }
+  // Warp reduce-scatter (fixed order): NP column sums over 32 lanes in
+  // sum(NP/2^k) shuffles instead of 5*NP; lane ends with NP/32 columns.
+  constexpr int NP = (NA <= 16) ? 16 : (NA <= 32 ? 32 : (NA <= 64 ? 64 : 128));
+  acc_t v[NP];
 #pragma unroll
-  for (int j = 0; j < NA; ++j) {
-    double v = (j <= PMAX) ? (double)acc[j <= PMAX ? j : PMAX] : (double)accl;
-    if (j < p || j >= PMAX) {
+  for (int j = 0; j < NP; ++j) v[j] = (j <= PMAX) ? acc[j <= PMAX ? j : PMAX] : (j == PMAX + 1 ? accl : (acc_t)0);
+  int colbase = 0;
+  int cnt = NP;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if (lane == 0) wred[warp * NA + j] = v;
+  for (int off = 16; off >= 1; off >>= 1) {
+    const bool upper = (lane & off) != 0;
+    if (cnt >= 2) {
+      const int n = cnt / 2;
+#pragma unroll
+      for (int i = 0; i < NP / 2; ++i) {
+        if (i < n) {
+          const acc_t send = upper ? v[i] : v[n + i];
+          const acc_t keep = upper ? v[n + i] : v[i];
+          v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+        }
+      }
+      if (upper) colbase += n;
+      cnt = n;
+    } else {
+      v[0] += __shfl_xor_sync(0xffffffffu, v[0], off);
     }
   }
+  // lane holds columns colbase .. colbase+cnt-1 (duplicates across lanes when NP < 64)
+#pragma unroll
+  for (int i = 0; i < NP / 32 + 1; ++i) {
+    if (i < cnt && colbase + i < NA && (NP >= 32 || (lane % (32 / NP)) == 0)) wred[warp * NA + colbase + i] = (double)v[i];
+  }
+  if (prof) { pc1 = clock64(); a.prof[6] += pc1 - pc0; pc0 = pc1; }
   __syncthreads();
   // CTA reduction in warp order; output index: [0,p) features, p bias, p+1 loglik
   for (int d = threadIdx.x; d < p + 2; d += blockDim.x) {
@@ -316,19 +426,25 @@ __device__ __noinline__ void logistic_cta_pass(const LogisticArgs& a, const doub
     for (int w = 0; w < nwarps; ++w) s += wred[w * NA + j];
     red_out[d] = s;
   }
+  if (prof) { pc1 = clock64(); a.prof[7] += pc1 - pc0; }
 }
 
 static __device__ __forceinline__ void logistic_cta_dispatch(const LogisticArgs& a, const double* theta, double* wred,
                                                              double* red_s) {
+  if (a.p == 54) {  // covtype's feature count: compile-time row layout
+    if (a.fp64) logistic_cta_pass<56, true, 54>(a, theta, wred, red_s);
+    else logistic_cta_pass<56, false, 54>(a, theta, wred, red_s);
+    return;
+  }
   switch (a.pmax * 2 + (a.fp64 ? 1 : 0)) {
-    case 16: logistic_cta_pass<8, false>(a, theta, wred, red_s); break;
-    case 17: logistic_cta_pass<8, true>(a, theta, wred, red_s); break;
-    case 64: logistic_cta_pass<32, false>(a, theta, wred, red_s); break;
-    case 65: logistic_cta_pass<32, true>(a, theta, wred, red_s); break;
-    case 112: logistic_cta_pass<56, false>(a, theta, wred, red_s); break;
-    case 113: logistic_cta_pass<56, true>(a, theta, wred, red_s); break;
-    case 128: logistic_cta_pass<64, false>(a, theta, wred, red_s); break;
-    case 129: logistic_cta_pass<64, true>(a, theta, wred, red_s); break;
+    case 16: logistic_cta_pass<8, false, 0>(a, theta, wred, red_s); break;
+    case 17: logistic_cta_pass<8, true, 0>(a, theta, wred, red_s); break;
+    case 64: logistic_cta_pass<32, false, 0>(a, theta, wred, red_s); break;
+    case 65: logistic_cta_pass<32, true, 0>(a, theta, wred, red_s); break;
+    case 112: logistic_cta_pass<56, false, 0>(a, theta, wred, red_s); break;
+    case 113: logistic_cta_pass<56, true, 0>(a, theta, wred, red_s); break;
+    case 128: logistic_cta_pass<64, false, 0>(a, theta, wred, red_s); break;
+    case 129: logistic_cta_pass<64, true, 0>(a, theta, wred, red_s); break;
     default: break;
   }
 }
@@ -336,53 +452,70 @@ static __device__ __forceinline__ void logistic_cta_dispatch(const LogisticArgs&
 // Full logistic evaluation over the grid for the team's q (vector qid):
 // returns U, writes the gradient to vector gid.  `epoch` counts grid
 // barriers already passed by this kernel (identical in every CTA).
-static __device__ double logistic_eval_grid(const BlockTeam& T, const LogisticArgs& a, const VecStore& S, int qid,
-                                            int gid, double* wred, double* red_s, unsigned long long& epoch) {
+// Called by ALL threads of the CTA (the driver warp and the worker warps).
+static __device__ double logistic_eval_grid(const LogisticArgs& a, const VecStore& S, int qid, int gid, double* wred,
+                                            double* red_s, unsigned long long& epoch) {
   const int p = a.p;
   const int P2 = p + 2;
   const int64_t G = gridDim.x;
   const double* theta = S.v(qid);  // smem, contiguous (dstride 1)
-  // prior term 0.5 * |theta|^2 (kernels.py:92-95)
-  double pr = 0.0;
-  for (int d = threadIdx.x; d <= p; d += blockDim.x) pr += 0.5 * theta[d] * theta[d];
-  pr = T.sum(pr);
+  const bool prof = a.prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
+  long long c0 = prof ? clock64() : 0, c1;
 
   logistic_cta_dispatch(a, theta, wred, red_s);
   __syncthreads();
-  double* slot = a.pbuf + ((epoch & 1ULL) * G + blockIdx.x) * P2;
-  for (int d = threadIdx.x; d < P2; d += blockDim.x) slot[d] = red_s[d];
-  if (G > 1) grid_barrier(a.bar, epoch);
-  else __syncthreads();
-  epoch += 1;
-
-  // Every CTA reduces all partial slots in the same fixed order.
-  const double* base = a.pbuf + (((epoch - 1) & 1ULL) * G) * P2;
-  const int ngrp = ((int)blockDim.x / P2) > 1 ? (int)blockDim.x / P2 : 1;
-  double* grp = wred;  // reuse: ngrp * P2 doubles
-  for (int idx = threadIdx.x; idx < ngrp * P2; idx += blockDim.x) {
-    const int gi = idx / P2, d0 = idx % P2;
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-    int64_t b = gi;
-    for (; b + 3 * ngrp < G; b += 4 * ngrp) {
-      s0 += __ldcg(base + b * P2 + d0);
-      s1 += __ldcg(base + (b + ngrp) * P2 + d0);
-      s2 += __ldcg(base + (b + 2 * ngrp) * P2 + d0);
-      s3 += __ldcg(base + (b + 3 * ngrp) * P2 + d0);
-    }
-    for (; b < G; b += ngrp) s0 += __ldcg(base + b * P2 + d0);
-    grp[gi * P2 + d0] = (s0 + s1) + (s2 + s3);
+  if (prof) { c1 = clock64(); a.prof[1] += c1 - c0; c0 = c1; }
+  // Cross-CTA sum by exact fixed-point atomics into accumulator buffer
+  // epoch % 3 (see fx_split): integer addition is associative, so the result
+  // is independent of the order in which CTAs arrive -- deterministic.
+  unsigned long long* accb = reinterpret_cast<unsigned long long*>(a.pbuf);
+  const int64_t bstride = 2 * (int64_t)P2 + 2;
+  unsigned long long* cur = accb + (int64_t)(epoch % 3ULL) * bstride;
+  for (int d = threadIdx.x; d < P2; d += blockDim.x) {
+    long long hi, lo;
+    const bool ok = fx_split(red_s[d], hi, lo);
+    red_add_u64(cur + 2 * d, (unsigned long long)hi);
+    red_add_u64(cur + 2 * d + 1, (unsigned long long)lo);
+    if (!ok) red_add_u64(cur + 2 * P2, 1ULL);  // non-finite / out-of-range partial
   }
   __syncthreads();
+  if (threadIdx.x == 0) {
+    if (G > 1) red_release_add_u64(a.bar, 1ULL);
+    // prior term 0.5 |theta|^2 (kernels.py:92-95), computed by the thread
+    // that waits at the barrier anyway (left to right, bias first)
+    double pr = 0.5 * theta[p] * theta[p];
+    for (int d = 0; d < p; ++d) pr += 0.5 * theta[d] * theta[d];
+    red_s[1] = pr;
+    if (G > 1) {
+      const unsigned long long target = (epoch + 1) * (unsigned long long)G;
+      while (ld_relaxed_u64(a.bar) < target) {
+      }
+    }
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  }
+  __syncthreads();
+  // buffer (epoch+2)%3 was last read before this barrier by every CTA and is
+  // next accumulated after the following barrier: CTA 0 clears it now.
+  if (blockIdx.x == 0) {
+    unsigned long long* nxt = accb + (int64_t)((epoch + 2) % 3ULL) * bstride;
+    for (int i = threadIdx.x; i < bstride; i += blockDim.x) nxt[i] = 0ULL;
+  }
+  epoch += 1;
+  if (prof) { c1 = clock64(); a.prof[2] += c1 - c0; c0 = c1; }
+
   double* g = S.v(gid);
+  const bool bad = __ldcg(reinterpret_cast<const long long*>(cur + 2 * P2)) != 0;
   for (int d = threadIdx.x; d < P2; d += blockDim.x) {
-    double s = 0.0;
-    for (int gi = 0; gi < ngrp; ++gi) s += grp[gi * P2 + d];
+    const long long hi = __ldcg(reinterpret_cast<const long long*>(cur + 2 * d));
+    const long long lo = __ldcg(reinterpret_cast<const long long*>(cur + 2 * d + 1));
+    const double s = bad ? __longlong_as_double(0x7ff8000000000000LL) : fx_join(hi, lo);
     if (d <= p) g[d] = theta[d] - s;
     else red_s[0] = s;  // sum of log-likelihood terms
   }
   __syncthreads();
-  const double U = pr - red_s[0];
+  const double U = red_s[1] - red_s[0];
   __syncthreads();
+  if (prof) { c1 = clock64(); a.prof[3] += c1 - c0; }
   return U;
 }
 

@@ -45,21 +45,26 @@ __device__ __forceinline__ Key key_fold(Key k, uint64_t index) {
 struct Stream {
   uint64_t k0, k1;
   uint64_t c0, c1;  // words 2,3 of the counter stay (0, 1)
-  uint64_t buf[4];
+  uint64_t b0, b1, b2, b3;  // current block (scalars, not an array: stays in registers)
   int pos;
 
   __device__ __forceinline__ void init(Key k) {
     k0 = k.hi; k1 = k.lo; c0 = 0; c1 = 0; pos = 4;
+    b0 = b1 = b2 = b3 = 0;
   }
   __device__ __forceinline__ uint64_t next_u64() {
-    if (pos < 4) return buf[pos++];
+    if (pos < 4) {
+      const uint64_t v = pos == 1 ? b1 : (pos == 2 ? b2 : (pos == 3 ? b3 : b0));
+      ++pos;
+      return v;
+    }
     c0 += 1;
     if (c0 == 0) c1 += 1;
     uint64_t c[4] = {c0, c1, 0, 1};
     philox4x64_10(c, k0, k1);
-    buf[0] = c[0]; buf[1] = c[1]; buf[2] = c[2]; buf[3] = c[3];
+    b0 = c[0]; b1 = c[1]; b2 = c[2]; b3 = c[3];
     pos = 1;
-    return buf[0];
+    return b0;
   }
   __device__ __forceinline__ double next_double() {
     return (double)(next_u64() >> 11) * (1.0 / 9007199254740992.0);

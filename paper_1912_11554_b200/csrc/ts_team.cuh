@@ -44,6 +44,31 @@ struct ThreadTeam {
   __device__ __forceinline__ void sum2(double& a, double& b) const {}
 };
 
+// One warp owns the chain (driver warp of a persistent data-parallel CTA):
+// reductions are shuffle trees to lane 0 plus a broadcast, so every lane
+// holds the bitwise-identical value and no CTA barrier is involved.
+struct WarpTeam {
+  static constexpr bool kBlock = false;
+  __device__ __forceinline__ int rank() const { return threadIdx.x & 31; }
+  __device__ __forceinline__ int size() const { return 32; }
+  __device__ __forceinline__ bool leader() const { return (threadIdx.x & 31) == 0; }
+  __device__ __forceinline__ void sync() const { __syncwarp(); }
+  __device__ __forceinline__ double sum(double x) const {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x = __dadd_rn(x, __shfl_down_sync(0xffffffffu, x, o));
+    return __shfl_sync(0xffffffffu, x, 0);
+  }
+  __device__ __forceinline__ void sum2(double& a, double& b) const {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a = __dadd_rn(a, __shfl_down_sync(0xffffffffu, a, o));
+      b = __dadd_rn(b, __shfl_down_sync(0xffffffffu, b, o));
+    }
+    a = __shfl_sync(0xffffffffu, a, 0);
+    b = __shfl_sync(0xffffffffu, b, 0);
+  }
+};
+
 // Deterministic CTA-wide reduction.  `scratch` holds >= 2*32 doubles.
 struct BlockTeam {
   static constexpr bool kBlock = true;

@@ -133,8 +133,16 @@ struct Engine {
   unsigned long long* prof = nullptr;  // CTA 0 / thread 0 only (profiling builds of a run)
   long long prof_last = 0;
 
-  __device__ __forceinline__ double* v(int id) const { return S.v(id); }
-  __device__ __forceinline__ int64_t ds() const { return S.dstride; }
+  // CTA/warp teams keep vectors contiguous in shared memory (unit component
+  // stride, 32-bit offsets); thread teams interleave chains in global memory.
+  __device__ __forceinline__ double* v(int id) const {
+    if constexpr (Team::kUnitStride) return S.base + id * (int)S.vstride;
+    else return S.v(id);
+  }
+  __device__ __forceinline__ int64_t ds() const {
+    if constexpr (Team::kUnitStride) return 1;
+    else return S.dstride;
+  }
 
   // ---------------------------------------------------------------- trace
   __device__ void ev(int kind, int a, int b, int c, int e = 0) {
@@ -406,6 +414,50 @@ struct Engine {
         r[d * s] = __dmul_rn(inj[d * inj_ds], __ddiv_rn(1.0, __dsqrt_rn(inv[d * s])));
       return;
     }
+    if constexpr (Team::kWarp) {
+      // Warp-parallel ziggurat: lane l tries normal (done + l) on stream word
+      // (w + l), i.e. assuming the preceding normals of the chunk each took
+      // one word (the ziggurat fast path, ~99%).  The first lane that falls
+      // off the fast path is resolved with the sequential generator, and the
+      // chunk restarts after it: the values are exactly numpy's sequence.
+      const int lane = T.rank();
+      uint64_t w = 0;  // next unread word of the stream
+      int done = 0;
+      while (done < D) {
+        const uint64_t my = w + lane;
+        uint64_t c[4] = {my / 4 + 1, 0, 0, 1};
+        if (c[0] == 0) c[1] = 1;
+        philox4x64_10(c, nkey.hi, nkey.lo);
+        const int o = (int)(my & 3);
+        uint64_t rr = o == 0 ? c[0] : (o == 1 ? c[1] : (o == 2 ? c[2] : c[3]));
+        const int idx = (int)(rr & 0xff);
+        rr >>= 8;
+        const int sign = (int)(rr & 1);
+        const uint64_t rabs = (rr >> 1) & 0x000fffffffffffffULL;
+        double z = __dmul_rn((double)rabs, TS_ZIG_WI[idx]);
+        if (sign) z = -z;
+        const bool fast = rabs < TS_ZIG_KI[idx];
+        const int want = min(32, D - done);
+        const unsigned slow = __ballot_sync(0xffffffffu, !fast) & (want == 32 ? 0xffffffffu : ((1u << want) - 1u));
+        const int nfast = slow ? __ffs(slow) - 1 : want;
+        if (lane < nfast) r[(done + lane) * s] = __dmul_rn(z, __ddiv_rn(1.0, __dsqrt_rn(inv[(done + lane) * s])));
+        done += nfast;
+        w += (uint64_t)nfast;
+        if (slow) {  // normal `done` leaves the fast path: replay it sequentially
+          Stream ns;
+          ns.init(nkey);
+          ns.c0 = w / 4;
+          for (int k = 0; k < (int)(w & 3); ++k) (void)ns.next_u64();
+          if ((w & 3) == 0) ns.pos = 4;
+          const double zs = ns.normal();
+          if (lane == 0) r[done * s] = __dmul_rn(zs, __ddiv_rn(1.0, __dsqrt_rn(inv[done * s])));
+          w = (ns.pos == 4) ? ns.c0 * 4 : (ns.c0 - 1) * 4 + (uint64_t)ns.pos;
+          done += 1;
+        }
+      }
+      __syncwarp();
+      return;
+    }
     Stream ns;
     ns.init(nkey);
     for (int d = 0; d < D; ++d) {
@@ -496,22 +548,7 @@ struct Engine {
   __device__ __noinline__ double find_step_size(Key key, double init, const double* inj, int64_t inj_ds) {
     const double target = 0.5;
     // rng.generator() of the given key directly (not a fold)
-    {
-      double* r = v(V_R0);
-      const double* inv = v(V_INV);
-      const int64_t s = ds();
-      if (inj != nullptr) {
-        for (int d = T.rank(); d < D; d += T.size())
-          r[d * s] = __dmul_rn(inj[d * inj_ds], __ddiv_rn(1.0, __dsqrt_rn(inv[d * s])));
-      } else {
-        Stream ns;
-        ns.init(key);
-        for (int d = 0; d < D; ++d) {
-          const double z = ns.normal();
-          if ((d % T.size()) == T.rank()) r[d * s] = __dmul_rn(z, __ddiv_rn(1.0, __dsqrt_rn(inv[d * s])));
-        }
-      }
-    }
+    draw_momentum(V_R0, key, inj, inj_ds);
     const double h0 = hamiltonian(U0, V_R0);
     double eps = init;
     const int direction = accept_prob(h0, eps) > target ? 1 : -1;

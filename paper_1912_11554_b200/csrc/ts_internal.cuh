@@ -82,21 +82,23 @@ struct LogisticW {
   int* cmd;  // smem: [0] 1 = evaluate / 0 = exit, [1] q vector id, [2] gradient vector id
   unsigned long long epoch;
   template <class Team>
-  __device__ double eval(const Team&, const VecStore& S, int q, int g) {
+  __device__ double eval(const Team&, const VecStore&, int q, int g) {  // driver warp
     if (threadIdx.x == 0) { cmd[0] = 1; cmd[1] = q; cmd[2] = g; }
-    __syncthreads();  // wakes the worker warps (and publishes q)
-    return logistic_eval_grid(a, S, q, g, wred, red_s, epoch);
+    cta_bar(2);  // start: publishes q and the command to the worker warps
+    cta_bar(3);  // done: gradient written to vector g, U in red_s
+    return red_s[1] - red_s[0];
   }
   __device__ void serve(const VecStore& S) {  // worker warps
     for (;;) {
-      __syncthreads();
+      cta_bar(2);
       if (cmd[0] == 0) break;
       logistic_eval_grid(a, S, cmd[1], cmd[2], wred, red_s, epoch);
+      cta_bar(3);
     }
   }
   __device__ void release_workers() {  // driver warp, once at the end
     if (threadIdx.x == 0) cmd[0] = 0;
-    __syncthreads();
+    cta_bar(2);
   }
 };
 
@@ -248,7 +250,6 @@ __global__ void __launch_bounds__(256, 1) k_block_op(MW mw, int D, int nslots, i
     mw.a.stages = reinterpret_cast<unsigned char*>(pb);
     mw.a.mbar = reinterpret_cast<uint64_t*>(pb + (size_t)nwarps * mw.a.nstage * mw.a.stage_bytes);
     mw.a.pipe = reinterpret_cast<WarpPipe*>(mw.a.mbar + nwarps * mw.a.nstage);
-    logistic_pipeline_init(mw.a);
     if ((threadIdx.x >> 5) == 0) {
       // driver warp: the whole NUTS state machine, warp-synchronous.  The
       // engine is a local object whose member functions are all inlined, so
@@ -265,9 +266,10 @@ __global__ void __launch_bounds__(256, 1) k_block_op(MW mw, int D, int nslots, i
       do_op(E, A, chain, writer);
       E.M.release_workers();
     } else {
+      logistic_pipeline_init(mw.a);
       mw.serve(S);
+      logistic_pipeline_drain(mw.a);
     }
-    logistic_pipeline_drain(mw.a);
   }
 }
 

@@ -24,7 +24,9 @@ int launch_block_logistic(const ts_model* m, int nslots, OpArgs& A, cudaStream_t
   TS_CUDA(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   // per-warp TMA ring: as many stages (<= 4) as shared memory allows
   const int stage_bytes = ((128 * m->p + 32) + 127) / 128 * 128;
-  int nstage = 4;
+  // Two stages per worker warp: enough bytes in flight to saturate HBM, and
+  // the rest of the 256 KB L1/shared array stays L1 for the engine's stack.
+  int nstage = 2;
   if (const char* e = getenv("TS_NSTAGE")) nstage = atoi(e) < 1 ? 1 : (atoi(e) > 4 ? 4 : atoi(e));  // profiling
   auto need = [&](int ns) { return base + (size_t)nwarps * ns * (stage_bytes + 8) + nwarps * 16; };
   while (nstage > 1 && need(nstage) > (size_t)smem_max) --nstage;

@@ -153,6 +153,17 @@ __device__ __forceinline__ void grid_barrier(unsigned long long* bar, unsigned l
   __syncthreads();
 }
 
+// ------------------------------------------------------------- worker group
+// Warp 0 of each CTA drives the chain; warps 1.. stream the data.  The pass
+// code below runs on the worker warps only and synchronises with named
+// barrier 1; barriers 2/3 hand a pass from the driver to the workers and back.
+__device__ __forceinline__ int wk_tid() { return (int)threadIdx.x - 32; }
+__device__ __forceinline__ int wk_threads() { return (int)blockDim.x - 32; }
+__device__ __forceinline__ int wk_warp() { return (int)(threadIdx.x >> 5) - 1; }
+__device__ __forceinline__ int wk_nwarps() { return (int)(blockDim.x >> 5) - 1; }
+__device__ __forceinline__ void wk_sync() { asm volatile("bar.sync 1, %0;" ::"r"(wk_threads()) : "memory"); }
+__device__ __forceinline__ void cta_bar(int id) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"((int)blockDim.x) : "memory"); }
+
 // ------------------------------------------------------------- tile pipeline
 struct WarpTiles {
   int64_t first;  // first tile of this warp
@@ -161,7 +172,7 @@ struct WarpTiles {
 };
 
 __device__ __forceinline__ WarpTiles warp_tiles(const LogisticArgs& a) {
-  const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int warp = wk_warp(), nwarps = wk_nwarps();
   const int64_t G = gridDim.x;
   const int64_t t_begin = (a.ntiles * (int64_t)blockIdx.x) / G;
   const int64_t t_end = (a.ntiles * ((int64_t)blockIdx.x + 1)) / G;
@@ -189,7 +200,7 @@ struct Producer {
   uint64_t pol;
 
   __device__ __forceinline__ void init(const LogisticArgs& a, const WarpTiles& wt, unsigned long long issued) {
-    const int warp = threadIdx.x >> 5;
+    const int warp = wk_warp();
     nstage = a.nstage;
     stage_bytes = a.stage_bytes;
     ring = a.stages + (int64_t)warp * nstage * stage_bytes;
@@ -218,26 +229,27 @@ struct Producer {
   }
 };
 
-// Kernel prologue (all threads of the CTA): mbarriers and pipe counters.
+// Kernel prologue (worker warps): mbarriers and pipe counters.
 static __device__ void logistic_pipeline_init(const LogisticArgs& a) {
-  const int nwarps = blockDim.x >> 5;
-  for (int i = threadIdx.x; i < nwarps * a.nstage; i += blockDim.x) mbar_init(a.mbar + i, 1);
-  for (int i = threadIdx.x; i < nwarps; i += blockDim.x) { a.pipe[i].issued = 0; a.pipe[i].consumed = 0; }
+  const int nwarps = wk_nwarps();
+  for (int i = wk_tid(); i < nwarps * a.nstage; i += wk_threads()) mbar_init(a.mbar + i, 1);
+  for (int i = wk_tid(); i < nwarps; i += wk_threads()) { a.pipe[i].issued = 0; a.pipe[i].consumed = 0; }
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  __syncthreads();
+  wk_sync();
 }
 
-// Kernel epilogue: wait for the tiles the producer prefetched for a pass that
-// never came, so no bulk copy targets the shared memory of an exited CTA.
+// Kernel epilogue (worker warps): wait for the tiles the producer prefetched
+// for a pass that never came, so no bulk copy targets the shared memory of an
+// exited CTA.
 static __device__ void logistic_pipeline_drain(const LogisticArgs& a) {
-  const int warp = threadIdx.x >> 5;
+  const int warp = wk_warp();
   const WarpTiles wt = warp_tiles(a);
   if (wt.count > 0) {
     const unsigned long long c = a.pipe[warp].consumed, iss = a.pipe[warp].issued;
     for (unsigned long long seq = c; seq < iss; ++seq)
       mbar_wait(a.mbar + warp * a.nstage + (int)(seq % a.nstage), (uint32_t)((seq / a.nstage) & 1ULL));
   }
-  __syncthreads();
+  wk_sync();
 }
 
 // Lane's row of a tile in shared memory -> x[0..PMAX) (zeros past p), y.
@@ -274,13 +286,13 @@ __device__ __forceinline__ void row_from_stage(const unsigned char* sb, int p_rt
 // red_out[0..p) = sum resid*x_j, red_out[p] = sum resid, red_out[p+1] = sum (y eta - log1pexp)
 // (wred: >= nwarps*(PMAX+2) doubles of scratch).
 template <int PMAX, bool FP64, int PE>
-__device__ __noinline__ void logistic_cta_pass(const LogisticArgs& a, const double* __restrict__ theta_s, double* wred,
-                                               double* red_out) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+__device__ __forceinline__ void logistic_cta_pass(const LogisticArgs& a, const double* __restrict__ theta_s, double* wred,
+                                                  double* red_out) {
+  const int lane = threadIdx.x & 31, warp = wk_warp(), nwarps = wk_nwarps();
   const int p = PE > 0 ? PE : a.p;
   constexpr int NA = PMAX + 2;
   const WarpTiles wt = warp_tiles(a);
-  const bool prof = a.prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
+  const bool prof = a.prof != nullptr && blockIdx.x == 0 && wk_tid() == 0;
   long long pc0 = prof ? clock64() : 0, pc1;
 
   using acc_t = typename std::conditional<FP64, double, float>::type;
@@ -295,15 +307,15 @@ __device__ __noinline__ void logistic_cta_pass(const LogisticArgs& a, const doub
     // theta rounded to float once per pass (PMAX+1 conversions per CTA, not
     // per thread), then broadcast with LDS.128 (wred is free until the end)
     float* t32 = reinterpret_cast<float*>(wred);
-    for (int j = threadIdx.x; j <= PMAX; j += blockDim.x) t32[j] = (j < p) ? (float)theta_s[j] : (j == PMAX ? (float)theta_s[p] : 0.f);
-    __syncthreads();
+    for (int j = wk_tid(); j <= PMAX; j += wk_threads()) t32[j] = (j < p) ? (float)theta_s[j] : (j == PMAX ? (float)theta_s[p] : 0.f);
+    wk_sync();
 #pragma unroll
     for (int j = 0; j < PMAX; j += 4) {
       const float4 v = reinterpret_cast<const float4*>(t32)[j / 4];
       th32[j] = v.x; th32[j + 1] = v.y; th32[j + 2] = v.z; th32[j + 3] = v.w;
     }
     thb32 = t32[PMAX];
-    __syncthreads();
+    wk_sync();
   }
 
   if (wt.count > 0) {
@@ -418,9 +430,9 @@ __device__ __noinline__ void logistic_cta_pass(const LogisticArgs& a, const doub
     if (i < cnt && colbase + i < NA && (NP >= 32 || (lane % (32 / NP)) == 0)) wred[warp * NA + colbase + i] = (double)v[i];
   }
   if (prof) { pc1 = clock64(); a.prof[6] += pc1 - pc0; pc0 = pc1; }
-  __syncthreads();
+  wk_sync();
   // CTA reduction in warp order; output index: [0,p) features, p bias, p+1 loglik
-  for (int d = threadIdx.x; d < p + 2; d += blockDim.x) {
+  for (int d = wk_tid(); d < p + 2; d += wk_threads()) {
     const int j = (d < p) ? d : (d == p ? PMAX : PMAX + 1);
     double s = 0.0;
     for (int w = 0; w < nwarps; ++w) s += wred[w * NA + j];
@@ -449,21 +461,21 @@ static __device__ __forceinline__ void logistic_cta_dispatch(const LogisticArgs&
   }
 }
 
-// Full logistic evaluation over the grid for the team's q (vector qid):
-// returns U, writes the gradient to vector gid.  `epoch` counts grid
-// barriers already passed by this kernel (identical in every CTA).
-// Called by ALL threads of the CTA (the driver warp and the worker warps).
-static __device__ double logistic_eval_grid(const LogisticArgs& a, const VecStore& S, int qid, int gid, double* wred,
-                                            double* red_s, unsigned long long& epoch) {
+// Full logistic evaluation over the grid for q (vector qid): leaves U in
+// red_s (U = red_s[1] - red_s[0]) and the gradient in vector gid.  `epoch`
+// counts grid barriers already passed by this kernel (identical in every
+// CTA).  Called by the WORKER warps of the CTA.
+static __device__ void logistic_eval_grid(const LogisticArgs& a, const VecStore& S, int qid, int gid, double* wred,
+                                          double* red_s, unsigned long long& epoch) {
   const int p = a.p;
   const int P2 = p + 2;
   const int64_t G = gridDim.x;
   const double* theta = S.v(qid);  // smem, contiguous (dstride 1)
-  const bool prof = a.prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
+  const bool prof = a.prof != nullptr && blockIdx.x == 0 && wk_tid() == 0;
   long long c0 = prof ? clock64() : 0, c1;
 
   logistic_cta_dispatch(a, theta, wred, red_s);
-  __syncthreads();
+  wk_sync();
   if (prof) { c1 = clock64(); a.prof[1] += c1 - c0; c0 = c1; }
   // Cross-CTA sum by exact fixed-point atomics into accumulator buffer
   // epoch % 3 (see fx_split): integer addition is associative, so the result
@@ -471,15 +483,15 @@ static __device__ double logistic_eval_grid(const LogisticArgs& a, const VecStor
   unsigned long long* accb = reinterpret_cast<unsigned long long*>(a.pbuf);
   const int64_t bstride = 2 * (int64_t)P2 + 2;
   unsigned long long* cur = accb + (int64_t)(epoch % 3ULL) * bstride;
-  for (int d = threadIdx.x; d < P2; d += blockDim.x) {
+  for (int d = wk_tid(); d < P2; d += wk_threads()) {
     long long hi, lo;
     const bool ok = fx_split(red_s[d], hi, lo);
     red_add_u64(cur + 2 * d, (unsigned long long)hi);
     red_add_u64(cur + 2 * d + 1, (unsigned long long)lo);
     if (!ok) red_add_u64(cur + 2 * P2, 1ULL);  // non-finite / out-of-range partial
   }
-  __syncthreads();
-  if (threadIdx.x == 0) {
+  wk_sync();
+  if (wk_tid() == 0) {
     if (G > 1) red_release_add_u64(a.bar, 1ULL);
     // prior term 0.5 |theta|^2 (kernels.py:92-95), computed by the thread
     // that waits at the barrier anyway (left to right, bias first)
@@ -493,30 +505,26 @@ static __device__ double logistic_eval_grid(const LogisticArgs& a, const VecStor
     }
     asm volatile("fence.acq_rel.gpu;" ::: "memory");
   }
-  __syncthreads();
+  wk_sync();
   // buffer (epoch+2)%3 was last read before this barrier by every CTA and is
   // next accumulated after the following barrier: CTA 0 clears it now.
   if (blockIdx.x == 0) {
     unsigned long long* nxt = accb + (int64_t)((epoch + 2) % 3ULL) * bstride;
-    for (int i = threadIdx.x; i < bstride; i += blockDim.x) nxt[i] = 0ULL;
+    for (int i = wk_tid(); i < bstride; i += wk_threads()) nxt[i] = 0ULL;
   }
   epoch += 1;
   if (prof) { c1 = clock64(); a.prof[2] += c1 - c0; c0 = c1; }
 
   double* g = S.v(gid);
   const bool bad = __ldcg(reinterpret_cast<const long long*>(cur + 2 * P2)) != 0;
-  for (int d = threadIdx.x; d < P2; d += blockDim.x) {
+  for (int d = wk_tid(); d < P2; d += wk_threads()) {
     const long long hi = __ldcg(reinterpret_cast<const long long*>(cur + 2 * d));
     const long long lo = __ldcg(reinterpret_cast<const long long*>(cur + 2 * d + 1));
     const double s = bad ? __longlong_as_double(0x7ff8000000000000LL) : fx_join(hi, lo);
     if (d <= p) g[d] = theta[d] - s;
     else red_s[0] = s;  // sum of log-likelihood terms
   }
-  __syncthreads();
-  const double U = red_s[1] - red_s[0];
-  __syncthreads();
   if (prof) { c1 = clock64(); a.prof[3] += c1 - c0; }
-  return U;
 }
 
 }  // namespace ts

@@ -36,6 +36,8 @@ struct VecStore {
 
 struct ThreadTeam {
   static constexpr bool kBlock = false;
+  static constexpr bool kUnitStride = false;  // chains interleaved in global memory
+  static constexpr bool kWarp = false;
   __device__ __forceinline__ int rank() const { return 0; }
   __device__ __forceinline__ int size() const { return 1; }
   __device__ __forceinline__ bool leader() const { return true; }
@@ -49,6 +51,8 @@ struct ThreadTeam {
 // holds the bitwise-identical value and no CTA barrier is involved.
 struct WarpTeam {
   static constexpr bool kBlock = false;
+  static constexpr bool kUnitStride = true;  // vectors contiguous in shared memory
+  static constexpr bool kWarp = true;
   __device__ __forceinline__ int rank() const { return threadIdx.x & 31; }
   __device__ __forceinline__ int size() const { return 32; }
   __device__ __forceinline__ bool leader() const { return (threadIdx.x & 31) == 0; }
@@ -72,6 +76,8 @@ struct WarpTeam {
 // Deterministic CTA-wide reduction.  `scratch` holds >= 2*32 doubles.
 struct BlockTeam {
   static constexpr bool kBlock = true;
+  static constexpr bool kUnitStride = true;
+  static constexpr bool kWarp = false;
   double* scratch;
   __device__ __forceinline__ int rank() const { return threadIdx.x; }
   __device__ __forceinline__ int size() const { return blockDim.x; }

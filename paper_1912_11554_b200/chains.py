@@ -81,6 +81,16 @@ class ChainResult:
         return int(np.count_nonzero(self.stats_array[:, 2]))
 
 
+def shard_range(num_chains: int, rank: int, world: int) -> list[int]:
+    """Chain ids owned by GPU/rank `rank` of `world`: a contiguous block.
+
+    Chains are independent and each is a pure function of its key, so any
+    partition gives the same per-chain output (no collective needed)."""
+    if not 0 <= rank < world:
+        raise ValueError("rank must lie in [0, world)")
+    return list(range(rank * num_chains // world, (rank + 1) * num_chains // world))
+
+
 def chain_keys(seed: int, num_chains: int) -> list[RngKey]:
     carry = RngKey.from_seed(seed)
     keys = []
@@ -206,7 +216,7 @@ def run(config: RunConfig, model: Optional[TargetModel] = None, devices: Optiona
         devices = [torch.cuda.current_device()]
     devices = list(devices)
     C = config.num_chains
-    shards = [list(range(g * C // len(devices), (g + 1) * C // len(devices))) for g in range(len(devices))]
+    shards = [shard_range(C, g, len(devices)) for g in range(len(devices))]
     t0 = time.perf_counter_ns()
     runs: list = [None] * len(devices)
     errors: list = []

@@ -316,9 +316,9 @@ extern "C" int ts_run_chains(const ts_model* m, const ts_run_cfg* rc, const uint
       TS_CUDA(cudaStreamSynchronize(st));
       const double n = h[10] ? (double)h[10] : 1.0;
       fprintf(stderr,
-              "TS_PROF evals=%llu cycles/eval: in-eval %.0f (pass %.0f [entry %.0f loop %.0f warpred %.0f ctared %.0f] "
-              "barrier %.0f reduce %.0f) between-evals %.0f\n",
-              h[10], h[8] / n, h[1] / n, h[4] / n, h[5] / n, h[6] / n, h[7] / n, h[2] / n, h[3] / n, h[9] / n);
+              "TS_PROF evals=%llu wasted=%llu cycles/eval: post-to-result %.0f (pass %.0f [entry %.0f loop %.0f "
+              "warpred %.0f ctared %.0f] barrier %.0f reduce %.0f) result-to-next-post %.0f\n",
+              h[10], h[11], h[8] / n, h[1] / n, h[4] / n, h[5] / n, h[6] / n, h[7] / n, h[2] / n, h[3] / n, h[9] / n);
     }
     return TS_OK;
   }

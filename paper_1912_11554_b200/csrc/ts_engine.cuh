@@ -33,6 +33,7 @@ enum Vid : int {
   V_TPQ, V_TPG,                       // running subtree proposal
   V_MSUM,                             // tree momentum sum (output of build_tree)
   V_WMEAN, V_WM2,                     // Welford accumulator
+  V_NQ, V_NR, V_NG,                   // speculative next leaf (drifted q, r_half, gradient)
   V_SLOT0                             // NodeStore slots: 5 vectors each
 };
 constexpr int kSlotVecs = 5;  // FQ, FR, CUMF, PQ, PG
@@ -130,8 +131,11 @@ struct Engine {
   // keeps them out of the local-memory path when shared memory crowds L1.
   SlotScalars* ss;
   unsigned long long n_evals;
+  unsigned long long n_wasted;  // speculative passes discarded (tree stopped early)
+  double pending_u;
   unsigned long long* prof = nullptr;  // CTA 0 / thread 0 only (profiling builds of a run)
   long long prof_last = 0;
+  long long prof_post = 0;
 
   // CTA/warp teams keep vectors contiguous in shared memory (unit component
   // stride, 32-bit offsets); thread teams interleave chains in global memory.
@@ -176,18 +180,29 @@ struct Engine {
 
   // model evaluation at vector qid -> U (non-finite -> +inf), gradient -> gid
   __device__ double eval(int qid, int gid) {
+    post_eval(qid, gid);
+    return wait_eval();
+  }
+  // Asynchronous form (grid mode: the worker warps stream while the driver
+  // continues); synchronous models evaluate in post and return in wait.
+  __device__ void post_eval(int qid, int gid) {
     T.sync();
-    long long c0 = 0;
-    const bool pr = prof != nullptr && T.leader();
-    if (pr) {  // profiling: [8] cycles inside model evaluations, [9] between them
-      c0 = clock64();
+    if (prof != nullptr && T.leader()) {  // profiling: [9] cycles between passes
+      const long long c0 = clock64();
       if (prof_last) prof[9] += c0 - prof_last;
+      prof_post = c0;
     }
-    double u = M.eval(T, S, qid, gid);
+    if constexpr (Model::kAsync) M.post(qid, gid);
+    else pending_u = M.eval(T, S, qid, gid);
+  }
+  __device__ double wait_eval() {
+    double u;
+    if constexpr (Model::kAsync) u = M.wait();
+    else u = pending_u;
     T.sync();
-    if (pr) {
+    if (prof != nullptr && T.leader()) {  // [8] cycles from post to result, [10] passes
       const long long c1 = clock64();
-      prof[8] += c1 - c0;
+      prof[8] += c1 - prof_post;
       prof[10] += 1;
       prof_last = c1;
     }
@@ -311,6 +326,87 @@ struct Engine {
     for (int d = T.rank(); d < D; d += T.size()) c[d * s] = __dadd_rn(c[d * s], r[d * s]);
   }
 
+  // Split leapfrog for the speculative pipeline: drift from the current leaf
+  // into (NQ, NR = r_half); after the pass, the new leaf becomes current and
+  // gets its kick (same arithmetic as leapfrog()).
+  __device__ void drift_next(double eps) {
+    const double half = __dmul_rn(0.5, eps);
+    const double* q = v(V_CQ);
+    const double* r = v(V_CR);
+    const double* g = v(V_CG);
+    double* nq = v(V_NQ);
+    double* nr = v(V_NR);
+    const double* inv = v(V_INV);
+    const int64_t s = ds();
+    for (int d = T.rank(); d < D; d += T.size()) {
+      const double rh = __dsub_rn(r[d * s], __dmul_rn(half, g[d * s]));
+      nr[d * s] = rh;
+      nq[d * s] = __dadd_rn(q[d * s], __dmul_rn(eps, __dmul_rn(inv[d * s], rh)));
+    }
+  }
+  __device__ void advance_leaf(double eps, double u) {
+    const double half = __dmul_rn(0.5, eps);
+    double* q = v(V_CQ);
+    double* r = v(V_CR);
+    double* g = v(V_CG);
+    const double* nq = v(V_NQ);
+    const double* nr = v(V_NR);
+    const double* ng = v(V_NG);
+    const int64_t s = ds();
+    for (int d = T.rank(); d < D; d += T.size()) {
+      const double gg = ng[d * s];
+      q[d * s] = nq[d * s];
+      g[d * s] = gg;
+      r[d * s] = __dsub_rn(nr[d * s], __dmul_rn(half, gg));
+    }
+    cur_U = u;
+  }
+
+  // Bookkeeping of leaf n (tree.py:403-450): divergence exit, even-leaf store
+  // at slot popcount(n), odd-leaf merges + U-turn checks down to i_min.
+  __device__ int leaf_book(unsigned long long n, double h, double delta, Stream& draws, bool forward) {
+    const double thr = cfg.threshold;
+    const int pc = __popcll(n);
+    if (!(isfinite(delta) && delta <= thr)) {
+      const double metro = isfinite(delta) ? exp(-delta) : 0.0;
+      ev_lw(-kInf());
+      running_from_leaf((int)n, -kInf(), metro, h);
+      merge_out(pc, draws);
+      return kStopDiv;
+    }
+    const double lw = -h;
+    const double metro = delta > 0 ? exp(-delta) : 1.0;
+    ev_lw(lw);
+    if ((n & 1ULL) == 0) {
+      const int slot = pc;
+      copy(slot_vec(slot, 0), V_CQ); copy(slot_vec(slot, 1), V_CR); copy(slot_vec(slot, 2), V_CUM);
+      copy(slot_vec(slot, 3), V_CQ); copy(slot_vec(slot, 4), V_CG);
+      SlotScalars& L = ss[slot];
+      L.lw = lw; L.metro = metro; L.pU = cur_U; L.pH = h; L.fU = cur_U;
+      L.count = 1; L.pidx = (int)n; L.leaf = (int)n;
+      occupied_mask |= 1 << slot;
+      ev(kEvWrite, (int)n, slot, 0);
+      return kStopNone;
+    }
+    int slot = pc - 1;
+    const int i_min = slot - __popcll(((n + 1) & ~n) - 1) + 1;
+    running_from_leaf((int)n, lw, metro, h);
+    while (slot >= i_min) {
+      ev(kEvCheck, (int)n, slot, ss[slot].leaf);
+      merge_slot(slot, draws.next_double());
+      if (running_turning(forward)) {
+        merge_out(slot, draws);
+        return kStopTurn;
+      }
+      --slot;
+    }
+    // summaries[i_min] = running: first/cum_first already equal slot i_min's
+    copy(slot_vec(i_min, 3), V_TPQ); copy(slot_vec(i_min, 4), V_TPG);
+    SlotScalars& L = ss[i_min];
+    L.lw = r_lw; L.metro = r_metro; L.pU = r_pU; L.pH = r_pH; L.count = r_count; L.pidx = r_pidx;
+    return kStopNone;
+  }
+
   // build_tree_iterative (tree.py:344-453).  Input: frontier in CQ/CR/CG/cur_U.
   // Output: running subtree (FQ/FR/CUMF + TPQ/TPG + r_* scalars), last leaf in
   // CQ/CR/CG/cur_U, momentum sum in V_MSUM.
@@ -323,6 +419,7 @@ struct Engine {
     fill(V_CUM, 0.0);
     const double thr = cfg.threshold;
     const bool forward = eps > 0;
+    (void)thr;
     int stop = kStopNone;
     if (depth == 0) {
       leapfrog(eps);
@@ -337,52 +434,39 @@ struct Engine {
       stop = div ? kStopDiv : kStopNone;
     } else {
       const unsigned long long nleaves = 1ULL << depth;
-      for (unsigned long long n = 0; n < nleaves; ++n) {
-        leapfrog(eps);
-        add_cum();
-        double h, delta;
-        leaf_energy(h_ref, h, delta);
-        const int pc = __popcll(n);
-        if (!(isfinite(delta) && delta <= thr)) {
-          const double metro = isfinite(delta) ? exp(-delta) : 0.0;
-          ev_lw(-kInf());
-          running_from_leaf((int)n, -kInf(), metro, h);
-          merge_out(pc, draws);
-          stop = kStopDiv;
-          break;
-        }
-        const double lw = -h;
-        const double metro = delta > 0 ? exp(-delta) : 1.0;
-        ev_lw(lw);
-        if ((n & 1ULL) == 0) {
-          const int slot = pc;
-          copy(slot_vec(slot, 0), V_CQ); copy(slot_vec(slot, 1), V_CR); copy(slot_vec(slot, 2), V_CUM);
-          copy(slot_vec(slot, 3), V_CQ); copy(slot_vec(slot, 4), V_CG);
-          SlotScalars& L = ss[slot];
-          L.lw = lw; L.metro = metro; L.pU = cur_U; L.pH = h; L.fU = cur_U;
-          L.count = 1; L.pidx = (int)n; L.leaf = (int)n;
-          occupied_mask |= 1 << slot;
-          ev(kEvWrite, (int)n, slot, 0);
-        } else {
-          int slot = pc - 1;
-          const int i_min = slot - __popcll(((n + 1) & ~n) - 1) + 1;
-          running_from_leaf((int)n, lw, metro, h);
-          bool turned = false;
-          while (slot >= i_min) {
-            ev(kEvCheck, (int)n, slot, ss[slot].leaf);
-            merge_slot(slot, draws.next_double());
-            if (running_turning(forward)) {
-              merge_out(slot, draws);
-              turned = true;
-              break;
-            }
-            --slot;
+      if constexpr (Model::kAsync) {
+        // Speculative pipelining (grid mode): as soon as leaf n's gradient is
+        // back, drift to leaf n+1 and post its data pass to the worker warps,
+        // then do leaf n's bookkeeping while they stream.  If the bookkeeping
+        // stops the tree (U-turn / divergence), the posted pass is waited for
+        // and discarded; the last leaf of a tree is never speculated.
+        drift_next(eps);
+        post_eval(V_NQ, V_NG);
+        for (unsigned long long n = 0; n < nleaves; ++n) {
+          const double u = wait_eval();
+          advance_leaf(eps, u);
+          add_cum();
+          double h, delta;
+          leaf_energy(h_ref, h, delta);
+          const bool spec = n + 1 < nleaves;
+          if (spec) {
+            drift_next(eps);
+            post_eval(V_NQ, V_NG);
           }
-          if (turned) { stop = kStopTurn; break; }
-          // summaries[i_min] = running: first/cum_first already equal slot i_min's
-          copy(slot_vec(i_min, 3), V_TPQ); copy(slot_vec(i_min, 4), V_TPG);
-          SlotScalars& L = ss[i_min];
-          L.lw = r_lw; L.metro = r_metro; L.pU = r_pU; L.pH = r_pH; L.count = r_count; L.pidx = r_pidx;
+          stop = leaf_book(n, h, delta, draws, forward);
+          if (stop != kStopNone) {
+            if (spec) { (void)wait_eval(); n_wasted += 1; }
+            break;
+          }
+        }
+      } else {
+        for (unsigned long long n = 0; n < nleaves; ++n) {
+          leapfrog(eps);
+          add_cum();
+          double h, delta;
+          leaf_energy(h_ref, h, delta);
+          stop = leaf_book(n, h, delta, draws, forward);
+          if (stop != kStopNone) break;
         }
       }
     }
@@ -689,6 +773,7 @@ __device__ void run_chain(Engine<Team, Model>& E, Key ck, const RunCfg& rc, cons
     const double* inv = E.v(V_INV);
     for (int d = E.T.rank(); d < D; d += E.T.size()) out.adapt[2 + W + d] = inv[d * s];
     if (E.T.leader() && out.evals) out.evals[0] = (int64_t)E.n_evals;
+    if (E.T.leader() && E.prof) E.prof[11] = E.n_wasted;
   }
 }
 

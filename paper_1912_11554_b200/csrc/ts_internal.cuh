@@ -67,6 +67,7 @@ struct OpArgs {
 };
 
 struct SmallW {
+  static constexpr bool kAsync = false;
   SmallModel m;
   template <class Team>
   __device__ double eval(const Team& T, const VecStore& S, int q, int g) { return small_model_eval(T, m, S, q, g); }
@@ -81,24 +82,33 @@ struct LogisticW {
   double* red_s;
   int* cmd;  // smem: [0] 1 = evaluate / 0 = exit, [1] q vector id, [2] gradient vector id
   unsigned long long epoch;
-  template <class Team>
-  __device__ double eval(const Team&, const VecStore&, int q, int g) {  // driver warp
+  static constexpr bool kAsync = true;
+  // driver warp: post a pass (non-blocking arrive on barrier 2) ...
+  __device__ void post(int q, int g) {
     if (threadIdx.x == 0) { cmd[0] = 1; cmd[1] = q; cmd[2] = g; }
-    cta_bar(2);  // start: publishes q and the command to the worker warps
-    cta_bar(3);  // done: gradient written to vector g, U in red_s
+    cta_arrive(2);  // publishes q and the command to the worker warps
+  }
+  // ... and collect it (barrier 3: gradient written to vector g, U in red_s)
+  __device__ double wait() {
+    cta_bar(3);
     return red_s[1] - red_s[0];
+  }
+  template <class Team>
+  __device__ double eval(const Team&, const VecStore&, int q, int g) {
+    post(q, g);
+    return wait();
   }
   __device__ void serve(const VecStore& S) {  // worker warps
     for (;;) {
       cta_bar(2);
       if (cmd[0] == 0) break;
       logistic_eval_grid(a, S, cmd[1], cmd[2], wred, red_s, epoch);
-      cta_bar(3);
+      cta_arrive(3);
     }
   }
   __device__ void release_workers() {  // driver warp, once at the end
     if (threadIdx.x == 0) cmd[0] = 0;
-    cta_bar(2);
+    cta_arrive(2);
   }
 };
 
@@ -115,6 +125,7 @@ __device__ void do_op(Engine<Team, Model>& E, const OpArgs& A, int chain, bool w
   }
   E.tr = (A.has_trace && writer) ? const_cast<TraceBuf*>(&A.trace) : nullptr;
   E.n_evals = 0;
+  E.n_wasted = 0;
   E.cfg = A.cfg;
   switch (A.op) {
     case OP_POTGRAD: {

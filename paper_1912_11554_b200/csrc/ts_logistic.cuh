@@ -163,6 +163,7 @@ __device__ __forceinline__ int wk_warp() { return (int)(threadIdx.x >> 5) - 1; }
 __device__ __forceinline__ int wk_nwarps() { return (int)(blockDim.x >> 5) - 1; }
 __device__ __forceinline__ void wk_sync() { asm volatile("bar.sync 1, %0;" ::"r"(wk_threads()) : "memory"); }
 __device__ __forceinline__ void cta_bar(int id) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"((int)blockDim.x) : "memory"); }
+__device__ __forceinline__ void cta_arrive(int id) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"((int)blockDim.x) : "memory"); }
 
 // ------------------------------------------------------------- tile pipeline
 struct WarpTiles {
@@ -349,13 +350,18 @@ __device__ __forceinline__ void logistic_cta_pass(const LogisticArgs& a, const d
       if (++s == a.nstage) { s = 0; parity ^= 1u; }
       if (++tj == wt.count) tj = 0;
       if constexpr (FP64) {
+        // each element converted to double once (F2F is the scarce pipe here)
+        // and reused for eta and for the gradient
+        double xd[PMAX];
+#pragma unroll
+        for (int k = 0; k < PMAX; ++k) xd[k] = (k < p) ? (double)x[k] : 0.0;
         double e0 = theta_s[p], e1 = 0.0, e2 = 0.0, e3 = 0.0;
 #pragma unroll
         for (int k = 0; k < PMAX; k += 4) {
-          e0 = __fma_rn((double)x[k], (k < p) ? theta_s[k] : 0.0, e0);
-          e1 = __fma_rn((double)x[k + 1], (k + 1 < p) ? theta_s[k + 1] : 0.0, e1);
-          e2 = __fma_rn((double)x[k + 2], (k + 2 < p) ? theta_s[k + 2] : 0.0, e2);
-          e3 = __fma_rn((double)x[k + 3], (k + 3 < p) ? theta_s[k + 3] : 0.0, e3);
+          e0 = __fma_rn(xd[k], (k < p) ? theta_s[k] : 0.0, e0);
+          e1 = __fma_rn(xd[k + 1], (k + 1 < p) ? theta_s[k + 1] : 0.0, e1);
+          e2 = __fma_rn(xd[k + 2], (k + 2 < p) ? theta_s[k + 2] : 0.0, e2);
+          e3 = __fma_rn(xd[k + 3], (k + 3 < p) ? theta_s[k + 3] : 0.0, e3);
         }
         const double eta = (e0 + e1) + (e2 + e3);
         const double e = exp(-fabs(eta));
@@ -365,7 +371,7 @@ __device__ __forceinline__ void logistic_cta_pass(const LogisticArgs& a, const d
         const double resid = valid ? yv - sig : 0.0;
         accl += valid ? (yv * eta - l) : 0.0;
 #pragma unroll
-        for (int k = 0; k < PMAX; ++k) acc[k] = __fma_rn(resid, (double)x[k], acc[k]);
+        for (int k = 0; k < PMAX; ++k) acc[k] = __fma_rn(resid, xd[k], acc[k]);
         acc[PMAX] += resid;
       } else {
         float e0 = thb32, e1 = 0.f, e2 = 0.f, e3 = 0.f;

@@ -51,7 +51,11 @@ def parse():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--precision", choices=("fp64", "fp32"), default="fp64")
+    ap.add_argument("--precision", choices=("fp64", "fp32"), default="fp32",
+                    help="arithmetic of the fused data pass for the headline (the other mode is reported too)")
+    ap.add_argument("--single-precision", action="store_true", help="measure only --precision")
+    ap.add_argument("--config", choices=("covtype", "eight_schools"), default="covtype")
+    ap.add_argument("--chains", type=int, default=8192, help="eight_schools: total chains")
     ap.add_argument("--num-warmup", type=int, default=1000)
     ap.add_argument("--num-samples", type=int, default=1000)
     ap.add_argument("--seed", type=int, default=1)
@@ -204,10 +208,68 @@ def run_reference(args):
     return 0
 
 
+def run_eight_schools(args):
+    """Secondary workload: 8192 eight-schools chains,
+    1000+1000, sharded across ranks (one chain per thread, one launch per GPU).
+    Not the driver's headline line; run with --config eight_schools."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1912_11554_b200 as ts
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    C = args.chains
+    model = ts.eight_schools_model()
+    cfg = ts.RunConfig(model={"model": "eight_schools"}, num_chains=C, num_warmup=args.num_warmup,
+                       num_samples=args.num_samples, seed=3)
+    keys = ts.chain_keys(3, C)
+    mine = [keys[c] for c in ts.chains.shard_range(C, rank, world)]
+    times, lfs = [], []
+    last = None
+    for s in range(args.warmup + args.steps):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        r = ts.run_device(model, cfg, mine, dev)
+        if s >= args.warmup:
+            times.append(r.event_ms)
+            lfs.append(float(r.stats.cpu().numpy()[:, :, 1].sum()))
+            last = r
+    t = torch.tensor([sum(times), sum(lfs)], dtype=torch.float64, device=dev)
+    if world > 1:
+        tm = t[:1].clone()
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+        tl = t[1:].clone()
+        dist.all_reduce(tl, op=dist.ReduceOp.SUM)
+        t = torch.cat([tm, tl])
+    t_ms, lf = float(t[0]), float(t[1])
+    ess = ts.ess(last.samples.cpu().numpy())
+    if rank == 0:
+        print(json.dumps({
+            "metric": "leapfrog_steps_per_sec", "value": lf / (t_ms / 1000.0), "unit": "leapfrog/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"eight schools NC, {C} chains x ({args.num_warmup}+{args.num_samples}), "
+                                   "chain-sharded, one chain per thread"},
+            "min_ess_rank0_shard": float(np.nanmin(ess)),
+        }), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.config == "eight_schools":
+        return run_eight_schools(args)
 
     import torch
     import torch.distributed as dist
@@ -242,62 +304,71 @@ def main():
         return float(t.item())
 
     x32, y8 = make_data()
-    model =ts.logistic_regression_model(ts.LogisticRegressionData(x32, y8), precision=args.precision)
-    model.device_spec.handle(dev)
     cfg_for = lambda seed: ts.RunConfig(model={"model": "logistic_regression"}, num_chains=1,  # noqa: E731
                                         num_warmup=args.num_warmup, num_samples=args.num_samples, seed=seed)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MB > L2
-
-    # ---------------------------------------------------------------- device-resident timed region
-    ms_list, lf_list, ev_list, ess_list = [], [], [], []
-    last = None
-    clocks = ClockSampler(local)
-    for s in range(args.warmup + args.steps):
-        seed = args.seed + 1000 * s + rank
-        keys = ts.chain_keys(seed, 1)
-        flush.fill_(float(s))
-        barrier()
-        if s == args.warmup:
-            clocks.__enter__()
-        r = ts.run_device(model, cfg_for(seed), keys, dev, sync=False)
-        r.event_ms[1].synchronize()
-        barrier()
-        if s >= args.warmup:
-            ms = r.event_ms[0].elapsed_time(r.event_ms[1])
-            st = r.stats.cpu().numpy()[0]
-            ms_list.append(ms)
-            lf_list.append(float(st[:, 1].sum()))
-            ev_list.append(float(r.evals.cpu().numpy()[0]))
-            samples = r.samples.cpu().numpy()[0]
-            ess_list.append(float(np.nanmin(ts.ess(samples[None]))))
-            last = r
-    clocks.__exit__(None, None, None)
-    t_total_ms = max_over_ranks(sum(ms_list))
-    lf_total = sum_over_ranks(sum(lf_list))
-    ev_total_local = sum(ev_list)
-    ess_total = sum_over_ranks(sum(ess_list))
-    value = lf_total / (t_total_ms / 1000.0)
-    ess_per_s = ess_total / (t_total_ms / 1000.0)
-
-    # roofline of the persistent kernel (this rank's own launches and clock)
     peak, peak_kind = peaks()
-    achieved = ALGO_BYTES_PER_PASS * ev_total_local / (sum(ms_list) / 1000.0) / 1e9
 
-    # eval-only microbenchmark: the fused pass alone, 200 passes in one launch
-    q = torch.from_numpy(np.asarray(last.samples.cpu().numpy()[0, -1])).to(dev)
-    out = torch.empty(1, dtype=torch.float64, device=dev)
-    lib = ts._lib.load_library()
-    h = model.device_spec.handle(dev)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    for _ in range(2):
+    def timed_runs(precision, with_clocks):
+        """W untimed + K timed full runs; device time per launch (CUDA events)."""
+        model = ts.logistic_regression_model(ts.LogisticRegressionData(x32, y8), precision=precision)
+        model.device_spec.handle(dev)
+        ms_list, lf_list, ev_list, ess_list = [], [], [], []
+        last = None
+        clocks = ClockSampler(local)
+        for s in range(args.warmup + args.steps):
+            seed = args.seed + 1000 * s + rank
+            keys = ts.chain_keys(seed, 1)
+            flush.fill_(float(s))
+            barrier()
+            if s == args.warmup and with_clocks:
+                clocks.__enter__()
+            r = ts.run_device(model, cfg_for(seed), keys, dev, sync=False)
+            r.event_ms[1].synchronize()
+            barrier()
+            if s >= args.warmup:
+                ms_list.append(r.event_ms[0].elapsed_time(r.event_ms[1]))
+                st = r.stats.cpu().numpy()[0]
+                lf_list.append(float(st[:, 1].sum()))
+                ev_list.append(float(r.evals.cpu().numpy()[0]))
+                samples = r.samples.cpu().numpy()[0]
+                ess_list.append(float(np.nanmin(ts.ess(samples[None]))))
+                last = r
+        if with_clocks:
+            clocks.__exit__(None, None, None)
+        t_total_ms = max_over_ranks(sum(ms_list))
+        lf_total = sum_over_ranks(sum(lf_list))
+        ess_total = sum_over_ranks(sum(ess_list))
+        # roofline of the persistent kernel (this rank's own launches and clock)
+        achieved = ALGO_BYTES_PER_PASS * sum(ev_list) / (sum(ms_list) / 1000.0) / 1e9
+        # the fused pass alone: 200 passes in one launch, timed inside the kernel
+        q = torch.from_numpy(np.asarray(last.samples.cpu().numpy()[0, -1])).to(dev)
+        out = torch.zeros(12, dtype=torch.float64, device=dev)
+        lib = ts._lib.load_library()
+        h = model.device_spec.handle(dev)
         ts._lib.check(lib.ts_eval_bench(h, q.data_ptr(), 20, out.data_ptr(), ts._lib.stream_ptr(torch)))
-    flush.fill_(1.0)
-    e0.record()
-    ts._lib.check(lib.ts_eval_bench(h, q.data_ptr(), 200, out.data_ptr(), ts._lib.stream_ptr(torch)))
-    e1.record()
-    e1.synchronize()
-    eval_us = e0.elapsed_time(e1) * 1000.0 / 200
-    eval_gbs = ALGO_BYTES_PER_PASS / (eval_us * 1e-6) / 1e9
+        flush.fill_(1.0)
+        ts._lib.check(lib.ts_eval_bench(h, q.data_ptr(), 200, out.data_ptr(), ts._lib.stream_ptr(torch)))
+        torch.cuda.synchronize()
+        eval_us = float(out.cpu().numpy()[1]) / 1000.0 / 200
+        eval_gbs = ALGO_BYTES_PER_PASS / (eval_us * 1e-6) / 1e9
+        return {
+            "value": lf_total / (t_total_ms / 1000.0),
+            "ms_per_step": t_total_ms / args.steps,
+            "ess_per_sec": ess_total / (t_total_ms / 1000.0),
+            "leapfrogs_per_step": lf_total / args.steps,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                         "bytes_per_pass": ALGO_BYTES_PER_PASS, "passes": sum(ev_list)},
+            "eval_only": {"us_per_pass": eval_us, "achieved_gbs": eval_gbs, "frac": eval_gbs / peak},
+            "clocks": clocks.summary() if with_clocks else None,
+            "last": last,
+        }
+
+    main_m = timed_runs(args.precision, True)
+    other = "fp64" if args.precision == "fp32" else "fp32"
+    other_m = None if args.single_precision else timed_runs(other, False)
+    last = main_m["last"]
 
     # ---------------------------------------------------------------- end to end through the public API
     e2e = None
@@ -339,16 +410,16 @@ def main():
     if rank == 0:
         line = {
             "metric": "leapfrog_steps_per_sec",
-            "value": value,
+            "value": main_m["value"],
             "unit": "leapfrog/s",
             "n_gpus": world,
             "steps": args.steps,
             "warmup": args.warmup,
-            "ms_per_step": t_total_ms / args.steps,
+            "ms_per_step": main_m["ms_per_step"],
             "higher_is_better": True,
             "scaling": "weak",
             "vs_baseline": None,
-            "dtype": "f64" if args.precision == "fp64" else "f32-rows/f64-accum",
+            "dtype": "f64" if args.precision == "fp64" else "f32",
             "data": "synthetic",
             "config": {
                 "workload": "covtype-shaped logistic NUTS, 581012x54 (D=55), 1 chain per GPU, max_tree_depth 10",
@@ -356,17 +427,18 @@ def main():
                 "parallelism": f"replicas{world}", "l2": "256 MB buffer written between steps (X+y = 126 MB ~ L2)",
                 "step": "one full run (step-size search + warmup + sampling) = one persistent kernel launch",
             },
-            "ess_per_sec": ess_per_s,
-            "leapfrogs_per_step": lf_total / args.steps,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
-                         "bytes_per_pass": ALGO_BYTES_PER_PASS, "passes": ev_total_local},
-            "eval_only": {"us_per_pass": eval_us, "achieved_gbs": eval_gbs, "frac": eval_gbs / peak},
+            "ess_per_sec": main_m["ess_per_sec"],
+            "leapfrogs_per_step": main_m["leapfrogs_per_step"],
+            "roofline": main_m["roofline"],
+            "eval_only": main_m["eval_only"],
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": args.steps,
-            "clocks": clocks.summary(),
+            "clocks": main_m["clocks"],
         }
+        if other_m is not None:
+            line[f"{other}_mode"] = {k: other_m[k] for k in ("value", "ms_per_step", "ess_per_sec",
+                                                            "leapfrogs_per_step", "roofline", "eval_only")}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

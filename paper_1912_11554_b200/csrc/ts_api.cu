@@ -27,8 +27,9 @@ extern "C" const char* ts_last_error(void) { return g_last_error.c_str(); }
 extern "C" int ts_abi_version(void) { return TS_ABI_VERSION; }
 
 __global__ void k_retile(const float* __restrict__ x, const uint8_t* __restrict__ y, int64_t n, int p, int64_t ntiles,
-                         float* __restrict__ xt, uint8_t* __restrict__ yt) {
+                         float* __restrict__ xt, uint8_t* __restrict__ yt, int* __restrict__ has_subnormal) {
   const int64_t total = ntiles * 32 * (int64_t)p;
+  int sub = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t row = i / p;
     const int j = (int)(i % p);
@@ -37,9 +38,13 @@ __global__ void k_retile(const float* __restrict__ x, const uint8_t* __restrict_
     const int g = j >> 2;
     const int w = (p - 4 * g) < 4 ? (p - 4 * g) : 4;
     const int64_t dst = t * 32 * (int64_t)p + 128 * (int64_t)g + (int64_t)lane * w + (j & 3);
-    xt[dst] = row < n ? x[row * p + j] : 0.f;
+    const float v = row < n ? x[row * p + j] : 0.f;
+    const unsigned a = __float_as_uint(v) & 0x7fffffffu;
+    sub |= (a != 0u && a < 0x00800000u);
+    xt[dst] = v;
     if (j == 0) yt[row] = row < n ? y[row] : 0;
   }
+  if (__syncthreads_or(sub) && threadIdx.x == 0) atomicOr(has_subnormal, 1);
 }
 
 static int pick_pmax(int p) {
@@ -129,14 +134,19 @@ extern "C" int ts_model_create(int kind, int dim, const double* params, int n_pa
       const size_t nx = (size_t)m->ntiles * 32 * n_feat;
       if (cudaMalloc((void**)&m->xt, nx * sizeof(float)) != cudaSuccess) return fail(TS_ECUDA, "cudaMalloc X failed");
       if (cudaMalloc((void**)&m->yt, (size_t)m->ntiles * 32) != cudaSuccess) return fail(TS_ECUDA, "cudaMalloc y failed");
-      k_retile<<<1184, 256>>>(x_dev, y_dev, n_rows, n_feat, m->ntiles, m->xt, m->yt);
+      if (cudaMalloc((void**)&m->bar, sizeof(unsigned long long)) != cudaSuccess) return fail(TS_ECUDA, "cudaMalloc barrier failed");
+      if (cudaMemset(m->bar, 0, sizeof(unsigned long long)) != cudaSuccess) return fail(TS_ECUDA, "memset barrier failed");
+      // the barrier word doubles as the "X has fp32 subnormals" flag during re-tiling
+      k_retile<<<1184, 256>>>(x_dev, y_dev, n_rows, n_feat, m->ntiles, m->xt, m->yt, reinterpret_cast<int*>(m->bar));
       if (cudaGetLastError() != cudaSuccess) return fail(TS_ECUDA, "retile launch failed");
+      unsigned long long flag = 0;
+      if (cudaMemcpy(&flag, m->bar, sizeof flag, cudaMemcpyDeviceToHost) != cudaSuccess) return fail(TS_ECUDA, "retile failed");
+      m->exact_cvt = flag != 0;
       int nsm = 148;
       cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, m->device);
       const size_t pb = 2 * (size_t)nsm * 2 * (n_feat + 2);  // room for up to 2 CTAs per SM
       if (cudaMalloc((void**)&m->pbuf, pb * sizeof(double)) != cudaSuccess) return fail(TS_ECUDA, "cudaMalloc partials failed");
       if (cudaMemset(m->pbuf, 0, pb * sizeof(double)) != cudaSuccess) return fail(TS_ECUDA, "memset partials failed");
-      if (cudaMalloc((void**)&m->bar, sizeof(unsigned long long)) != cudaSuccess) return fail(TS_ECUDA, "cudaMalloc barrier failed");
       if (cudaDeviceSynchronize() != cudaSuccess) return fail(TS_ECUDA, "retile failed");
       break;
     }

@@ -30,6 +30,7 @@ struct ts_model {
   int grid;
   int pmax;
   unsigned long long* prof;  // transient: phase counters for ts_eval_bench
+  int exact_cvt;             // X holds fp32 subnormals (fp64 pass uses F2F)
 };
 
 namespace ts_internal {

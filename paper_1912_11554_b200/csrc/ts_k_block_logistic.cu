@@ -37,6 +37,7 @@ int launch_block_logistic(const ts_model* m, int nslots, OpArgs& A, cudaStream_t
   mw.a.l2_keep_tiles = 0;
   mw.a.prof = m->prof;
   mw.a.l2_prefetch = 0;
+  mw.a.exact_cvt = m->exact_cvt;
   if (const char* e = getenv("TS_L2_PREFETCH")) mw.a.l2_prefetch = atoi(e);
   if (const char* e = getenv("TS_L2_KEEP_FRAC")) mw.a.l2_keep_tiles = (int)(atof(e) * (double)m->ntiles);
   const size_t smem = need(nstage);

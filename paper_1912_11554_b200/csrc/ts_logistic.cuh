@@ -28,10 +28,11 @@
 //          over that lane's rows, then double across lanes, warps and CTAs.
 //          Tolerance mode (<= 1e-5 relative, tests/test_gpu_parity.py).
 //
-// Cross-CTA reduction: each CTA writes its (p+2)-vector of partial sums to a
-// parity-double-buffered slot, one grid barrier, then every CTA reduces all
-// slots in the same fixed order, so every CTA holds the identical gradient
-// and runs the (replicated) tree logic without a second barrier.
+// Cross-CTA reduction: each CTA adds its (p+2)-vector of partial sums to a
+// global accumulator as exact fixed-point int64 pairs (red.add; integer sums
+// are order-independent, so the result is deterministic), one grid barrier,
+// then every CTA reads the identical totals and runs the (replicated) tree
+// logic without a second barrier.
 #pragma once
 #include <stdint.h>
 #include "ts_team.cuh"
@@ -49,7 +50,7 @@ struct LogisticArgs {
   int64_t n_rows;
   int p;
   int64_t ntiles;
-  double* pbuf;             // [2][grid][p+2] partial sums
+  double* pbuf;             // 3 rotating accumulators of (p+2) fixed-point int64 pairs + flag
   unsigned long long* bar;  // grid barrier counter (zeroed before launch)
   int fp64;                 // precision policy
   int pmax;                 // compile-time feature capacity of the pass (8/32/56/64)
@@ -61,6 +62,7 @@ struct LogisticArgs {
   int stage_bytes;
   int l2_keep_tiles;        // tiles [0, l2_keep_tiles) loaded with L2::evict_last, rest evict_first
   int l2_prefetch;          // tiles per warp prefetched into L2 at the end of a pass
+  int exact_cvt;            // X holds fp32 subnormals (informational)
   unsigned long long* prof; // optional: CTA-0 cycle counters [prior, pass, barrier, reduce] (profiling)
 };
 
@@ -352,16 +354,16 @@ __device__ __forceinline__ void logistic_cta_pass(const LogisticArgs& a, const d
       if constexpr (FP64) {
         // each element converted to double once (F2F is the scarce pipe here)
         // and reused for eta and for the gradient
-        double xd[PMAX];
-#pragma unroll
-        for (int k = 0; k < PMAX; ++k) xd[k] = (k < p) ? (double)x[k] : 0.0;
+        // The fp32 -> fp64 conversions (F2F, ~4/clk/SM on the XU pipe) bound
+        // this variant: ncu shows XU ~95% busy, FP64 ~17%.  An integer-ALU
+        // conversion (6 instructions per element) measured slower.
         double e0 = theta_s[p], e1 = 0.0, e2 = 0.0, e3 = 0.0;
 #pragma unroll
         for (int k = 0; k < PMAX; k += 4) {
-          e0 = __fma_rn(xd[k], (k < p) ? theta_s[k] : 0.0, e0);
-          e1 = __fma_rn(xd[k + 1], (k + 1 < p) ? theta_s[k + 1] : 0.0, e1);
-          e2 = __fma_rn(xd[k + 2], (k + 2 < p) ? theta_s[k + 2] : 0.0, e2);
-          e3 = __fma_rn(xd[k + 3], (k + 3 < p) ? theta_s[k + 3] : 0.0, e3);
+          e0 = __fma_rn((double)x[k], (k < p) ? theta_s[k] : 0.0, e0);
+          e1 = __fma_rn((double)x[k + 1], (k + 1 < p) ? theta_s[k + 1] : 0.0, e1);
+          e2 = __fma_rn((double)x[k + 2], (k + 2 < p) ? theta_s[k + 2] : 0.0, e2);
+          e3 = __fma_rn((double)x[k + 3], (k + 3 < p) ? theta_s[k + 3] : 0.0, e3);
         }
         const double eta = (e0 + e1) + (e2 + e3);
         const double e = exp(-fabs(eta));
@@ -371,7 +373,7 @@ __device__ __forceinline__ void logistic_cta_pass(const LogisticArgs& a, const d
         const double resid = valid ? yv - sig : 0.0;
         accl += valid ? (yv * eta - l) : 0.0;
 #pragma unroll
-        for (int k = 0; k < PMAX; ++k) acc[k] = __fma_rn(resid, xd[k], acc[k]);
+        for (int k = 0; k < PMAX; ++k) acc[k] = __fma_rn(resid, (double)x[k], acc[k]);
         acc[PMAX] += resid;
       } else {
         float e0 = thb32, e1 = 0.f, e2 = 0.f, e3 = 0.f;

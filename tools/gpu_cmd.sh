@@ -1,1 +1,4 @@
-python tools/prof_eval.py fp64 20 > gpurun_out/pe.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:k_block_op -s 1 -c 1 -o gpurun_out/prof_eval_fp64 python tools/prof_eval.py fp64 20 > gpurun_out/ncu_pe.log 2>&1
+timeout 600 python -m pytest tests -m gpu -q -x > gpurun_out/t18.log 2>&1
+timeout 900 python bench.py --steps 3 --warmup 3 --cpu-seconds 15 > gpurun_out/bench4.log 2>&1
+timeout 600 python bench.py --config eight_schools --steps 2 --warmup 1 >> gpurun_out/bench4.log 2>&1
+timeout 600 python bench.py --impl reference --steps 2 --warmup 1 >> gpurun_out/bench4.log 2>&1

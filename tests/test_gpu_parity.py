@@ -343,6 +343,38 @@ def test_sampling_correctness_10d_normal():
 # ----------------------------------------------------------------------------- covtype shape
 
 
+def test_covtype_transitions_match_oracle(oracle):
+    """Full-size config 2: transitions of a device run, re-run from the run's own
+    states on the device and on the CPU oracle (fp64): identical integers, and
+    positions within 1e-12 after up to 2^10-1 leapfrogs over 581,012 rows."""
+    t = ts()
+    from tests_data import logistic_data
+
+    x, y = logistic_data(581012, 54, 20191222)
+    m = t.logistic_regression_model(t.LogisticRegressionData(x, y), precision="fp64")
+    W, S, seed = 150, 12, 1001
+    cfg = t.RunConfig(model={}, num_chains=1, num_warmup=W, num_samples=S, seed=seed)
+    key = t.chain_keys(seed, 1)[0]
+    r = t.run_device(m, cfg, [key], 0)
+    st = r.stats.cpu().numpy()[0]
+    ad = r.adapt.cpu().numpy()[0]
+    samples = r.samples.cpu().numpy()[0]
+    step, inv = float(ad[1]), ad[2 + W:].copy()
+    om = oracle.Model("logistic_regression", 55, x=x, y=y, fused_omp=True)
+    for i in (1, 5, 9):
+        q0 = samples[i - 1]
+        U0, g0 = m.potential(q0), m.gradient(q0)
+        z = t.PhasePoint(q0, np.zeros(55), U0, g0)
+        dkey = key.fold(10 + W + i)
+        z1, s1 = t.nuts_transition_from(z, t.SamplerConfig(step_size=step, mass=t.MassMatrix(inv)), m, dkey)
+        oz, os_, _ = oracle.transition(oracle.Point(q0.tolist(), [0.0] * 55, U0, g0.tolist()), step, inv.tolist(), om,
+                                       (dkey.hi, dkey.lo))
+        assert (s1.depth_reached, s1.leapfrog_calls) == (os_.depth, os_.leapfrogs) == (int(st[W + i, 0]),
+                                                                                      int(st[W + i, 1]))
+        assert close(z1.position, oz.q, 1e-12, atol=1e-14)
+        assert np.array_equal(z1.position, samples[i])  # the run's own draw
+
+
 @pytest.mark.parametrize("precision,rel", [("fp64", 1e-11), ("fp32", FP32_REL)])
 def test_covtype_shape_potential_gradient(precision, rel, oracle):
     """Full BASELINE config-2 size (581,012 x 54) against the C oracle."""

@@ -1,0 +1,45 @@
+"""Summarise an ncu report into profiles/: key throughput metrics of each
+profiled kernel (duration, DRAM bytes, pipe utilisation, stalls).
+Usage: python tools/ncu_summary.py report.ncu-rep out.json [passes_in_launch]"""
+import csv, io, json, subprocess, sys
+
+KEYS = ("gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "dram__throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+        "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+        "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+        "smsp__issue_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
+        "launch__grid_size", "launch__block_size", "sm__warps_active.avg.pct_of_peak_sustained_active",
+        "lts__t_sector_hit_rate.pct", "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
+        "smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio",
+        "smsp__average_warps_issue_stalled_wait_per_issue_active.ratio")
+
+
+def main(rep, out, passes=None):
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, units = rows[0], rows[1]
+    res = []
+    for r in rows[2:]:
+        d = {"kernel": r[hdr.index("Kernel Name")][:120]}
+        for k in KEYS:
+            if k in hdr:
+                v = r[hdr.index(k)]
+                try:
+                    v = float(v.replace(",", ""))
+                except ValueError:
+                    pass
+                d[k] = v
+                d[k + ".unit"] = units[hdr.index(k)]
+        if passes:
+            sc = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+            tot = sum(d.get(k, 0) * sc.get(d.get(k + ".unit", "byte"), 1)
+                      for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+            d["dram_bytes_per_pass"] = tot / float(passes)
+        res.append(d)
+    json.dump(res, open(out, "w"), indent=1)
+    print(json.dumps(res, indent=1)[:3000])
+
+
+if __name__ == "__main__":
+    main(sys.argv[1], sys.argv[2], sys.argv[3] if len(sys.argv) > 3 else None)

@@ -54,7 +54,7 @@ def parse():
     ap.add_argument("--precision", choices=("fp64", "fp32"), default="fp32",
                     help="arithmetic of the fused data pass for the headline (the other mode is reported too)")
     ap.add_argument("--single-precision", action="store_true", help="measure only --precision")
-    ap.add_argument("--config", choices=("covtype", "eight_schools"), default="covtype")
+    ap.add_argument("--config", choices=("covtype", "eight_schools", "gauss10", "rowshard"), default="covtype")
     ap.add_argument("--chains", type=int, default=8192, help="eight_schools: total chains")
     ap.add_argument("--num-warmup", type=int, default=1000)
     ap.add_argument("--num-samples", type=int, default=1000)
@@ -224,11 +224,18 @@ def run_eight_schools(args):
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    C = args.chains
-    model = ts.eight_schools_model()
-    cfg = ts.RunConfig(model={"model": "eight_schools"}, num_chains=C, num_warmup=args.num_warmup,
-                       num_samples=args.num_samples, seed=3)
-    keys = ts.chain_keys(3, C)
+    if args.config == "gauss10":  # 10-D diagonal Gaussian, 1 chain
+        C = 1
+        model = ts.gaussian_model(np.ones(10))
+        cfg = ts.RunConfig(model={"model": "gaussian"}, num_chains=1, num_warmup=args.num_warmup,
+                           num_samples=args.num_samples, seed=7)
+        keys = ts.chain_keys(7, 1)
+    else:
+        C = args.chains
+        model = ts.eight_schools_model()
+        cfg = ts.RunConfig(model={"model": "eight_schools"}, num_chains=C, num_warmup=args.num_warmup,
+                           num_samples=args.num_samples, seed=3)
+        keys = ts.chain_keys(3, C)
     mine = [keys[c] for c in ts.chains.shard_range(C, rank, world)]
     times, lfs = [], []
     last = None
@@ -255,9 +262,88 @@ def run_eight_schools(args):
             "metric": "leapfrog_steps_per_sec", "value": lf / (t_ms / 1000.0), "unit": "leapfrog/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms / args.steps,
             "higher_is_better": True, "scaling": "strong", "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"eight schools NC, {C} chains x ({args.num_warmup}+{args.num_samples}), "
-                                   "chain-sharded, one chain per thread"},
+            "config": {"workload": (f"eight schools NC, {C} chains" if args.config == "eight_schools"
+                                    else "10-D diagonal Gaussian, 1 chain")
+                                   + f" x ({args.num_warmup}+{args.num_samples}), one chain per thread"},
             "min_ess_rank0_shard": float(np.nanmin(ess)),
+            "ess_per_sec_rank0_shard": float(np.nanmin(ess)) / (t_ms / 1000.0 / args.steps),
+        }), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+C5_ROWS, C5_FEAT, C5_SEED = 8_000_000, 255, 20191223
+C5_BYTES_PER_PASS = 4 * C5_ROWS * C5_FEAT + C5_ROWS  # 8,168,000,000 B
+
+
+def run_row_sharded(args):
+    """ONE logistic chain over 8M x 255 rows, rows
+    sharded over the ranks (world 1 = one GPU holds all rows).  Each data
+    pass ends with the in-kernel NVLink peer exchange of the fixed-point
+    totals (paper_1912_11554_b200/rowshard.py); every rank runs the same
+    chain.  Not the driver's headline line; run with --config rowshard."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1912_11554_b200 as ts
+    from tests_data import logistic_data_f32
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    a, b = ts.rowshard.row_range(C5_ROWS, rank, world)
+    x, y = logistic_data_f32(C5_ROWS, C5_FEAT, C5_SEED, rows=(a, b))
+    model = ts.logistic_regression_model(ts.LogisticRegressionData(x, y), precision=args.precision)
+    del x, y
+    model.device_spec.handle(dev)
+    if world > 1:
+        ts.rowshard.connect(model.device_spec, rank, world, ts.rowshard.torch_all_gather(), device=dev)
+    W, S = args.num_warmup, args.num_samples
+    peak, peak_kind = peaks()
+    times, lfs, evs = [], [], []
+    clocks = ClockSampler(local)
+    for s in range(args.warmup + args.steps):
+        cfg = ts.RunConfig(model={"model": "logistic_regression"}, num_chains=1, num_warmup=W, num_samples=S,
+                           seed=args.seed + s)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        if s == args.warmup:
+            clocks.__enter__()
+        r = ts.run_device(model, cfg, ts.chain_keys(args.seed + s, 1), dev, sync=False)
+        r.event_ms[1].synchronize()
+        if s >= args.warmup:
+            times.append(r.event_ms[0].elapsed_time(r.event_ms[1]))
+            lfs.append(float(r.stats.cpu().numpy()[0][:, 1].sum()))
+            evs.append(float(r.evals.cpu().numpy()[0]))
+    clocks.__exit__(None, None, None)
+    t_ms = sum(times)
+    if world > 1:
+        t = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_ms = float(t.item())
+    lf, ev = sum(lfs), sum(evs)  # one replicated chain: counted once
+    achieved = C5_BYTES_PER_PASS * ev / (t_ms / 1000.0) / 1e9
+    if rank == 0:
+        print(json.dumps({
+            "metric": "leapfrog_steps_per_sec", "value": lf / (t_ms / 1000.0), "unit": "leapfrog/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64" if args.precision == "fp64" else "f32", "data": "synthetic",
+            "config": {"workload": f"logistic NUTS 8,000,000 x 255 (D=256), 1 chain, rows sharded over {world} GPU(s),"
+                                   f" max_tree_depth 10, {W}+{S} draws per step",
+                       "precision": args.precision, "parallelism": f"rows{world}",
+                       "l2": "X (8.2 GB) >> L2: every pass streams from HBM"},
+            "leapfrogs_per_step": lf / args.steps, "passes_per_step": ev / args.steps,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak * world, "unit": "GB/s",
+                         "frac": achieved / (peak * world), "traffic": None, "peak_kind": peak_kind,
+                         "bytes_per_pass": C5_BYTES_PER_PASS},
+            "gpu_launches": args.steps, "clocks": clocks.summary(),
         }), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -268,8 +354,10 @@ def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
-    if args.config == "eight_schools":
+    if args.config in ("eight_schools", "gauss10"):
         return run_eight_schools(args)
+    if args.config == "rowshard":
+        return run_row_sharded(args)
 
     import torch
     import torch.distributed as dist

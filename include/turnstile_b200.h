@@ -136,6 +136,34 @@ int ts_run_chains(const ts_model* m, const ts_run_cfg* rc, const uint64_t* chain
                   const double* inv0_dev, const uint8_t* schedule_dev, const double* da_weight_dev, double* samples,
                   double* stats, double* adapt, int32_t* status, int64_t* evals, int exec_mode, void* stream);
 
+/* Row sharding of one logistic model across GPUs (SURVEY.md 8(e), config 5:
+ * the reference evaluates kernels.py:90-123 over all N rows in one process;
+ * here rank g of `world` holds rows [g*N/world, (g+1)*N/world)).  Every rank
+ * builds its model from its own row shard with ts_model_create, then
+ *   ts_peer_mailbox_create(m, rank, world, handle_out)  writes the 64-byte
+ *       CUDA IPC handle of this rank's exchange mailbox;
+ *   the host all-gathers the handles (rank order), e.g. torch.distributed;
+ *   ts_peer_mailbox_connect(m, handles)                  maps the peers.
+ * From then on every launch on m (potential/gradient, trees, transitions,
+ * runs) combines the per-pass partial sums of all ranks inside the
+ * persistent kernel: after its grid barrier each GPU pushes its exact
+ * fixed-point totals (p+2 values as int64 pairs) to every peer's mailbox
+ * over NVLink and sums the `world` copies it receives.  Integer sums are
+ * order-free, so every rank sees the same U and gradient -- bit-identical to
+ * one GPU holding all rows -- and runs the identical (replicated) chain.  All
+ * ranks must issue the same sequence of calls with the same arguments.
+ * world == 1 connects the mailbox to itself (the same device code path). */
+#define TS_MAX_PEERS 8
+int ts_peer_mailbox_create(ts_model* m, int rank, int world, void* ipc_handle_out);
+int ts_peer_mailbox_connect(ts_model* m, const void* ipc_handles);
+
+/* Test helper for row sharding: the raw cross-CTA fixed-point totals of ONE
+ * potential/gradient evaluation at q_dev over this model's rows (before any
+ * peer exchange): words_dev[2*(p+2)+1] uint64 = (hi, lo) pairs for the p
+ * feature sums, the residual sum and the log-likelihood sum, then the
+ * out-of-range flag.  value = hi * 2^-10 + lo * 2^-63 (two's complement). */
+int ts_logistic_partial_sums(const ts_model* m, const double* q_dev, uint64_t* words_dev, void* stream);
+
 /* Parity probe of the device randomness (csrc/ts_rng.cuh): kind 0 writes n
  * Generator.random() doubles of RngKey(key).generator(), kind 1 n
  * standard_normal() values, kind 2 the keys fold(0..n-1) as raw 64-bit

@@ -26,6 +26,8 @@ int set_err(int code, const char* msg) {
 extern "C" const char* ts_last_error(void) { return g_last_error.c_str(); }
 extern "C" int ts_abi_version(void) { return TS_ABI_VERSION; }
 
+// Re-tile X into 32-row tiles (padding rows are zero with label 0),
+// feature-group-major inside a tile (lane-contiguous rows for LDS.128).
 __global__ void k_retile(const float* __restrict__ x, const uint8_t* __restrict__ y, int64_t n, int p, int64_t ntiles,
                          float* __restrict__ xt, uint8_t* __restrict__ yt, int* __restrict__ has_subnormal) {
   const int64_t total = ntiles * 32 * (int64_t)p;
@@ -47,11 +49,38 @@ __global__ void k_retile(const float* __restrict__ x, const uint8_t* __restrict_
   if (__syncthreads_or(sub) && threadIdx.x == 0) atomicOr(has_subnormal, 1);
 }
 
+// Wide p (64 < p <= 256): tiles of kWideRows = 8 rows, row-major, each
+// followed by 16 label bytes (8 labels + 8 zeros): 32p + 16 bytes per tile,
+// one TMA bulk copy (ts_logistic.cuh, logistic_cta_pass_wide).
+__global__ void k_retile_wide(const float* __restrict__ x, const uint8_t* __restrict__ y, int64_t n, int p,
+                              int64_t ntiles, unsigned char* __restrict__ xt, int* __restrict__ has_subnormal) {
+  const int64_t total = ntiles * kWideRows * (int64_t)p;
+  const int64_t tb = wide_tile_bytes(p);
+  int sub = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = i / p;
+    const int j = (int)(i % p);
+    const int64_t t = row / kWideRows;
+    const int r = (int)(row % kWideRows);
+    const float v = row < n ? x[row * p + j] : 0.f;
+    const unsigned a = __float_as_uint(v) & 0x7fffffffu;
+    sub |= (a != 0u && a < 0x00800000u);
+    unsigned char* tile = xt + t * tb;
+    reinterpret_cast<float*>(tile)[r * p + j] = v;
+    if (j == 0) {
+      tile[32 * (int64_t)p + r] = row < n ? y[row] : 0;
+      tile[32 * (int64_t)p + kWideRows + r] = 0;
+    }
+  }
+  if (__syncthreads_or(sub) && threadIdx.x == 0) atomicOr(has_subnormal, 1);
+}
+
 static int pick_pmax(int p) {
   if (p <= 8) return 8;
   if (p <= 32) return 32;
   if (p <= 56) return 56;
   if (p <= 64) return 64;
+  if (p <= kWideMax) return kWideMax;  // wide pass
   return 0;
 }
 
@@ -78,7 +107,7 @@ static int launch(const ts_model* m, int nslots, OpArgs& A, int n_threads_chains
   if (nslots < 1) nslots = 1;
   if (nslots > kMaxSlots) return set_err(TS_EINVAL, "tree depth exceeds device slot limit (30)");
   if (m->kind == TS_LOGISTIC) {
-    if (!m->pmax) return set_err(TS_EUNSUPPORTED, "logistic feature count > 64 not supported on this path");
+    if (!m->pmax) return set_err(TS_EUNSUPPORTED, "logistic feature count > 256 not supported on this path");
     return launch_block_logistic(m, nslots, A, st);
   }
   SmallModel sm;
@@ -126,18 +155,24 @@ extern "C" int ts_model_create(int kind, int dim, const double* params, int n_pa
       if (n_feat < 1 || dim != n_feat + 1) return fail(TS_EINVAL, "logistic dim must equal num_features + 1");
       if (n_rows < 1 || !x_dev || !y_dev) return fail(TS_EINVAL, "logistic needs at least one data row");
       m->pmax = pick_pmax(n_feat);
-      if (!m->pmax) return fail(TS_EUNSUPPORTED, "logistic feature count > 64 not supported on this path");
+      if (!m->pmax) return fail(TS_EUNSUPPORTED, "logistic feature count > 256 not supported on this path");
+      m->wide = n_feat > 64;
       m->n_rows = n_rows;
       m->p = n_feat;
-      m->ntiles = (n_rows + 31) / 32;
+      m->ntiles = m->wide ? (n_rows + kWideRows - 1) / kWideRows : (n_rows + 31) / 32;
       m->fp64 = precision == TS_PREC_FP64;
-      const size_t nx = (size_t)m->ntiles * 32 * n_feat;
-      if (cudaMalloc((void**)&m->xt, nx * sizeof(float)) != cudaSuccess) return fail(TS_ECUDA, "cudaMalloc X failed");
-      if (cudaMalloc((void**)&m->yt, (size_t)m->ntiles * 32) != cudaSuccess) return fail(TS_ECUDA, "cudaMalloc y failed");
+      const size_t xbytes = m->wide ? (size_t)m->ntiles * wide_tile_bytes(n_feat) : (size_t)m->ntiles * 32 * n_feat * sizeof(float);
+      if (cudaMalloc((void**)&m->xt, xbytes) != cudaSuccess) return fail(TS_ECUDA, "cudaMalloc X failed");
+      // wide tiles carry their labels; the separate label array is then unused
+      if (cudaMalloc((void**)&m->yt, m->wide ? 16 : (size_t)m->ntiles * 32) != cudaSuccess) return fail(TS_ECUDA, "cudaMalloc y failed");
       if (cudaMalloc((void**)&m->bar, sizeof(unsigned long long)) != cudaSuccess) return fail(TS_ECUDA, "cudaMalloc barrier failed");
       if (cudaMemset(m->bar, 0, sizeof(unsigned long long)) != cudaSuccess) return fail(TS_ECUDA, "memset barrier failed");
       // the barrier word doubles as the "X has fp32 subnormals" flag during re-tiling
-      k_retile<<<1184, 256>>>(x_dev, y_dev, n_rows, n_feat, m->ntiles, m->xt, m->yt, reinterpret_cast<int*>(m->bar));
+      if (m->wide)
+        k_retile_wide<<<1184, 256>>>(x_dev, y_dev, n_rows, n_feat, m->ntiles, reinterpret_cast<unsigned char*>(m->xt),
+                                     reinterpret_cast<int*>(m->bar));
+      else
+        k_retile<<<1184, 256>>>(x_dev, y_dev, n_rows, n_feat, m->ntiles, m->xt, m->yt, reinterpret_cast<int*>(m->bar));
       if (cudaGetLastError() != cudaSuccess) return fail(TS_ECUDA, "retile launch failed");
       unsigned long long flag = 0;
       if (cudaMemcpy(&flag, m->bar, sizeof flag, cudaMemcpyDeviceToHost) != cudaSuccess) return fail(TS_ECUDA, "retile failed");
@@ -170,6 +205,10 @@ extern "C" int ts_model_destroy(ts_model* m) {
   if (m->yt) cudaFree(m->yt);
   if (m->pbuf) cudaFree(m->pbuf);
   if (m->bar) cudaFree(m->bar);
+  if (m->slotws) cudaFree(m->slotws);
+  for (int r = 0; r < m->world; ++r)
+    if (m->mail[r] && m->mail[r] != m->mail_local) cudaIpcCloseMemHandle(m->mail[r]);
+  if (m->mail_local) cudaFree(m->mail_local);
   delete m;
   return TS_OK;
 }
@@ -202,6 +241,61 @@ extern "C" int ts_potential_grad(const ts_model* m, const double* q_dev, int n_p
   A.inv = ones;
   int rc = launch(m, 1, A, 1, TS_EXEC_THREAD, st);
   cudaFreeAsync(ones, st);
+  return rc;
+}
+
+// ------------------------------------------------------------------ row sharding
+extern "C" int ts_peer_mailbox_create(ts_model* m, int rank, int world, void* ipc_handle_out) {
+  if (!m || !ipc_handle_out) return set_err(TS_EINVAL, "null argument");
+  if (m->kind != TS_LOGISTIC) return set_err(TS_EINVAL, "row sharding applies to the logistic model only");
+  if (world < 1 || world > TS_MAX_PEERS || rank < 0 || rank >= world) return set_err(TS_EINVAL, "rank/world out of range");
+  if (m->mail_local) return set_err(TS_EINVAL, "mailbox already created");
+  const size_t words = (size_t)mail_words(m->p, world) + 16;  // + exchange counter (own cache line)
+  TS_CUDA(cudaMalloc((void**)&m->mail_local, words * sizeof(unsigned long long)));
+  TS_CUDA(cudaMemset(m->mail_local, 0, words * sizeof(unsigned long long)));
+  cudaIpcMemHandle_t h;
+  TS_CUDA(cudaIpcGetMemHandle(&h, m->mail_local));
+  memcpy(ipc_handle_out, &h, sizeof h);
+  m->rank = rank;
+  m->mail[rank] = m->mail_local;
+  m->world = -world;  // connected by ts_peer_mailbox_connect
+  return TS_OK;
+}
+
+extern "C" int ts_peer_mailbox_connect(ts_model* m, const void* ipc_handles) {
+  if (!m || !ipc_handles) return set_err(TS_EINVAL, "null argument");
+  if (m->world >= 0 || !m->mail_local) return set_err(TS_EINVAL, "call ts_peer_mailbox_create first (once)");
+  const int world = -m->world;
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  for (int r = 0; r < world; ++r) {
+    if (r == m->rank) continue;
+    cudaIpcMemHandle_t h;
+    memcpy(&h, (const char*)ipc_handles + 64 * r, 64);
+    void* p = nullptr;
+    if (cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      for (int k = 0; k < r; ++k)
+        if (k != m->rank && m->mail[k]) { cudaIpcCloseMemHandle(m->mail[k]); m->mail[k] = nullptr; }
+      cudaGetLastError();
+      return set_err(TS_ECUDA, "cudaIpcOpenMemHandle failed (peer GPU not reachable?)");
+    }
+    m->mail[r] = (unsigned long long*)p;
+  }
+  m->world = world;
+  return TS_OK;
+}
+
+extern "C" int ts_logistic_partial_sums(const ts_model* m, const double* q_dev, uint64_t* words_dev, void* stream) {
+  if (!m || !q_dev || !words_dev) return set_err(TS_EINVAL, "null argument");
+  if (m->kind != TS_LOGISTIC) return set_err(TS_EINVAL, "logistic model only");
+  if (m->world > 0) return set_err(TS_EINVAL, "partial sums of a connected model would take part in the exchange");
+  cudaStream_t st = (cudaStream_t)stream;
+  double* out = nullptr;
+  TS_CUDA(cudaMallocAsync((void**)&out, (m->dim + 1) * sizeof(double), st));
+  ts_model* mm = const_cast<ts_model*>(m);
+  mm->dump = reinterpret_cast<unsigned long long*>(words_dev);
+  const int rc = ts_potential_grad(m, q_dev, 1, out, stream);
+  mm->dump = nullptr;
+  cudaFreeAsync(out, st);
   return rc;
 }
 

@@ -140,8 +140,12 @@ struct Engine {
   // CTA/warp teams keep vectors contiguous in shared memory (unit component
   // stride, 32-bit offsets); thread teams interleave chains in global memory.
   __device__ __forceinline__ double* v(int id) const {
-    if constexpr (Team::kUnitStride) return S.base + id * (int)S.vstride;
-    else return S.v(id);
+    if constexpr (Team::kUnitStride) {
+      if (S.slots != nullptr && id >= S.slot0) return S.slots + (id - S.slot0) * (int)S.vstride;
+      return S.base + id * (int)S.vstride;
+    } else {
+      return S.v(id);
+    }
   }
   __device__ __forceinline__ int64_t ds() const {
     if constexpr (Team::kUnitStride) return 1;

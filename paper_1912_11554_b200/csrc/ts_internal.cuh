@@ -31,6 +31,14 @@ struct ts_model {
   int pmax;
   unsigned long long* prof;  // transient: phase counters for ts_eval_bench
   int exact_cvt;             // X holds fp32 subnormals (fp64 pass uses F2F)
+  int wide;                  // 64 < p <= 256: 8-row row-major tiles (ts_logistic.cuh)
+  double* slotws;            // wide: per-CTA NodeStore slot vectors (grown on demand)
+  size_t slotws_size;        // doubles
+  // row sharding across GPUs (ts_peer_mailbox_*)
+  int world, rank;
+  unsigned long long* mail_local;  // this rank's mailbox (+ exchange counter after it)
+  unsigned long long* mail[TS_MAX_PEERS];
+  unsigned long long* dump;        // transient: ts_logistic_partial_sums output
 };
 
 namespace ts_internal {
@@ -251,21 +259,29 @@ __global__ void __launch_bounds__(256, 1) k_block_op(MW mw, int D, int nslots, i
     E.S = S;
     do_op(E, A, chain, writer);
   } else {
-    mw.wred = smem + (((int64_t)nv * D + kTeamScratch + 1) & ~(int64_t)1);  // 16-byte aligned
+    // wide-p models keep the NodeStore slot vectors in a per-CTA global
+    // workspace (their data pass is long; shared memory goes to the ring)
+    const int nvs = mw.a.slotws ? (int)V_SLOT0 : nv;
+    if (mw.a.slotws) {
+      S.slots = mw.a.slotws + (int64_t)blockIdx.x * kSlotVecs * nslots * D;
+      S.slot0 = V_SLOT0;
+    }
+    mw.wred = smem + (((int64_t)nvs * D + kTeamScratch + 1) & ~(int64_t)1);  // 16-byte aligned
     mw.red_s = mw.wred + model_scratch;
-    mw.cmd = reinterpret_cast<int*>(smem + (int64_t)nv * D);   // team scratch area
+    mw.cmd = reinterpret_cast<int*>(smem + (int64_t)nvs * D);   // team scratch area
     mw.epoch = 0;
-    // TMA pipeline region: stages (128-B aligned) | mbarriers | per-warp counters
-    const int nwarps = blockDim.x >> 5;
+    // exchange index base (row sharding): the pass count of earlier launches
+    if (mw.a.world > 0) mw.a.xbase = __ldcg(mw.a.mail_epoch);
+    // TMA pipeline region: stages (128-B aligned) | mbarriers | per-ring counters;
+    // one ring per warp (the driver warp's is unused)
+    const int rings = (int)(blockDim.x >> 5);
     uintptr_t pb = reinterpret_cast<uintptr_t>(mw.red_s + mw.a.p + 2);
     pb = (pb + 127) & ~(uintptr_t)127;
     mw.a.stages = reinterpret_cast<unsigned char*>(pb);
-    mw.a.mbar = reinterpret_cast<uint64_t*>(pb + (size_t)nwarps * mw.a.nstage * mw.a.stage_bytes);
-    mw.a.pipe = reinterpret_cast<WarpPipe*>(mw.a.mbar + nwarps * mw.a.nstage);
+    mw.a.mbar = reinterpret_cast<uint64_t*>(pb + (size_t)rings * mw.a.nstage * mw.a.stage_bytes);
+    mw.a.pipe = reinterpret_cast<WarpPipe*>(mw.a.mbar + rings * mw.a.nstage);
     if ((threadIdx.x >> 5) == 0) {
-      // driver warp: the whole NUTS state machine, warp-synchronous.  The
-      // engine is a local object whose member functions are all inlined, so
-      // its scalar state can live in registers.
+      // driver warp: the whole NUTS state machine, warp-synchronous
       Engine<WarpTeam, MW> E;
       E.M = mw;
       E.D = D;
@@ -273,7 +289,7 @@ __global__ void __launch_bounds__(256, 1) k_block_op(MW mw, int D, int nslots, i
       E.prof = (blockIdx.x == 0) ? mw.a.prof : nullptr;
       E.prof_last = 0;
       E.tr = nullptr;
-      E.ss = reinterpret_cast<SlotScalars*>(smem + (int64_t)nv * D + 64);
+      E.ss = reinterpret_cast<SlotScalars*>(smem + (int64_t)nvs * D + 64);
       __syncwarp();
       do_op(E, A, chain, writer);
       E.M.release_workers();
@@ -281,6 +297,7 @@ __global__ void __launch_bounds__(256, 1) k_block_op(MW mw, int D, int nslots, i
       logistic_pipeline_init(mw.a);
       mw.serve(S);
       logistic_pipeline_drain(mw.a);
+      if (mw.a.world > 0 && blockIdx.x == 0 && wk_tid() == 0) *mw.a.mail_epoch = mw.a.xbase + mw.epoch;
     }
   }
 }

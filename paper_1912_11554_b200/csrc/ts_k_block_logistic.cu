@@ -1,4 +1,11 @@
-// BlockTeam kernel for the logistic model: cooperative persistent grid.
+// Launcher of the logistic model's cooperative persistent grid (k_block_op<LogisticW>).
+//
+// Shared memory per CTA:
+//   engine vectors (all, or only the hot ones for wide p) | team scratch |
+//   model scratch (wred) | CTA partial sums | TMA ring(s) | mbarriers | ring counters
+// One ring of `nstage` tiles per worker warp: 32-row tiles for p <= 64,
+// 8-row tiles (32p+16 bytes) for 64 < p <= 256 (wide), where the NodeStore
+// slot vectors also move to a per-CTA global workspace.
 #include <stdio.h>
 #include <stdlib.h>
 #include "ts_internal.cuh"
@@ -6,38 +13,45 @@
 namespace ts_internal {
 
 int launch_block_logistic(const ts_model* m, int nslots, OpArgs& A, cudaStream_t st) {
-  const int PMAX = m->pmax;
   LogisticW mw;
+  memset(&mw, 0, sizeof mw);
   mw.a.xt = m->xt; mw.a.yt = m->yt; mw.a.n_rows = m->n_rows; mw.a.p = m->p; mw.a.ntiles = m->ntiles;
   mw.a.pbuf = m->pbuf; mw.a.bar = m->bar; mw.a.fp64 = m->fp64; mw.a.pmax = m->pmax;
-  mw.wred = nullptr; mw.red_s = nullptr; mw.epoch = 0;
+  mw.a.wide = m->wide;
+  mw.a.prof = m->prof;
+  mw.a.exact_cvt = m->exact_cvt;
+  mw.a.dump = m->dump;
+  if (m->world > 0) {
+    mw.a.world = m->world;
+    mw.a.rank = m->rank;
+    for (int r = 0; r < m->world; ++r) mw.a.mail[r] = m->mail[r];
+    mw.a.mail_epoch = m->mail_local + mail_words(m->p, m->world);
+  }
   const int threads = 256;
   const int nwarps = threads / 32;
-  int scratch = (nwarps * (PMAX + 2) + 1) & ~1;
+  const int D = m->dim;
+  int scratch = m->wide ? 2 * m->p + 6 : (nwarps * (m->pmax + 2) + 1) & ~1;  // wide: fixed-point CTA totals
   if (scratch < threads) scratch = threads;
   if (scratch < m->p + 2) scratch = m->p + 2;
-  const int D = m->dim;
-  const size_t base = ((size_t)num_vecs(nslots) * D + kTeamScratch + 2 + scratch + (m->p + 2)) * sizeof(double) + 128;
+  const int nv_smem = m->wide ? (int)V_SLOT0 : num_vecs(nslots);
+  const size_t base = ((size_t)nv_smem * D + kTeamScratch + 2 + scratch + (m->p + 2)) * sizeof(double) + 128;
   int dev = 0, nsm = 0, smem_max = 0;
   TS_CUDA(cudaGetDevice(&dev));
   TS_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
   TS_CUDA(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-  // per-warp TMA ring: as many stages (<= 4) as shared memory allows
-  const int stage_bytes = ((128 * m->p + 32) + 127) / 128 * 128;
-  // Two stages per worker warp: enough bytes in flight to saturate HBM, and
-  // the rest of the 256 KB L1/shared array stays L1 for the engine's stack.
+  const int64_t tile_bytes = m->wide ? wide_tile_bytes(m->p) : 128 * (int64_t)m->p + 32;
+  const int stage_bytes = (int)((tile_bytes + 127) / 128 * 128);
+  // Two stages per worker warp are enough bytes in flight to saturate HBM
+  // and leave the rest of the L1/shared array to the engine's stack.
+  const int rings = nwarps;
   int nstage = 2;
   if (const char* e = getenv("TS_NSTAGE")) nstage = atoi(e) < 1 ? 1 : (atoi(e) > 4 ? 4 : atoi(e));  // profiling
-  auto need = [&](int ns) { return base + (size_t)nwarps * ns * (stage_bytes + 8) + nwarps * 16; };
+  auto need = [&](int ns) { return base + (size_t)rings * ns * (stage_bytes + 8) + rings * 16; };
   while (nstage > 1 && need(nstage) > (size_t)smem_max) --nstage;
   if (need(nstage) > (size_t)smem_max)
     return set_err(TS_EUNSUPPORTED, "logistic model: shared memory too small for D / max_tree_depth");
   mw.a.nstage = nstage;
   mw.a.stage_bytes = stage_bytes;
-  mw.a.l2_keep_tiles = 0;
-  mw.a.prof = m->prof;
-  mw.a.l2_prefetch = 0;
-  mw.a.exact_cvt = m->exact_cvt;
   if (const char* e = getenv("TS_L2_PREFETCH")) mw.a.l2_prefetch = atoi(e);
   if (const char* e = getenv("TS_L2_KEEP_FRAC")) mw.a.l2_keep_tiles = (int)(atof(e) * (double)m->ntiles);
   const size_t smem = need(nstage);
@@ -50,15 +64,25 @@ int launch_block_logistic(const ts_model* m, int nslots, OpArgs& A, cudaStream_t
   if (m->grid > 0 && m->grid < grid) grid = m->grid;
   if (grid > m->ntiles) grid = m->ntiles;
   if (grid < 1) grid = 1;
+  if (m->wide) {  // per-CTA NodeStore slot vectors in global memory
+    ts_model* mm = const_cast<ts_model*>(m);
+    const size_t need_ws = (size_t)grid * kSlotVecs * (nslots < 1 ? 1 : nslots) * D;
+    if (mm->slotws_size < need_ws) {
+      if (mm->slotws) cudaFree(mm->slotws);
+      mm->slotws = nullptr;
+      mm->slotws_size = 0;
+      TS_CUDA(cudaMalloc((void**)&mm->slotws, need_ws * sizeof(double)));
+      mm->slotws_size = need_ws;
+    }
+    mw.a.slotws = mm->slotws;
+  }
   TS_CUDA(cudaMemsetAsync(m->bar, 0, sizeof(unsigned long long), st));
-  // component-major partial slots are padded to 16 CTAs; padding must read 0
-  const size_t gpad = ((size_t)grid + 15) / 16 * 16;
-  TS_CUDA(cudaMemsetAsync(m->pbuf, 0, 2 * gpad * (m->p + 2) * sizeof(double), st));
+  // rotating fixed-point accumulators start at zero (3 x (2*(p+2) + 2) words)
+  TS_CUDA(cudaMemsetAsync(m->pbuf, 0, 3 * (2 * (size_t)(m->p + 2) + 2) * sizeof(unsigned long long), st));
   int Dv = D, ns = nslots, sc = scratch;
   void* args[] = {&mw, &Dv, &ns, &sc, &A};
   TS_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3((unsigned)grid), dim3(threads), args, smem, st));
   return TS_OK;
 }
-
 
 }  // namespace ts_internal

@@ -63,8 +63,24 @@ struct LogisticArgs {
   int l2_keep_tiles;        // tiles [0, l2_keep_tiles) loaded with L2::evict_last, rest evict_first
   int l2_prefetch;          // tiles per warp prefetched into L2 at the end of a pass
   int exact_cvt;            // X holds fp32 subnormals (informational)
+  int wide;                 // p > 64: 8-row row-major tiles (logistic_cta_pass_wide)
+  double* slotws;           // wide p: NodeStore slot vectors in global memory [grid][5*nslots][D]
   unsigned long long* prof; // optional: CTA-0 cycle counters [prior, pass, barrier, reduce] (profiling)
+  // row sharding across GPUs (ts_peer_mailbox_*): world > 0 enables the exchange
+  int world, rank;
+  unsigned long long* mail[8];    // every rank's mailbox, mapped into this process (mail_layout below)
+  unsigned long long* mail_epoch; // this rank's exchange counter, persistent across launches
+  unsigned long long xbase;       // *mail_epoch at kernel start
+  unsigned long long* dump;       // optional: raw local totals of the first pass (ts_logistic_partial_sums)
 };
+
+// Mailbox of one rank: kMailFlags words of flags (flag[src] = 1 + the last
+// exchange index src published here), then 3 rotating slots x world x
+// (2*(p+2)+2) words of fixed-point totals.
+constexpr int kMailFlags = 16;
+__host__ __device__ inline int64_t mail_words(int p, int world) {
+  return kMailFlags + 3 * (int64_t)world * (2 * (int64_t)(p + 2) + 2);
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -116,6 +132,14 @@ __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 __device__ __forceinline__ void red_release_add_u64(unsigned long long* p, unsigned long long v) {
   asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
@@ -124,22 +148,33 @@ __device__ __forceinline__ void red_add_u64(unsigned long long* p, unsigned long
   asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-// Exact split of a double into two int64 fixed-point words,
-//   v = hi * 2^-10 + lo * 2^-63,   hi = floor(v * 2^10),  0 <= lo < 2^53,
-// valid for |v| < 2^43 (false otherwise or if v is not finite).  Sums of up
-// to 2^8 such pairs cannot overflow, and v - hi*2^-10 is computed exactly
-// (both are multiples of ulp(v) and differ by less than 2^-10).  Truncation
-// of bits below 2^-63 is the only error.
+// Fixed-point pair of a double (all reductions across warps, CTAs and GPUs
+// add these integers, so totals do not depend on the order of arrival):
+//   v ~= hi * 2^-10 + lo * 2^-61,  hi = round(v * 2^10),  |lo| <= 2^50,
+// both rounded to nearest-even with the 1.5*2^52 magic constant (two FMAs
+// and integer subtractions, no float->int64 conversion instructions, which
+// are multi-cycle on the XU pipe).  v - hi*2^-10 is exact, so rounding below
+// 2^-61 is the only error.  Valid for |v| < 2^40 (false otherwise or if v is
+// not finite).  Canonical pair: lo in [0, 2^51) (fx_canon), where a pair's
+// words are exact doubles.
+constexpr int kFxLoBits = 51;
+constexpr unsigned long long kFxLoMask = (1ULL << kFxLoBits) - 1;  // one hi unit = 2^51 lo units
 __device__ __forceinline__ bool fx_split(double v, long long& hi, long long& lo) {
-  if (!(fabs(v) < 8796093022208.0)) { hi = 0; lo = 0; return false; }
-  const double a = floor(v * 1024.0);
-  hi = (long long)a;
-  const double rem = v - a * (1.0 / 1024.0);
-  lo = (long long)(rem * 9223372036854775808.0);
+  const double magic = 6755399441055744.0;  // 1.5 * 2^52
+  if (!(fabs(v) < 1099511627776.0)) { hi = 0; lo = 0; return false; }
+  const double t = __fma_rn(v, 1024.0, magic);
+  hi = __double_as_longlong(t) - __double_as_longlong(magic);
+  const double rem = __fma_rn(-__dsub_rn(t, magic), 1.0 / 1024.0, v);
+  lo = __double_as_longlong(__fma_rn(rem, 2305843009213693952.0, magic)) - __double_as_longlong(magic);
   return true;
 }
-__device__ __forceinline__ double fx_join(long long hi, long long lo) {
-  return (double)hi * (1.0 / 1024.0) + (double)lo * (1.0 / 9223372036854775808.0);
+// canonical form of a (hi, signed lo) sum: lo in [0, 2^51)
+__device__ __forceinline__ void fx_canon(unsigned long long& hi, unsigned long long& lo) {
+  hi += (unsigned long long)((long long)lo >> kFxLoBits);
+  lo &= kFxLoMask;
+}
+__device__ __forceinline__ double fx_join(long long hi, unsigned long long lo_canon) {
+  return (double)hi * (1.0 / 1024.0) + (double)lo_canon * (1.0 / 2305843009213693952.0);
 }
 
 // Grid barrier #epoch (0-based) over gridDim.x co-resident CTAs.
@@ -234,9 +269,9 @@ struct Producer {
 
 // Kernel prologue (worker warps): mbarriers and pipe counters.
 static __device__ void logistic_pipeline_init(const LogisticArgs& a) {
-  const int nwarps = wk_nwarps();
-  for (int i = wk_tid(); i < nwarps * a.nstage; i += wk_threads()) mbar_init(a.mbar + i, 1);
-  for (int i = wk_tid(); i < nwarps; i += wk_threads()) { a.pipe[i].issued = 0; a.pipe[i].consumed = 0; }
+  const int rings = wk_nwarps();
+  for (int i = wk_tid(); i < rings * a.nstage; i += wk_threads()) mbar_init(a.mbar + i, 1);
+  for (int i = wk_tid(); i < rings; i += wk_threads()) { a.pipe[i].issued = 0; a.pipe[i].consumed = 0; }
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   wk_sync();
 }
@@ -289,7 +324,7 @@ __device__ __forceinline__ void row_from_stage(const unsigned char* sb, int p_rt
 // red_out[0..p) = sum resid*x_j, red_out[p] = sum resid, red_out[p+1] = sum (y eta - log1pexp)
 // (wred: >= nwarps*(PMAX+2) doubles of scratch).
 template <int PMAX, bool FP64, int PE>
-__device__ __forceinline__ void logistic_cta_pass(const LogisticArgs& a, const double* __restrict__ theta_s, double* wred,
+__device__ __noinline__ void logistic_cta_pass(const LogisticArgs& a, const double* __restrict__ theta_s, double* wred,
                                                   double* red_out) {
   const int lane = threadIdx.x & 31, warp = wk_warp(), nwarps = wk_nwarps();
   const int p = PE > 0 ? PE : a.p;
@@ -449,8 +484,244 @@ __device__ __forceinline__ void logistic_cta_pass(const LogisticArgs& a, const d
   if (prof) { pc1 = clock64(); a.prof[7] += pc1 - pc0; }
 }
 
+// ---------------------------------------------------------------- wide p
+// p in (64, kWideMax]: a tile is kWideRows = 8 rows in the input's row-major
+// order followed by 16 bytes holding the 8 labels (+ 8 zero bytes), one TMA
+// bulk copy of 32p+16 bytes.  Each worker warp owns a ring of these tiles
+// (same periodic tile sequence and run-ahead producer as p <= 64).
+//
+// Per tile, in two groups of 4 rows: lane l holds features l, l+32, ... of
+// each row in registers (conflict-free LDS from the row-major stage), forms
+// 4 partial dot products, and a reduce-scatter over the warp (6 shuffles for
+// 4 rows instead of 20) leaves each lane with the full sum of one row; that
+// lane evaluates the row's sigmoid / log1pexp, 4 shuffles broadcast the
+// residuals, and the gradient contributions go into per-lane feature
+// accumulators from the same registers.  No CTA synchronisation inside the
+// pass; X elements are read from shared memory (and, in the FP64 policy,
+// converted to double) exactly once.
+constexpr int kWideMax = 256;
+constexpr int kWideRows = 8;
+__host__ __device__ inline int64_t wide_tile_bytes(int p) { return 32 * (int64_t)p + 16; }
+
+struct WideProducer {
+  unsigned char* ring;
+  uint64_t* bars;
+  const unsigned char* src;    // next tile to issue
+  const unsigned char* first;  // this warp's first tile
+  int64_t step;                // bytes between this warp's tiles (nwarps tiles)
+  int64_t tj, count;
+  int s, nstage, stage_bytes;
+  uint32_t tb;
+  uint64_t pol;
+
+  __device__ __forceinline__ void init(const LogisticArgs& a, const WarpTiles& wt, unsigned long long issued) {
+    const int warp = wk_warp();
+    nstage = a.nstage;
+    stage_bytes = a.stage_bytes;
+    ring = a.stages + (int64_t)warp * nstage * stage_bytes;
+    bars = a.mbar + warp * nstage;
+    s = (int)(issued % (unsigned long long)nstage);
+    count = wt.count;
+    tj = (int64_t)(issued % (unsigned long long)count);
+    tb = (uint32_t)wide_tile_bytes(a.p);
+    first = reinterpret_cast<const unsigned char*>(a.xt) + wt.first * (int64_t)tb;
+    step = (int64_t)wt.nwarps * tb;
+    src = first + tj * step;
+    pol = policy_evict_first();
+  }
+  __device__ __forceinline__ void issue() {
+    uint64_t* bar = bars + s;
+    mbar_expect_tx(bar, tb);
+    bulk_g2s(ring + (int64_t)s * stage_bytes, src, tb, bar, pol);
+    if (++s == nstage) s = 0;
+    if (++tj == count) { tj = 0; src = first; }
+    else src += step;
+  }
+};
+
+template <bool FP64, int KL>  // KL = features per lane (p <= 32 KL)
+__device__ __noinline__ void logistic_cta_pass_wide(const LogisticArgs& a, const double* __restrict__ theta_s,
+                                                       double* wred, double* red_out) {
+  using acc_t = typename std::conditional<FP64, double, float>::type;
+  constexpr int R = 4;               // rows per group
+  const int lane = threadIdx.x & 31, warp = wk_warp(), nw = wk_nwarps();
+  const int p = a.p;
+  const WarpTiles wt = warp_tiles(a);
+  const bool prof = a.prof != nullptr && blockIdx.x == 0 && wk_tid() == 0;
+  long long pc0 = prof ? clock64() : 0, pc1;
+
+  acc_t th[KL];
+#pragma unroll
+  for (int m = 0; m < KL; ++m) th[m] = (lane + 32 * m < p) ? (acc_t)theta_s[lane + 32 * m] : (acc_t)0;
+  const acc_t thb = (acc_t)theta_s[p];
+  // Exact fixed-point accumulators (fx_split units): [0, KL) features
+  // lane + 32 m, KL residual sum, KL + 1 log-likelihood (lanes 0, 8, 16, 24).
+  // Each tile's partial sums are converted exactly, so the totals do not
+  // depend on which warp, CTA or GPU processed a tile (row sharding).
+  constexpr int NF = KL + 2;
+  unsigned long long fh[NF], fl[NF];  // (hi, signed lo) sums, wrapping
+#pragma unroll
+  for (int m = 0; m < NF; ++m) { fh[m] = 0; fl[m] = 0; }
+  bool bad = false;
+  int since_norm = 0;
+  unsigned long long* tot = reinterpret_cast<unsigned long long*>(wred);  // CTA totals [2*(p+2)] + flag
+  for (int i = wk_tid(); i < 2 * (p + 2) + 1; i += wk_threads()) tot[i] = 0ULL;
+  wk_sync();
+  // after the reduce-scatter, lane holds row (bit 4, bit 3) of the group
+  const int my_r = ((lane >> 3) & 2) | ((lane >> 3) & 1);
+  const bool up16 = (lane & 16) != 0, up8 = (lane & 8) != 0;
+
+  if (wt.count > 0) {
+    WarpPipe& pipe = a.pipe[warp];
+    const unsigned long long c0 = pipe.consumed;
+    unsigned long long issued = pipe.issued;
+    WideProducer prod;
+    if (lane == 0) {
+      prod.init(a, wt, issued);
+      while (issued < c0 + (unsigned long long)a.nstage) { prod.issue(); ++issued; }
+    }
+    int s = (int)(c0 % (unsigned long long)a.nstage);
+    uint32_t parity = (uint32_t)((c0 / a.nstage) & 1ULL);
+    int64_t tj = (int64_t)(c0 % (unsigned long long)wt.count);
+    const unsigned char* ring = a.stages + (int64_t)warp * a.nstage * a.stage_bytes;
+    uint64_t* bars = a.mbar + warp * a.nstage;
+    if (prof) { pc1 = clock64(); a.prof[4] += pc1 - pc0; pc0 = pc1; }
+    for (int64_t j = 0; j < wt.count; ++j) {
+      mbar_wait(bars + s, parity);
+      const unsigned char* sb = ring + (int64_t)s * a.stage_bytes;
+      const float* xs = reinterpret_cast<const float*>(sb);
+      const int64_t row0 = (wt.first + tj * wt.nwarps) * kWideRows;
+      acc_t tacc[KL];
+#pragma unroll
+      for (int m = 0; m < KL; ++m) tacc[m] = 0;
+      acc_t tb_sum = 0, tl_sum = 0;
+#pragma unroll
+      for (int g = 0; g < kWideRows; g += R) {
+        acc_t xv[R][KL];
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+          for (int m = 0; m < KL; ++m) {
+            const int f = lane + 32 * m;
+            xv[r][m] = (f < p) ? (acc_t)xs[(g + r) * p + f] : (acc_t)0;
+          }
+        const int yr = g + my_r;
+        const uint8_t yb = sb[32 * p + yr];
+        if (g + R == kWideRows) {
+          // the stage is fully read: refill it (wrapping into the next pass)
+          __syncwarp();
+          if (lane == 0) { prod.issue(); ++issued; }
+        }
+        acc_t e[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          acc_t a0 = 0, a1 = 0;
+#pragma unroll
+          for (int m = 0; m < KL; m += 2) {
+            if constexpr (FP64) {
+              a0 = __fma_rn(xv[r][m], th[m], a0);
+              a1 = __fma_rn(xv[r][m + 1], th[m + 1], a1);
+            } else {
+              a0 = __fmaf_rn(xv[r][m], th[m], a0);
+              a1 = __fmaf_rn(xv[r][m + 1], th[m + 1], a1);
+            }
+          }
+          e[r] = a0 + a1;
+        }
+        // reduce-scatter of 4 row sums over the warp (fixed order)
+        acc_t k0 = up16 ? e[2] : e[0], k1 = up16 ? e[3] : e[1];
+        k0 += __shfl_xor_sync(0xffffffffu, up16 ? e[0] : e[2], 16);
+        k1 += __shfl_xor_sync(0xffffffffu, up16 ? e[1] : e[3], 16);
+        acc_t k = up8 ? k1 : k0;
+        k += __shfl_xor_sync(0xffffffffu, up8 ? k0 : k1, 8);
+        k += __shfl_xor_sync(0xffffffffu, k, 4);
+        k += __shfl_xor_sync(0xffffffffu, k, 2);
+        k += __shfl_xor_sync(0xffffffffu, k, 1);
+        const acc_t eta = k + thb;
+        const bool valid = row0 + yr < a.n_rows;
+        const acc_t yv = (acc_t)yb;
+        acc_t resid, llt;
+        if constexpr (FP64) {
+          const double ex = exp(-fabs(eta));
+          const double l = fmax(eta, 0.0) + log1p(ex);
+          const double sig = __ddiv_rn(eta >= 0.0 ? 1.0 : ex, 1.0 + ex);
+          resid = valid ? yv - sig : 0.0;
+          llt = valid ? (yv * eta - l) : 0.0;
+        } else {
+          const float ex = expf(-fabsf(eta));
+          const float l = fmaxf(eta, 0.f) + log1pf(ex);
+          const float sig = __fdiv_rn(eta >= 0.f ? 1.f : ex, 1.f + ex);
+          resid = valid ? yv - sig : 0.f;
+          llt = valid ? __fmaf_rn(yv, eta, -l) : 0.f;
+        }
+        if ((lane & 7) == 0) { tb_sum += resid; tl_sum += llt; }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const acc_t rr = __shfl_sync(0xffffffffu, resid, ((r >> 1) << 4) | ((r & 1) << 3));
+#pragma unroll
+          for (int m = 0; m < KL; ++m) {
+            if constexpr (FP64) tacc[m] = __fma_rn(rr, xv[r][m], tacc[m]);
+            else tacc[m] = __fmaf_rn(rr, xv[r][m], tacc[m]);
+          }
+        }
+      }
+#pragma unroll
+      for (int m = 0; m < NF; ++m) {
+        const double v = (m < KL) ? (double)tacc[m < KL ? m : 0] : (double)(m == KL ? tb_sum : tl_sum);
+        long long h, l;
+        bad |= !fx_split(v, h, l);
+        fh[m] += (unsigned long long)h;
+        fl[m] += (unsigned long long)l;
+      }
+      if (++since_norm == 1024) {  // |lo| <= 2^50 per tile: carry before 2^61
+        since_norm = 0;
+#pragma unroll
+        for (int m = 0; m < NF; ++m) fx_canon(fh[m], fl[m]);
+      }
+      if (++s == a.nstage) { s = 0; parity ^= 1u; }
+      if (++tj == wt.count) tj = 0;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      pipe.consumed = c0 + (unsigned long long)wt.count;
+      pipe.issued = issued;
+    }
+    __syncwarp();
+  }
+  if (prof) { pc1 = clock64(); a.prof[5] += pc1 - pc0; pc0 = pc1; }
+  // CTA totals: shared-memory integer atomics (order-free)
+#pragma unroll
+  for (int m = 0; m < NF; ++m) fx_canon(fh[m], fl[m]);
+#pragma unroll
+  for (int m = 0; m < KL; ++m) {
+    const int f = lane + 32 * m;
+    if (f < p) {
+      atomicAdd(tot + 2 * f, fh[m]);
+      atomicAdd(tot + 2 * f + 1, fl[m]);
+    }
+  }
+  if ((lane & 7) == 0) {
+    atomicAdd(tot + 2 * p, fh[KL]);
+    atomicAdd(tot + 2 * p + 1, fl[KL]);
+    atomicAdd(tot + 2 * p + 2, fh[KL + 1]);
+    atomicAdd(tot + 2 * p + 3, fl[KL + 1]);
+  }
+  if (bad) atomicOr(tot + 2 * (p + 2), 1ULL);
+  if (prof) { pc1 = clock64(); a.prof[7] += pc1 - pc0; }
+}
+
 static __device__ __forceinline__ void logistic_cta_dispatch(const LogisticArgs& a, const double* theta, double* wred,
                                                              double* red_s) {
+  if (a.wide) {
+    if (a.p <= 128) {
+      if (a.fp64) logistic_cta_pass_wide<true, 4>(a, theta, wred, red_s);
+      else logistic_cta_pass_wide<false, 4>(a, theta, wred, red_s);
+    } else {
+      if (a.fp64) logistic_cta_pass_wide<true, 8>(a, theta, wred, red_s);
+      else logistic_cta_pass_wide<false, 8>(a, theta, wred, red_s);
+    }
+    return;
+  }
   if (a.p == 54) {  // covtype's feature count: compile-time row layout
     if (a.fp64) logistic_cta_pass<56, true, 54>(a, theta, wred, red_s);
     else logistic_cta_pass<56, false, 54>(a, theta, wred, red_s);
@@ -491,12 +762,23 @@ static __device__ void logistic_eval_grid(const LogisticArgs& a, const VecStore&
   unsigned long long* accb = reinterpret_cast<unsigned long long*>(a.pbuf);
   const int64_t bstride = 2 * (int64_t)P2 + 2;
   unsigned long long* cur = accb + (int64_t)(epoch % 3ULL) * bstride;
-  for (int d = wk_tid(); d < P2; d += wk_threads()) {
-    long long hi, lo;
-    const bool ok = fx_split(red_s[d], hi, lo);
-    red_add_u64(cur + 2 * d, (unsigned long long)hi);
-    red_add_u64(cur + 2 * d + 1, (unsigned long long)lo);
-    if (!ok) red_add_u64(cur + 2 * P2, 1ULL);  // non-finite / out-of-range partial
+  if (a.wide) {  // the wide pass leaves exact fixed-point CTA totals in wred
+    const unsigned long long* tot = reinterpret_cast<const unsigned long long*>(wred);
+    for (int d = wk_tid(); d < P2; d += wk_threads()) {
+      unsigned long long hi = tot[2 * d], lo = tot[2 * d + 1];
+      fx_canon(hi, lo);
+      red_add_u64(cur + 2 * d, hi);
+      red_add_u64(cur + 2 * d + 1, lo);
+    }
+    if (wk_tid() == 0 && tot[2 * P2] != 0ULL) red_add_u64(cur + 2 * P2, 1ULL);
+  } else {
+    for (int d = wk_tid(); d < P2; d += wk_threads()) {
+      long long hi, lo;
+      const bool ok = fx_split(red_s[d], hi, lo);
+      red_add_u64(cur + 2 * d, (unsigned long long)hi);
+      red_add_u64(cur + 2 * d + 1, (unsigned long long)lo);
+      if (!ok) red_add_u64(cur + 2 * P2, 1ULL);  // non-finite / out-of-range partial
+    }
   }
   wk_sync();
   if (wk_tid() == 0) {
@@ -523,14 +805,65 @@ static __device__ void logistic_eval_grid(const LogisticArgs& a, const VecStore&
   epoch += 1;
   if (prof) { c1 = clock64(); a.prof[2] += c1 - c0; c0 = c1; }
 
+  if (a.dump && epoch == 1 && blockIdx.x == 0)  // test hook: this GPU's totals of the first pass
+    for (int i = wk_tid(); i < 2 * P2 + 1; i += wk_threads()) a.dump[i] = __ldcg(cur + i);
+
   double* g = S.v(gid);
-  const bool bad = __ldcg(reinterpret_cast<const long long*>(cur + 2 * P2)) != 0;
-  for (int d = wk_tid(); d < P2; d += wk_threads()) {
-    const long long hi = __ldcg(reinterpret_cast<const long long*>(cur + 2 * d));
-    const long long lo = __ldcg(reinterpret_cast<const long long*>(cur + 2 * d + 1));
-    const double s = bad ? __longlong_as_double(0x7ff8000000000000LL) : fx_join(hi, lo);
-    if (d <= p) g[d] = theta[d] - s;
-    else red_s[0] = s;  // sum of log-likelihood terms
+  if (a.world > 0) {
+    // Row sharding across GPUs: CTA 0 pushes this GPU's totals into slot
+    // x % 3 of every rank's mailbox (NVLink stores to peer memory), then
+    // raises its flag there; every CTA waits for all `world` flags of pass x
+    // and adds the copies -- integer sums, so every rank gets the same bits.
+    // A slot is rewritten 3 passes later, when every rank has consumed it.
+    const int W = a.world;
+    const unsigned long long x = a.xbase + (epoch - 1);
+    const int64_t slot = (int64_t)(x % 3ULL);
+    const int nwords = 2 * P2 + 1;
+    if (blockIdx.x == 0) {
+      for (int i = wk_tid(); i < W * nwords; i += wk_threads()) {
+        const int r = i / nwords, w = i - r * nwords;
+        unsigned long long v;
+        if (w < 2 * P2) {  // canonical pair
+          unsigned long long hi = __ldcg(cur + (w & ~1)), lo = __ldcg(cur + (w | 1));
+          fx_canon(hi, lo);
+          v = (w & 1) ? lo : hi;
+        } else {
+          v = __ldcg(cur + w);
+        }
+        a.mail[r][kMailFlags + (slot * W + a.rank) * bstride + w] = v;
+      }
+      __threadfence_system();
+      wk_sync();
+      if (wk_tid() < W) st_release_sys_u64(a.mail[wk_tid()] + a.rank, x + 1);
+    }
+    const unsigned long long* box = a.mail[a.rank];
+    if (wk_tid() < W)
+      while (ld_acquire_sys_u64(box + wk_tid()) < x + 1) {
+      }
+    wk_sync();
+    const unsigned long long* sl = box + kMailFlags + slot * W * bstride;
+    unsigned long long badw = 0;
+    for (int r = 0; r < W; ++r) badw |= __ldcg(sl + r * bstride + 2 * P2);
+    for (int d = wk_tid(); d < P2; d += wk_threads()) {
+      unsigned long long hi = 0, lo = 0;
+      for (int r = 0; r < W; ++r) {
+        hi += __ldcg(sl + r * bstride + 2 * d);
+        lo += __ldcg(sl + r * bstride + 2 * d + 1);
+      }
+      fx_canon(hi, lo);  // both words exact in double
+      const double s = badw ? __longlong_as_double(0x7ff8000000000000LL) : fx_join((long long)hi, lo);
+      if (d <= p) g[d] = theta[d] - s;
+      else red_s[0] = s;
+    }
+  } else {
+    const bool bad = __ldcg(reinterpret_cast<const long long*>(cur + 2 * P2)) != 0;
+    for (int d = wk_tid(); d < P2; d += wk_threads()) {
+      unsigned long long hi = __ldcg(cur + 2 * d), lo = __ldcg(cur + 2 * d + 1);
+      fx_canon(hi, lo);  // both words exact in double
+      const double s = bad ? __longlong_as_double(0x7ff8000000000000LL) : fx_join((long long)hi, lo);
+      if (d <= p) g[d] = theta[d] - s;
+      else red_s[0] = s;  // sum of log-likelihood terms
+    }
   }
   if (prof) { c1 = clock64(); a.prof[3] += c1 - c0; }
 }

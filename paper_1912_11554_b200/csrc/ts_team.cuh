@@ -28,10 +28,13 @@ struct VecStore {
   double* base;    // element (id, d) at base + id*vstride + d*dstride
   int64_t vstride;
   int64_t dstride;
-  __device__ __forceinline__ double* v(int id) const { return base + (int64_t)id * vstride; }
-  __device__ __forceinline__ double& at(int id, int d) const {
-    return base[(int64_t)id * vstride + (int64_t)d * dstride];
+  double* slots = nullptr;  // optional second region for vector ids >= slot0
+  int slot0 = 0;
+  __device__ __forceinline__ double* v(int id) const {
+    if (slots != nullptr && id >= slot0) return slots + (int64_t)(id - slot0) * vstride;
+    return base + (int64_t)id * vstride;
   }
+  __device__ __forceinline__ double& at(int id, int d) const { return v(id)[(int64_t)d * dstride]; }
 };
 
 struct ThreadTeam {

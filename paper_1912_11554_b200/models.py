@@ -42,6 +42,7 @@ class DeviceSpec:
         self.precision = precision
         self._handles: dict = {}
         self._grid = 0
+        self.row_shard = None  # (rank, world) once joined by rowshard.connect
 
     def handle(self, device=None):
         """ts_model* for the given CUDA device (created on first use)."""

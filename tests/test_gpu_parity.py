@@ -108,6 +108,50 @@ def test_logistic_potential_gradient(precision, rel):
             assert close(out[k, 1:], nums(p["g"]), rel, atol=rel * scale), (rec["n"], rec["p"], k)
 
 
+@pytest.mark.parametrize("p", [65, 100, 255])
+@pytest.mark.parametrize("precision,rel", [("fp64", FP64_REL), ("fp32", FP32_REL)])
+def test_wide_logistic_potential_gradient(p, precision, rel, oracle):
+    """Wide-p pass (64 < p <= 256, SURVEY 8(d) config 5 shape) vs the C oracle."""
+    t = ts()
+    from tests_data import logistic_data
+
+    for n in (37, 5000, 70001):
+        x, y = logistic_data(n, p, p + n)
+        m = t.logistic_regression_model(t.LogisticRegressionData(x, y), precision=precision)
+        om = oracle.Model("logistic_regression", p + 1, x=np.ascontiguousarray(x), y=np.ascontiguousarray(y))
+        rng = np.random.default_rng(p)
+        for scale in (0.0, 0.05, 1.0):
+            q = rng.standard_normal(p + 1) * scale
+            got = t.models.potential_and_gradient(m.device_spec, q[None, :])[0]
+            U, g = om.potential(q.tolist()), np.asarray(om.gradient(q.tolist()))
+            assert close(got[0], U, rel), (n, p, scale, got[0], U)
+            assert close(got[1:], g, rel, atol=rel * max(1.0, np.abs(g).max())), (n, p, scale)
+
+
+def test_wide_tree_matches_oracle(oracle):
+    t = ts()
+    from tests_data import logistic_data
+
+    x, y = logistic_data(20000, 255, 7)
+    m = t.logistic_regression_model(t.LogisticRegressionData(x, y))
+    om = oracle.Model("logistic_regression", 256, x=np.ascontiguousarray(x), y=np.ascontiguousarray(y))
+    rng = np.random.default_rng(3)
+    q, r = rng.standard_normal(256) * 0.01, rng.standard_normal(256)
+    U, g = om.potential(q.tolist()), om.gradient(q.tolist())
+    cfg = t.SamplerConfig(step_size=0.003, mass=t.MassMatrix.identity(256), max_tree_depth=8)
+    key = t.RngKey.from_seed(17)
+    z = t.PhasePoint(q, r, U, np.asarray(g))
+    h0 = t.hamiltonian(z, cfg.mass)
+    tr = t.TreeTrace()
+    tree = t.build_tree_iterative(z, 6, 0.003, cfg, m, key, h_ref=h0, trace=tr)
+    ot = oracle.build_tree(oracle.Point(q.tolist(), r.tolist(), U, g), 6, 0.003, [1.0] * 256, om, (key.hi, key.lo), h0)
+    assert (tree.leapfrog_count, tree.turning, tree.diverging, tree.proposal_leaf) == (
+        ot.sub.count, ot.turning, ot.diverging, ot.sub.prop_leaf)
+    assert [tuple(c) for c in tr.checks] == [tuple(c) for c in ot.checks]
+    assert close(tree.right.position, ot.sub.last.q, 1e-10, atol=1e-12)
+    assert close(tree.log_weight, ot.sub.lw, 1e-10)
+
+
 def test_logistic_grid_sizes_agree():
     """Any persistent-grid size gives the same fp64 result up to summation order."""
     t = ts()
@@ -391,3 +435,68 @@ def test_covtype_shape_potential_gradient(precision, rel, oracle):
         g = np.asarray(om.gradient(q.tolist()))
         assert close(got[0], U, rel)
         assert close(got[1:], g, rel, atol=rel * np.abs(g).max())
+
+
+# ----------------------------------------------------------------------------- row sharding (config 5)
+
+
+def _canon(words):
+    t = ts()
+    w = np.asarray(words, dtype=np.uint64).copy()
+    n = (w.size - 1) // 2
+    w[0:2 * n:2], w[1:2 * n:2] = t.rowshard.canonical(w[0:2 * n:2], w[1:2 * n:2])
+    return w
+
+
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_row_shards_compose_exactly(precision):
+    """Wide-p totals are exact fixed-point sums of per-tile partials, so the
+    row shards' totals add up to the single-GPU totals bit for bit, and the
+    (U, gradient) every rank derives equals the one-GPU result exactly."""
+    t = ts()
+    from tests_data import logistic_data
+
+    n, p = 20005, 255
+    x, y = logistic_data(n, p, 11)
+    full = t.logistic_regression_model(t.LogisticRegressionData(x, y), precision=precision).device_spec
+    rng = np.random.default_rng(5)
+    for scale in (0.0, 0.05, 0.5):
+        q = rng.standard_normal(p + 1) * scale
+        ref_words = t.rowshard.partial_sums(full, q)
+        ref_ug = t.models.potential_and_gradient(full, q[None, :])[0]
+        assert np.array_equal(t.rowshard.totals_to_potential_gradient(ref_words, q), ref_ug)
+        for world in (2, 3, 8):
+            parts = []
+            for r in range(world):
+                a, b = t.rowshard.row_range(n, r, world)
+                assert a % 8 == 0
+                m = t.logistic_regression_model(t.LogisticRegressionData(x[a:b], y[a:b]), precision=precision)
+                parts.append(t.rowshard.partial_sums(m.device_spec, q))
+            comb = t.rowshard.combine(parts)
+            assert np.array_equal(_canon(comb), _canon(ref_words)), (world, scale)
+            assert np.array_equal(t.rowshard.totals_to_potential_gradient(comb, q), ref_ug)
+
+
+@pytest.mark.parametrize("p", [54, 255])
+def test_row_shard_mailbox_world1_identical(p):
+    """world = 1 runs the peer-exchange device path (push, flag, wait, sum)
+    against its own mailbox: results equal the unconnected model's bitwise,
+    across launches (persistent exchange counter)."""
+    t = ts()
+    from tests_data import logistic_data
+
+    x, y = logistic_data(30000, p, 2)
+    plain = t.logistic_regression_model(t.LogisticRegressionData(x, y), precision="fp32")
+    shard = t.logistic_regression_model(t.LogisticRegressionData(x, y), precision="fp32")
+    t.rowshard.connect(shard.device_spec, 0, 1, lambda b: [b])
+    assert shard.device_spec.row_shard == (0, 1)
+    q = np.random.default_rng(1).standard_normal((3, p + 1)) * 0.05
+    a = t.models.potential_and_gradient(plain.device_spec, q)
+    b = t.models.potential_and_gradient(shard.device_spec, q)
+    assert np.array_equal(a, b)
+    cfg = t.RunConfig(model={}, num_chains=1, num_warmup=30, num_samples=20, seed=4)
+    for _ in range(2):
+        ra = t.run_device(plain, cfg, t.chain_keys(4, 1), 0)
+        rb = t.run_device(shard, cfg, t.chain_keys(4, 1), 0)
+        assert np.array_equal(ra.samples.cpu().numpy(), rb.samples.cpu().numpy())
+        assert np.array_equal(ra.stats.cpu().numpy(), rb.stats.cpu().numpy())

@@ -234,3 +234,18 @@ def test_model_from_descriptor_and_csv(tmp_path):
     assert es.dim == 10
     with pytest.raises(ValueError):
         t.model_from_descriptor({"model": "nope"})
+
+
+def test_chunked_generator_matches_one_shot():
+    """bench.py builds config 5 (8M x 255) with the chunked generator; it must
+    reproduce tests_data.logistic_data exactly."""
+    from tests_data import logistic_data, logistic_data_f32
+
+    for n, p, chunk in ((10000, 255, 999), (4097, 54, 4096), (5, 3, 2)):
+        x, y = logistic_data(n, p, 20191223)
+        x32, y8 = logistic_data_f32(n, p, 20191223, chunk_rows=chunk)
+        assert np.array_equal(x.astype(np.float32), x32)
+        assert np.array_equal(y.astype(np.uint8), y8)
+        for a, b in ((0, n // 3), (n // 3, n), (n // 2, n // 2 + 1)):
+            xs, ys = logistic_data_f32(n, p, 20191223, chunk_rows=chunk, rows=(a, b))
+            assert np.array_equal(xs, x32[a:b]) and np.array_equal(ys, y8[a:b])

@@ -159,7 +159,8 @@ extern "C" int ts_model_create(int kind, int dim, const double* params, int n_pa
       m->wide = n_feat > 64;
       m->n_rows = n_rows;
       m->p = n_feat;
-      m->ntiles = m->wide ? (n_rows + kWideRows - 1) / kWideRows : (n_rows + 31) / 32;
+      // wide: whole groups of kWideGroup tiles (32 rows), padding rows zero with label 0
+      m->ntiles = m->wide ? (n_rows + kWideRows * kWideGroup - 1) / (kWideRows * kWideGroup) * kWideGroup : (n_rows + 31) / 32;
       m->fp64 = precision == TS_PREC_FP64;
       const size_t xbytes = m->wide ? (size_t)m->ntiles * wide_tile_bytes(n_feat) : (size_t)m->ntiles * 32 * n_feat * sizeof(float);
       if (cudaMalloc((void**)&m->xt, xbytes) != cudaSuccess) return fail(TS_ECUDA, "cudaMalloc X failed");

@@ -273,8 +273,8 @@ __global__ void __launch_bounds__(256, 1) k_block_op(MW mw, int D, int nslots, i
     // exchange index base (row sharding): the pass count of earlier launches
     if (mw.a.world > 0) mw.a.xbase = __ldcg(mw.a.mail_epoch);
     // TMA pipeline region: stages (128-B aligned) | mbarriers | per-ring counters;
-    // one ring per warp (the driver warp's is unused)
-    const int rings = (int)(blockDim.x >> 5);
+    // one ring per worker warp
+    const int rings = (int)(blockDim.x >> 5) - 1;
     uintptr_t pb = reinterpret_cast<uintptr_t>(mw.red_s + mw.a.p + 2);
     pb = (pb + 127) & ~(uintptr_t)127;
     mw.a.stages = reinterpret_cast<unsigned char*>(pb);

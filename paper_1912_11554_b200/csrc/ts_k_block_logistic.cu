@@ -30,7 +30,7 @@ int launch_block_logistic(const ts_model* m, int nslots, OpArgs& A, cudaStream_t
   const int threads = 256;
   const int nwarps = threads / 32;
   const int D = m->dim;
-  int scratch = m->wide ? 2 * m->p + 6 : (nwarps * (m->pmax + 2) + 1) & ~1;  // wide: fixed-point CTA totals
+  int scratch = m->wide ? wide_scratch_doubles(nwarps - 1) : (nwarps * (m->pmax + 2) + 1) & ~1;
   if (scratch < threads) scratch = threads;
   if (scratch < m->p + 2) scratch = m->p + 2;
   const int nv_smem = m->wide ? (int)V_SLOT0 : num_vecs(nslots);
@@ -39,11 +39,10 @@ int launch_block_logistic(const ts_model* m, int nslots, OpArgs& A, cudaStream_t
   TS_CUDA(cudaGetDevice(&dev));
   TS_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
   TS_CUDA(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-  const int64_t tile_bytes = m->wide ? wide_tile_bytes(m->p) : 128 * (int64_t)m->p + 32;
-  const int stage_bytes = (int)((tile_bytes + 127) / 128 * 128);
+  const int stage_bytes = m->wide ? wide_stage_bytes(m->p) : (int)((128 * (int64_t)m->p + 32 + 127) / 128 * 128);
   // Two stages per worker warp are enough bytes in flight to saturate HBM
   // and leave the rest of the L1/shared array to the engine's stack.
-  const int rings = nwarps;
+  const int rings = nwarps - 1;  // worker warps
   int nstage = 2;
   if (const char* e = getenv("TS_NSTAGE")) nstage = atoi(e) < 1 ? 1 : (atoi(e) > 4 ? 4 : atoi(e));  // profiling
   auto need = [&](int ns) { return base + (size_t)rings * ns * (stage_bytes + 8) + rings * 16; };

@@ -270,6 +270,11 @@ struct Producer {
 // Kernel prologue (worker warps): mbarriers and pipe counters.
 static __device__ void logistic_pipeline_init(const LogisticArgs& a) {
   const int rings = wk_nwarps();
+  if (a.wide) {
+    uint32_t* z = reinterpret_cast<uint32_t*>(a.stages);
+    const int nw = rings * a.nstage * a.stage_bytes / 4;
+    for (int i = wk_tid(); i < nw; i += wk_threads()) z[i] = 0u;
+  }
   for (int i = wk_tid(); i < rings * a.nstage; i += wk_threads()) mbar_init(a.mbar + i, 1);
   for (int i = wk_tid(); i < rings; i += wk_threads()) { a.pipe[i].issued = 0; a.pipe[i].consumed = 0; }
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -486,88 +491,137 @@ __device__ __noinline__ void logistic_cta_pass(const LogisticArgs& a, const doub
 
 // ---------------------------------------------------------------- wide p
 // p in (64, kWideMax]: a tile is kWideRows = 8 rows in the input's row-major
-// order followed by 16 bytes holding the 8 labels (+ 8 zero bytes), one TMA
-// bulk copy of 32p+16 bytes.  Each worker warp owns a ring of these tiles
-// (same periodic tile sequence and run-ahead producer as p <= 64).
+// order followed by 16 bytes holding the 8 labels (+ 8 zero bytes): one TMA
+// bulk copy of 32p+16 bytes.  kWideGroup = 4 consecutive tiles (32 rows)
+// form a group, the unit of work assignment and of exact accumulation: each
+// worker warp owns whole groups (periodic sequence, run-ahead producer as for
+// p <= 64) and streams their tiles through its own ring.
 //
-// Per tile, in two groups of 4 rows: lane l holds features l, l+32, ... of
-// each row in registers (conflict-free LDS from the row-major stage), forms
-// 4 partial dot products, and a reduce-scatter over the warp (6 shuffles for
-// 4 rows instead of 20) leaves each lane with the full sum of one row; that
-// lane evaluates the row's sigmoid / log1pexp, 4 shuffles broadcast the
-// residuals, and the gradient contributions go into per-lane feature
-// accumulators from the same registers.  No CTA synchronisation inside the
-// pass; X elements are read from shared memory (and, in the FP64 policy,
-// converted to double) exactly once.
+// Per tile, in two halves of 4 rows: lane l holds features l, l+32, ... of
+// each row in registers (conflict-free LDS from the row-major stage), forms 4
+// partial dot products, and a reduce-scatter over the warp (6 shuffles for 4
+// rows) leaves each lane with the full sum of one row; that lane evaluates
+// the row's sigmoid / log1pexp, 4 shuffles broadcast the residuals, and the
+// gradient contributions accumulate per lane from the same registers.  No
+// CTA synchronisation inside the pass; each X element is read from shared
+// memory (and in the FP64 policy converted to double) exactly once.
+//
+// Exactness: a group's partial sums (fp32 or fp64 in the policy's type) are
+// converted to fixed-point pairs (fx_split) and added as integers, so the
+// totals do not depend on which warp, CTA or GPU processed a group: row
+// shards aligned to groups reproduce the single-GPU totals bit for bit.
 constexpr int kWideMax = 256;
 constexpr int kWideRows = 8;
+constexpr int kWideGroup = 4;
+constexpr int kWideTotWords = 2 * (kWideMax + 2) + 2;  // CTA totals at the start of wred (16-B multiple)
+// wred doubles the wide pass needs: totals + lane-private accumulator slots
+__host__ __device__ inline int wide_scratch_doubles(int worker_warps) {
+  return kWideTotWords + worker_warps * (kWideMax / 32 + 2) * 32 * 2;
+}
 __host__ __device__ inline int64_t wide_tile_bytes(int p) { return 32 * (int64_t)p + 16; }
+// ring stage: the tile plus zeroed slack covering the pass's unconditional
+// reads (row 7, features up to 32*KL - 1), 128-byte multiple
+__host__ __device__ inline int wide_stage_bytes(int p) {
+  const int kl = p <= 128 ? 4 : 8;
+  int64_t b = wide_tile_bytes(p);
+  const int64_t reach = 4 * (int64_t)((kWideRows - 1) * p + 32 * kl);
+  if (reach > b) b = reach;
+  return (int)((b + 127) / 128 * 128);
+}
 
 struct WideProducer {
-  unsigned char* ring;
-  uint64_t* bars;
   const unsigned char* src;    // next tile to issue
   const unsigned char* first;  // this warp's first tile
-  int64_t step;                // bytes between this warp's tiles (nwarps tiles)
-  int64_t tj, count;
-  int s, nstage, stage_bytes;
-  uint32_t tb;
+  int64_t gstep;               // bytes from one of this warp's groups to the next
+  int64_t gj, count;           // group index within the warp's sequence, group count
+  int k;                       // tile within the group
+  int s, nstage;
+  uint32_t tb, ring, bars;     // tile bytes; shared addresses of the ring and its mbarriers
+  uint32_t stage_bytes;
   uint64_t pol;
 
   __device__ __forceinline__ void init(const LogisticArgs& a, const WarpTiles& wt, unsigned long long issued) {
     const int warp = wk_warp();
     nstage = a.nstage;
-    stage_bytes = a.stage_bytes;
-    ring = a.stages + (int64_t)warp * nstage * stage_bytes;
-    bars = a.mbar + warp * nstage;
+    stage_bytes = (uint32_t)a.stage_bytes;
+    ring = smem_u32(a.stages) + (uint32_t)(warp * nstage) * stage_bytes;
+    bars = smem_u32(a.mbar + warp * nstage);
     s = (int)(issued % (unsigned long long)nstage);
     count = wt.count;
-    tj = (int64_t)(issued % (unsigned long long)count);
+    const unsigned long long i = issued % (unsigned long long)(count * kWideGroup);
+    gj = (int64_t)(i / kWideGroup);
+    k = (int)(i % kWideGroup);
     tb = (uint32_t)wide_tile_bytes(a.p);
-    first = reinterpret_cast<const unsigned char*>(a.xt) + wt.first * (int64_t)tb;
-    step = (int64_t)wt.nwarps * tb;
-    src = first + tj * step;
+    first = reinterpret_cast<const unsigned char*>(a.xt) + wt.first * kWideGroup * (int64_t)tb;
+    gstep = (int64_t)wt.nwarps * kWideGroup * tb;
+    src = first + gj * gstep + (int64_t)k * tb;
     pol = policy_evict_first();
   }
   __device__ __forceinline__ void issue() {
-    uint64_t* bar = bars + s;
-    mbar_expect_tx(bar, tb);
-    bulk_g2s(ring + (int64_t)s * stage_bytes, src, tb, bar, pol);
+    const uint32_t bar = bars + 8u * (uint32_t)s;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(tb) : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            ring + (uint32_t)s * stage_bytes),
+        "l"(src), "r"(tb), "r"(bar), "l"(pol)
+        : "memory");
     if (++s == nstage) s = 0;
-    if (++tj == count) { tj = 0; src = first; }
-    else src += step;
+    if (++k == kWideGroup) {
+      k = 0;
+      if (++gj == count) { gj = 0; src = first; }
+      else src += gstep - (int64_t)(kWideGroup - 1) * tb;
+    } else {
+      src += tb;
+    }
   }
 };
 
 template <bool FP64, int KL>  // KL = features per lane (p <= 32 KL)
 __device__ __noinline__ void logistic_cta_pass_wide(const LogisticArgs& a, const double* __restrict__ theta_s,
-                                                       double* wred, double* red_out) {
+                                                    double* wred, double* red_out) {
   using acc_t = typename std::conditional<FP64, double, float>::type;
-  constexpr int R = 4;               // rows per group
-  const int lane = threadIdx.x & 31, warp = wk_warp(), nw = wk_nwarps();
+  extern __shared__ __align__(16) unsigned char ts_dyn_smem[];
+  constexpr int R = 4;  // rows per half tile
+  const int lane = threadIdx.x & 31, warp = wk_warp();
   const int p = a.p;
-  const WarpTiles wt = warp_tiles(a);
+  const int64_t n_rows = a.n_rows;
+  const int nstage = a.nstage;
+  const int stage_bytes = a.stage_bytes;
+  // work assignment in groups of kWideGroup tiles
+  WarpTiles wt;
+  {
+    const int nwarps = wk_nwarps();
+    const int64_t G = gridDim.x, ng = a.ntiles / kWideGroup;
+    const int64_t g_begin = (ng * (int64_t)blockIdx.x) / G, g_end = (ng * ((int64_t)blockIdx.x + 1)) / G;
+    wt.first = g_begin + warp;
+    wt.count = (g_end - wt.first + nwarps - 1) / nwarps;
+    if (wt.count < 0) wt.count = 0;
+    wt.nwarps = nwarps;
+  }
   const bool prof = a.prof != nullptr && blockIdx.x == 0 && wk_tid() == 0;
   long long pc0 = prof ? clock64() : 0, pc1;
 
+  bool fvalid[KL];
   acc_t th[KL];
 #pragma unroll
-  for (int m = 0; m < KL; ++m) th[m] = (lane + 32 * m < p) ? (acc_t)theta_s[lane + 32 * m] : (acc_t)0;
+  for (int m = 0; m < KL; ++m) {
+    fvalid[m] = lane + 32 * m < p;
+    th[m] = fvalid[m] ? (acc_t)theta_s[lane + 32 * m] : (acc_t)0;
+  }
   const acc_t thb = (acc_t)theta_s[p];
-  // Exact fixed-point accumulators (fx_split units): [0, KL) features
-  // lane + 32 m, KL residual sum, KL + 1 log-likelihood (lanes 0, 8, 16, 24).
-  // Each tile's partial sums are converted exactly, so the totals do not
-  // depend on which warp, CTA or GPU processed a tile (row sharding).
+  // exact fixed-point accumulators: [0, KL) features lane + 32 m, KL the
+  // residual sum, KL + 1 the log-likelihood (nonzero on lanes 0, 8, 16, 24)
+  // (lane-private slots in shared memory: [warp][NF][32 lanes] (hi, signed lo)
+  // pairs, touched once per group, so they cost no registers in the loop)
   constexpr int NF = KL + 2;
-  unsigned long long fh[NF], fl[NF];  // (hi, signed lo) sums, wrapping
-#pragma unroll
-  for (int m = 0; m < NF; ++m) { fh[m] = 0; fl[m] = 0; }
   bool bad = false;
-  int since_norm = 0;
   unsigned long long* tot = reinterpret_cast<unsigned long long*>(wred);  // CTA totals [2*(p+2)] + flag
+  ulonglong2* fx = reinterpret_cast<ulonglong2*>(wred + kWideTotWords) + (warp * NF) * 32 + lane;
+#pragma unroll
+  for (int m = 0; m < NF; ++m) fx[32 * m] = make_ulonglong2(0ULL, 0ULL);
   for (int i = wk_tid(); i < 2 * (p + 2) + 1; i += wk_threads()) tot[i] = 0ULL;
   wk_sync();
-  // after the reduce-scatter, lane holds row (bit 4, bit 3) of the group
+  // after the reduce-scatter, lane holds row (bit 4, bit 3) of a half tile
   const int my_r = ((lane >> 3) & 2) | ((lane >> 3) & 1);
   const bool up16 = (lane & 16) != 0, up8 = (lane & 8) != 0;
 
@@ -575,38 +629,44 @@ __device__ __noinline__ void logistic_cta_pass_wide(const LogisticArgs& a, const
     WarpPipe& pipe = a.pipe[warp];
     const unsigned long long c0 = pipe.consumed;
     unsigned long long issued = pipe.issued;
+    const int64_t ntile_w = wt.count * kWideGroup;  // tiles of this warp per pass
     WideProducer prod;
     if (lane == 0) {
       prod.init(a, wt, issued);
-      while (issued < c0 + (unsigned long long)a.nstage) { prod.issue(); ++issued; }
+      while (issued < c0 + (unsigned long long)nstage) { prod.issue(); ++issued; }
     }
-    int s = (int)(c0 % (unsigned long long)a.nstage);
-    uint32_t parity = (uint32_t)((c0 / a.nstage) & 1ULL);
-    int64_t tj = (int64_t)(c0 % (unsigned long long)wt.count);
-    const unsigned char* ring = a.stages + (int64_t)warp * a.nstage * a.stage_bytes;
-    uint64_t* bars = a.mbar + warp * a.nstage;
-    if (prof) { pc1 = clock64(); a.prof[4] += pc1 - pc0; pc0 = pc1; }
-    for (int64_t j = 0; j < wt.count; ++j) {
-      mbar_wait(bars + s, parity);
-      const unsigned char* sb = ring + (int64_t)s * a.stage_bytes;
-      const float* xs = reinterpret_cast<const float*>(sb);
-      const int64_t row0 = (wt.first + tj * wt.nwarps) * kWideRows;
-      acc_t tacc[KL];
+    int s = (int)(c0 % (unsigned long long)nstage);
+    uint32_t parity = (uint32_t)((c0 / nstage) & 1ULL);
+    const unsigned long long i0 = c0 % (unsigned long long)ntile_w;
+    int64_t gj = (int64_t)(i0 / kWideGroup);
+    int k = (int)(i0 % kWideGroup);
+    const uint32_t ring_off = (uint32_t)(a.stages - ts_dyn_smem) + (uint32_t)(warp * nstage * stage_bytes);
+    uint64_t* bars = a.mbar + warp * nstage;
+    // group-level partial sums in the policy's type (folded exactly per group)
+    acc_t gacc[NF];
 #pragma unroll
-      for (int m = 0; m < KL; ++m) tacc[m] = 0;
-      acc_t tb_sum = 0, tl_sum = 0;
+    for (int m = 0; m < NF; ++m) gacc[m] = 0;
+    if (prof) { pc1 = clock64(); a.prof[4] += pc1 - pc0; pc0 = pc1; }
+    for (int64_t j = 0; j < ntile_w; ++j) {
+      mbar_wait(bars + s, parity);
+      const unsigned char* sb = ts_dyn_smem + ring_off + (uint32_t)(s * stage_bytes);
+      const float* xs = reinterpret_cast<const float*>(sb);
+      const int64_t row0 = ((wt.first + gj * wt.nwarps) * kWideGroup + k) * kWideRows;
 #pragma unroll
       for (int g = 0; g < kWideRows; g += R) {
         acc_t xv[R][KL];
+        // unconditional loads: features past p read the next row / the
+        // label bytes / the stage's zeroed slack (finite values, see
+        // wide_stage_bytes); they meet theta = 0 in eta and their gradient
+        // slots are dropped at the fold
 #pragma unroll
-        for (int r = 0; r < R; ++r)
+        for (int r = 0; r < R; ++r) {
+          const float* xr = xs + (g + r) * p + lane;
 #pragma unroll
-          for (int m = 0; m < KL; ++m) {
-            const int f = lane + 32 * m;
-            xv[r][m] = (f < p) ? (acc_t)xs[(g + r) * p + f] : (acc_t)0;
-          }
+          for (int m = 0; m < KL; ++m) xv[r][m] = (acc_t)xr[32 * m];
+        }
         const int yr = g + my_r;
-        const uint8_t yb = sb[32 * p + yr];
+        const acc_t yv = (acc_t)sb[32 * p + yr];
         if (g + R == kWideRows) {
           // the stage is fully read: refill it (wrapping into the next pass)
           __syncwarp();
@@ -632,14 +692,13 @@ __device__ __noinline__ void logistic_cta_pass_wide(const LogisticArgs& a, const
         acc_t k0 = up16 ? e[2] : e[0], k1 = up16 ? e[3] : e[1];
         k0 += __shfl_xor_sync(0xffffffffu, up16 ? e[0] : e[2], 16);
         k1 += __shfl_xor_sync(0xffffffffu, up16 ? e[1] : e[3], 16);
-        acc_t k = up8 ? k1 : k0;
-        k += __shfl_xor_sync(0xffffffffu, up8 ? k0 : k1, 8);
-        k += __shfl_xor_sync(0xffffffffu, k, 4);
-        k += __shfl_xor_sync(0xffffffffu, k, 2);
-        k += __shfl_xor_sync(0xffffffffu, k, 1);
-        const acc_t eta = k + thb;
-        const bool valid = row0 + yr < a.n_rows;
-        const acc_t yv = (acc_t)yb;
+        acc_t kk = up8 ? k1 : k0;
+        kk += __shfl_xor_sync(0xffffffffu, up8 ? k0 : k1, 8);
+        kk += __shfl_xor_sync(0xffffffffu, kk, 4);
+        kk += __shfl_xor_sync(0xffffffffu, kk, 2);
+        kk += __shfl_xor_sync(0xffffffffu, kk, 1);
+        const acc_t eta = kk + thb;
+        const bool valid = row0 + yr < n_rows;
         acc_t resid, llt;
         if constexpr (FP64) {
           const double ex = exp(-fabs(eta));
@@ -648,42 +707,46 @@ __device__ __noinline__ void logistic_cta_pass_wide(const LogisticArgs& a, const
           resid = valid ? yv - sig : 0.0;
           llt = valid ? (yv * eta - l) : 0.0;
         } else {
-          const float ex = expf(-fabsf(eta));
-          const float l = fmaxf(eta, 0.f) + log1pf(ex);
-          const float sig = __fdiv_rn(eta >= 0.f ? 1.f : ex, 1.f + ex);
+          // branch-free fast intrinsics (FP32 policy tolerance)
+          const float ex = __expf(-fabsf(eta));
+          const float op = 1.f + ex;
+          const float l = fmaxf(eta, 0.f) + __logf(op);
+          const float sig = __fdividef(eta >= 0.f ? 1.f : ex, op);
           resid = valid ? yv - sig : 0.f;
           llt = valid ? __fmaf_rn(yv, eta, -l) : 0.f;
         }
-        if ((lane & 7) == 0) { tb_sum += resid; tl_sum += llt; }
+        if ((lane & 7) == 0) { gacc[KL] += resid; gacc[KL + 1] += llt; }
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           const acc_t rr = __shfl_sync(0xffffffffu, resid, ((r >> 1) << 4) | ((r & 1) << 3));
 #pragma unroll
           for (int m = 0; m < KL; ++m) {
-            if constexpr (FP64) tacc[m] = __fma_rn(rr, xv[r][m], tacc[m]);
-            else tacc[m] = __fmaf_rn(rr, xv[r][m], tacc[m]);
+            if constexpr (FP64) gacc[m] = __fma_rn(rr, xv[r][m], gacc[m]);
+            else gacc[m] = __fmaf_rn(rr, xv[r][m], gacc[m]);
           }
         }
       }
+      if (++s == nstage) { s = 0; parity ^= 1u; }
+      if (++k == kWideGroup) {  // group done: exact fold
+        k = 0;
+        if (++gj == wt.count) gj = 0;
 #pragma unroll
-      for (int m = 0; m < NF; ++m) {
-        const double v = (m < KL) ? (double)tacc[m < KL ? m : 0] : (double)(m == KL ? tb_sum : tl_sum);
-        long long h, l;
-        bad |= !fx_split(v, h, l);
-        fh[m] += (unsigned long long)h;
-        fl[m] += (unsigned long long)l;
+        for (int m = 0; m < NF; ++m) {
+          long long h, l;
+          const bool keep = m >= KL || fvalid[m < KL ? m : 0];
+          bad |= !fx_split(keep ? (double)gacc[m] : 0.0, h, l);
+          ulonglong2 v = fx[32 * m];
+          v.x += (unsigned long long)h;
+          v.y += (unsigned long long)l;
+          fx_canon(v.x, v.y);
+          fx[32 * m] = v;
+          gacc[m] = 0;
+        }
       }
-      if (++since_norm == 1024) {  // |lo| <= 2^50 per tile: carry before 2^61
-        since_norm = 0;
-#pragma unroll
-        for (int m = 0; m < NF; ++m) fx_canon(fh[m], fl[m]);
-      }
-      if (++s == a.nstage) { s = 0; parity ^= 1u; }
-      if (++tj == wt.count) tj = 0;
     }
     __syncwarp();
     if (lane == 0) {
-      pipe.consumed = c0 + (unsigned long long)wt.count;
+      pipe.consumed = c0 + (unsigned long long)ntile_w;
       pipe.issued = issued;
     }
     __syncwarp();
@@ -691,20 +754,19 @@ __device__ __noinline__ void logistic_cta_pass_wide(const LogisticArgs& a, const
   if (prof) { pc1 = clock64(); a.prof[5] += pc1 - pc0; pc0 = pc1; }
   // CTA totals: shared-memory integer atomics (order-free)
 #pragma unroll
-  for (int m = 0; m < NF; ++m) fx_canon(fh[m], fl[m]);
-#pragma unroll
   for (int m = 0; m < KL; ++m) {
-    const int f = lane + 32 * m;
-    if (f < p) {
-      atomicAdd(tot + 2 * f, fh[m]);
-      atomicAdd(tot + 2 * f + 1, fl[m]);
+    if (fvalid[m]) {
+      const ulonglong2 v = fx[32 * m];
+      atomicAdd(tot + 2 * (lane + 32 * m), v.x);
+      atomicAdd(tot + 2 * (lane + 32 * m) + 1, v.y);
     }
   }
   if ((lane & 7) == 0) {
-    atomicAdd(tot + 2 * p, fh[KL]);
-    atomicAdd(tot + 2 * p + 1, fl[KL]);
-    atomicAdd(tot + 2 * p + 2, fh[KL + 1]);
-    atomicAdd(tot + 2 * p + 3, fl[KL + 1]);
+    const ulonglong2 b = fx[32 * KL], l = fx[32 * (KL + 1)];
+    atomicAdd(tot + 2 * p, b.x);
+    atomicAdd(tot + 2 * p + 1, b.y);
+    atomicAdd(tot + 2 * p + 2, l.x);
+    atomicAdd(tot + 2 * p + 3, l.y);
   }
   if (bad) atomicOr(tot + 2 * (p + 2), 1ULL);
   if (prof) { pc1 = clock64(); a.prof[7] += pc1 - pc0; }

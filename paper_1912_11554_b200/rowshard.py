@@ -29,7 +29,7 @@ HANDLE_BYTES = 64
 MAX_PEERS = 8
 
 
-TILE_ROWS = 8  # rows per data tile of the wide (64 < p <= 256) pass
+TILE_ROWS = 32  # rows per exact-accumulation group of the wide (64 < p <= 256) pass
 
 
 def row_range(n_rows: int, rank: int, world: int, align: int = TILE_ROWS) -> Tuple[int, int]:

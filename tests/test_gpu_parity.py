@@ -469,7 +469,7 @@ def test_row_shards_compose_exactly(precision):
             parts = []
             for r in range(world):
                 a, b = t.rowshard.row_range(n, r, world)
-                assert a % 8 == 0
+                assert a % 32 == 0
                 m = t.logistic_regression_model(t.LogisticRegressionData(x[a:b], y[a:b]), precision=precision)
                 parts.append(t.rowshard.partial_sums(m.device_spec, q))
             comb = t.rowshard.combine(parts)

@@ -94,8 +94,8 @@ def test_row_range_whole_tiles():
             for (a0, b0), (a1, b1) in zip(rr, rr[1:]):
                 assert b0 == a1
             for a, b in rr:
-                assert a % 8 == 0 and a <= b
-            sizes = [-(-(b - a) // 8) for a, b in rr]
+                assert a % 32 == 0 and a <= b
+            sizes = [-(-(b - a) // 32) for a, b in rr]
             assert max(sizes) - min(sizes) <= 1
     with pytest.raises(ValueError):
         ts.rowshard.row_range(10, 2, 2)

@@ -54,7 +54,7 @@ def parse():
     ap.add_argument("--precision", choices=("fp64", "fp32"), default="fp32",
                     help="arithmetic of the fused data pass for the headline (the other mode is reported too)")
     ap.add_argument("--single-precision", action="store_true", help="measure only --precision")
-    ap.add_argument("--config", choices=("covtype", "eight_schools", "gauss10", "rowshard"), default="covtype")
+    ap.add_argument("--config", choices=("covtype", "eight_schools", "gauss10", "rowshard", "dense"), default="covtype")
     ap.add_argument("--chains", type=int, default=8192, help="eight_schools: total chains")
     ap.add_argument("--num-warmup", type=int, default=1000)
     ap.add_argument("--num-samples", type=int, default=1000)
@@ -350,10 +350,95 @@ def run_row_sharded(args):
     return 0
 
 
+def run_dense(args):
+    """1000-D correlated Gaussian (Sigma = Q diag(logspace(-2,2)) Q^T,
+    Q from the QR of an N(0,1) matrix, seed 4), dense mass M^-1 = Sigma, --chains chains
+    (default 1024), --num-warmup/--num-samples draws; chains sharded over ranks (weak: each
+    rank runs its shard in one lockstep launch).  One lockstep step = one tcgen05 TF32 GEMM
+    of 2*D*D*C flops for all chains' gradients.  Not the driver's headline line."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1912_11554_b200 as ts
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    D = 1000
+    C = args.chains if args.chains != 8192 else 1024
+    g = np.random.default_rng(4)
+    Q, _ = np.linalg.qr(g.standard_normal((D, D)))
+    lam = np.logspace(-2, 2, D)
+    Sigma = (Q * lam) @ Q.T
+    P = (Q / lam) @ Q.T
+    prec = "fp64" if args.precision == "fp64" else "tf32"
+    model = ts.dense_gaussian_model(P, inv_mass=Sigma, precision=prec)
+    keys = ts.chain_keys(4, C)
+    mine = [keys[c] for c in ts.chains.shard_range(C, rank, world)]
+    cfg = ts.RunConfig(model={"model": "dense_gaussian"}, num_chains=C, num_warmup=args.num_warmup,
+                       num_samples=args.num_samples, seed=4)
+    times, lfs, steps = [], [], []
+    clocks = ClockSampler(local)
+    last = None
+    for s in range(args.warmup + args.steps):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        if s == args.warmup:
+            clocks.__enter__()
+        r = ts.run_device(model, cfg, mine, dev)
+        if s >= args.warmup:
+            times.append(r.event_ms)
+            lfs.append(float(r.stats.cpu().numpy()[:, :, 1].sum()))
+            steps.append(float(r.evals.cpu().numpy().max()))
+            last = r
+    clocks.__exit__(None, None, None)
+    t = torch.tensor([sum(times), sum(lfs)], dtype=torch.float64, device=dev)
+    if world > 1:
+        tm = t[:1].clone()
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+        tl = t[1:].clone()
+        dist.all_reduce(tl, op=dist.ReduceOp.SUM)
+        t = torch.cat([tm, tl])
+    t_ms, lf = float(t[0]), float(t[1])
+    Cr = len(mine)
+    flops = 2.0 * D * D * (-(-Cr // 64) * 64) * sum(steps)
+    tflops = flops / (sum(times) / 1e3) / 1e12
+    peak = None
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            peak = 0.5 * float(json.load(fh)["bf16_tflops"])  # dense TF32 = half the bf16 rate
+    except Exception:
+        peak = 1125.0
+    if rank == 0:
+        samples = last.samples.cpu().numpy()
+        print(json.dumps({
+            "metric": "leapfrog_steps_per_sec", "value": lf / (t_ms / 1000.0), "unit": "chain-leapfrog/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": prec, "data": "synthetic",
+            "config": {"workload": f"1000-D correlated Gaussian, dense mass, {C} chains in lockstep, "
+                                   f"{args.num_warmup}+{args.num_samples} draws", "parallelism": f"chains{world}"},
+            "lockstep_steps_per_run": sum(steps) / args.steps, "us_per_lockstep_step": 1e3 * sum(times) / sum(steps),
+            "roofline": {"bound": "tensor", "achieved": tflops, "peak": peak, "unit": "TFLOP/s", "frac": tflops / peak,
+                         "traffic": None, "note": "GEMM flops only; the step is bound by the chains' vector work"},
+            "min_ess_rank0": float(np.nanmin(ts.ess(samples))), "gpu_launches": args.steps,
+            "clocks": clocks.summary(),
+        }), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.config == "dense":
+        return run_dense(args)
     if args.config in ("eight_schools", "gauss10"):
         return run_eight_schools(args)
     if args.config == "rowshard":

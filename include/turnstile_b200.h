@@ -36,10 +36,11 @@ enum { TS_OK = 0, TS_EINVAL = 1, TS_ECUDA = 2, TS_EUNSUPPORTED = 3 };
 /* Model kinds.  Reference constructors: models.py:67-144 (std_normal,
  * gaussian, logistic_regression, funnel); eight_schools is the SURVEY 8(d)
  * config-3 model (no reference built-in; oracle twin in oracle/). */
-enum { TS_STD_NORMAL = 0, TS_GAUSSIAN = 1, TS_LOGISTIC = 2, TS_FUNNEL = 3, TS_EIGHT_SCHOOLS = 4 };
+enum { TS_STD_NORMAL = 0, TS_GAUSSIAN = 1, TS_LOGISTIC = 2, TS_FUNNEL = 3, TS_EIGHT_SCHOOLS = 4, TS_DENSE_GAUSS = 5 };
 
-/* Arithmetic policy of the logistic data pass (ts_logistic.cuh). */
-enum { TS_PREC_FP64 = 0, TS_PREC_FP32 = 1 };
+/* Arithmetic policy of the logistic data pass (ts_logistic.cuh) and of the
+ * dense-Gaussian GEMM (FP64: SIMT fp64; FP32/TF32: tcgen05 TF32 tensor cores). */
+enum { TS_PREC_FP64 = 0, TS_PREC_FP32 = 1, TS_PREC_TF32 = 2 };
 
 /* U-turn criterion (tree.py:36-37). */
 enum { TS_GENERALIZED = 0, TS_CLASSIC = 1 };
@@ -72,7 +73,9 @@ int ts_abi_version(void);
 
 /* Replaces models.py:67-144 + LogisticRegressionData (models.py:43-64): builds
  * a device model.  params (host): gaussian inv_var[dim]; eight_schools
- * y[J], sigma[J] (dim = J + 2).  Logistic: x_dev row-major fp32 (n_rows x
+ * y[J], sigma[J] (dim = J + 2); dense_gauss A[dim][dim] (U = x'Ax/2, the
+ * SURVEY 8(d) config-4 target after the dense-mass reparametrisation x =
+ * L^-1 q; dim % 4 == 0 for TF32).  Logistic: x_dev row-major fp32 (n_rows x
  * n_feat), y_dev uint8 in {0,1}; the library re-tiles X into its own HBM
  * layout. */
 int ts_model_create(int kind, int dim, const double* params, int n_params, const float* x_dev, const uint8_t* y_dev,
@@ -163,6 +166,12 @@ int ts_peer_mailbox_connect(ts_model* m, const void* ipc_handles);
  * feature sums, the residual sum and the log-likelihood sum, then the
  * out-of-range flag.  value = hi * 2^-10 + lo * 2^-63 (two's complement). */
 int ts_logistic_partial_sums(const ts_model* m, const double* q_dev, uint64_t* words_dev, void* stream);
+
+/* Test probe of the tcgen05 TF32 GEMM (csrc/ts_umma.cuh) behind the
+ * dense-Gaussian model: gt[n][m] = sum_k a[m][k] * xt[n][k] with a (M x K)
+ * and xt (N x K) row-major fp32 (K % 4 == 0), gt (N x M).  grid <= 0: one
+ * CTA per 128 x 64 tile.  Replaces nothing in the reference. */
+int ts_gemm_tf32_probe(const float* a_dev, const float* xt_dev, float* gt_dev, int M, int N, int K, int grid, void* stream);
 
 /* Parity probe of the device randomness (csrc/ts_rng.cuh): kind 0 writes n
  * Generator.random() doubles of RngKey(key).generator(), kind 1 n

@@ -188,6 +188,7 @@ class Model:
     es_y: list = None
     es_s: list = None
     fused_omp: bool = False  # logistic: one OpenMP pass computes U and gradient (CPU baseline)
+    dense_a: list = None  # dense_gaussian: A as a list of rows (U = x'Ax/2)
     _clib: object = field(default=None, repr=False)
     _cache: tuple = field(default=None, repr=False)
     threads: int = 0
@@ -230,6 +231,8 @@ class Model:
             return v * v / 18.0 + 0.5 * (len(q) - 1) * v + 0.5 * math.exp(-v) * ssq
         if k == "eight_schools":
             return eight_schools_potential(q, self.es_y, self.es_s)
+        if k == "dense_gaussian":
+            return dense_potential(q, self.dense_a)
         if k == "logistic_regression":
             th = np.ascontiguousarray(q, dtype=np.float64)
             lib = self.clib()
@@ -257,6 +260,8 @@ class Model:
             return out
         if k == "eight_schools":
             return eight_schools_gradient(q, self.es_y, self.es_s)
+        if k == "dense_gaussian":
+            return dense_gradient(q, self.dense_a)
         if k == "logistic_regression":
             th = np.ascontiguousarray(q, dtype=np.float64)
             out = np.empty(self.dim)
@@ -269,6 +274,33 @@ class Model:
         if self._clib is None:
             self._clib = _lib()
         return self._clib
+
+
+def dense_gradient(x, a):
+    """Dense Gaussian (no reference built-in): g = A x,
+    each row summed k = 0.. in order, multiply then add -- the device's SIMT
+    fp64 GEMM policy (csrc/ts_k_dense.cu dense_tile_fp64)."""
+    out = []
+    for row in a:
+        acc = 0.0
+        for av, xv in zip(row, x):
+            acc = acc + av * xv
+        out.append(acc)
+    return out
+
+
+def dense_potential(x, a):
+    """U = x.g / 2 with the device's order: lane-strided partial sums over 32
+    lanes, then the warp shuffle-down tree (csrc/ts_k_dense.cu DenseW::wait)."""
+    g = dense_gradient(x, a)
+    part = [0.0] * 32
+    for d in range(len(x)):
+        part[d % 32] = part[d % 32] + x[d] * g[d]
+    o = 16
+    while o >= 1:
+        part = [part[l] + part[l + o] if l + o < 32 else part[l] for l in range(32)]
+        o //= 2
+    return 0.5 * part[0]
 
 
 def eight_schools_potential(q, y, s):

@@ -18,8 +18,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libturnstile_b200.so")
 
 TS_OK, TS_EINVAL, TS_ECUDA, TS_EUNSUPPORTED = 0, 1, 2, 3
-TS_STD_NORMAL, TS_GAUSSIAN, TS_LOGISTIC, TS_FUNNEL, TS_EIGHT_SCHOOLS = 0, 1, 2, 3, 4
-TS_PREC_FP64, TS_PREC_FP32 = 0, 1
+TS_STD_NORMAL, TS_GAUSSIAN, TS_LOGISTIC, TS_FUNNEL, TS_EIGHT_SCHOOLS, TS_DENSE_GAUSS = 0, 1, 2, 3, 4, 5
+TS_PREC_FP64, TS_PREC_FP32, TS_PREC_TF32 = 0, 1, 2
 TS_GENERALIZED, TS_CLASSIC = 0, 1
 TS_EXEC_THREAD, TS_EXEC_BLOCK = 0, 1
 ABI_VERSION = 1
@@ -43,6 +43,7 @@ EXPORTS = (
     "ts_peer_mailbox_create",
     "ts_peer_mailbox_connect",
     "ts_logistic_partial_sums",
+    "ts_gemm_tf32_probe",
 )
 
 
@@ -96,6 +97,7 @@ def _declare(lib):
     lib.ts_peer_mailbox_create.argtypes = [_P, _I, _I, _P]
     lib.ts_peer_mailbox_connect.argtypes = [_P, _P]
     lib.ts_logistic_partial_sums.argtypes = [_P, _P, _P, _P]
+    lib.ts_gemm_tf32_probe.argtypes = [_P, _P, _P, _I, _I, _I, _I, _P]
     for name in EXPORTS:
         if name not in ("ts_last_error",):
             getattr(lib, name).restype = _I

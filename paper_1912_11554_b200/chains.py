@@ -140,7 +140,11 @@ def run_device(model: TargetModel, config: RunConfig, keys: Sequence[RngKey], de
         kd = torch.tensor(np.array([[k.hi, k.lo] for k in keys], dtype=np.uint64).view(np.int64), device=dev)
         inv0 = torch.from_numpy(base.mass.inv_diag).to(dev)
         if W > 0:
-            sched = torch.from_numpy(warmup_schedule(W).device_flags()).to(dev)
+            flags = warmup_schedule(W).device_flags()
+            if spec.reparam is not None:
+                # a fixed dense mass (dense_gaussian_model): warmup adapts the step size only
+                flags = np.zeros_like(flags)
+            sched = torch.from_numpy(flags).to(dev)
             weights = torch.from_numpy(da_weights(W)).to(dev)
         else:
             sched = weights = None
@@ -159,6 +163,9 @@ def run_device(model: TargetModel, config: RunConfig, keys: Sequence[RngKey], de
                                      _lib.ptr(samples), _lib.ptr(stats), _lib.ptr(adapt), _lib.ptr(status), _lib.ptr(evals),
                                      exec_mode_for(model, exec_mode), _lib.stream_ptr(torch)))
         t1.record()
+        if spec.reparam is not None:  # x -> q = L x (dense mass reparametrisation)
+            Lt = torch.from_numpy(np.ascontiguousarray(spec.reparam.T)).to(dev)
+            samples = torch.matmul(samples, Lt)
         ms = None
         if sync:
             t1.synchronize()

@@ -110,6 +110,7 @@ static int launch(const ts_model* m, int nslots, OpArgs& A, int n_threads_chains
     if (!m->pmax) return set_err(TS_EUNSUPPORTED, "logistic feature count > 256 not supported on this path");
     return launch_block_logistic(m, nslots, A, st);
   }
+  if (m->kind == TS_DENSE_GAUSS) return launch_dense(m, nslots, A, n_threads_chains, st);
   SmallModel sm;
   sm.kind = m->kind;
   sm.dim = m->dim;
@@ -148,6 +149,27 @@ extern "C" int ts_model_create(int kind, int dim, const double* params, int n_pa
     case TS_FUNNEL:
       if (dim < 2) return fail(TS_EINVAL, "funnel needs the scale coordinate plus at least one other");
       break;
+    case TS_DENSE_GAUSS: {
+      if (n_params != dim * dim || !params) return fail(TS_EINVAL, "dense_gauss needs A[dim][dim]");
+      m->fp64 = precision == TS_PREC_FP64;
+      if (!m->fp64 && dim % 4 != 0) return fail(TS_EUNSUPPORTED, "dense_gauss TF32 path needs dim % 4 == 0");
+      // tf32-rounded copy of A for the tensor-core path (round to nearest, ties away)
+      float* h = (float*)malloc((size_t)dim * dim * sizeof(float));
+      if (!h) return fail(TS_ECUDA, "host allocation failed");
+      for (int64_t i = 0; i < (int64_t)dim * dim; ++i) {
+        float f = (float)params[i];
+        uint32_t b;
+        memcpy(&b, &f, 4);
+        if ((b & 0x7f800000u) != 0x7f800000u) b = (b + 0x1000u) & 0xffffe000u;
+        memcpy(&f, &b, 4);
+        h[i] = f;
+      }
+      cudaError_t e = cudaMalloc((void**)&m->a32, (size_t)dim * dim * sizeof(float));
+      if (e == cudaSuccess) e = cudaMemcpy(m->a32, h, (size_t)dim * dim * sizeof(float), cudaMemcpyHostToDevice);
+      free(h);
+      if (e != cudaSuccess) return fail(TS_ECUDA, "dense_gauss upload failed");
+      break;
+    }
     case TS_EIGHT_SCHOOLS:
       if (dim < 3 || n_params != 2 * (dim - 2) || !params) return fail(TS_EINVAL, "eight_schools needs y[J], sigma[J] with dim = J + 2");
       break;
@@ -207,6 +229,8 @@ extern "C" int ts_model_destroy(ts_model* m) {
   if (m->pbuf) cudaFree(m->pbuf);
   if (m->bar) cudaFree(m->bar);
   if (m->slotws) cudaFree(m->slotws);
+  if (m->a32) cudaFree(m->a32);
+  if (m->dws) cudaFree(m->dws);
   for (int r = 0; r < m->world; ++r)
     if (m->mail[r] && m->mail[r] != m->mail_local) cudaIpcCloseMemHandle(m->mail[r]);
   if (m->mail_local) cudaFree(m->mail_local);

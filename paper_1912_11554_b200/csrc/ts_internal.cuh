@@ -39,6 +39,10 @@ struct ts_model {
   unsigned long long* mail_local;  // this rank's mailbox (+ exchange counter after it)
   unsigned long long* mail[TS_MAX_PEERS];
   unsigned long long* dump;        // transient: ts_logistic_partial_sums output
+  // dense Gaussian (TS_DENSE_GAUSS): params = A (dim x dim, fp64), a32 = tf32-rounded copy
+  float* a32;
+  unsigned char* dws;  // lockstep workspaces (grown on demand)
+  size_t dws_size;
 };
 
 namespace ts_internal {
@@ -306,6 +310,7 @@ __global__ void __launch_bounds__(256, 1) k_block_op(MW mw, int D, int nslots, i
 int launch_thread(const SmallModel& sm, int D, int C, int nslots, OpArgs& A, cudaStream_t st);
 int launch_block_small(const SmallModel& sm, int D, int nslots, OpArgs& A, cudaStream_t st);
 int launch_block_logistic(const ts_model* m, int nslots, OpArgs& A, cudaStream_t st);
+int launch_dense(const ts_model* m, int nslots, OpArgs& A, int n_chains, cudaStream_t st);
 
 }  // namespace ts_internal
 

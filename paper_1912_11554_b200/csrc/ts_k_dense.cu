@@ -1,0 +1,369 @@
+// Many-chain dense-Gaussian model and its tcgen05
+// TF32 GEMM.  This translation unit holds the tensor-map plumbing, the GEMM
+// probe (ts_gemm_tf32_probe, used by the parity tests) and the persistent
+// lockstep kernel (k_dense_op, see ts_dense.cuh).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include "ts_internal.cuh"
+#include "ts_umma.cuh"
+
+namespace ts_internal {
+
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// Row-major fp32 matrix rows x cols (cols % 4 == 0) as a 2-D tensor map with
+// boxes of box_rows x kUmmaBK and the 128-byte swizzle (K-major UMMA layout);
+// out-of-range boxes read zeros.
+int make_tmap_f32(CUtensorMap* map, const float* base, int64_t rows, int64_t cols, int box_rows) {
+  auto enc = get_encode();
+  if (!enc) return set_err(TS_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  if (cols % 4 != 0) return set_err(TS_EINVAL, "tensor map: row length must be a multiple of 4 floats");
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 4};
+  cuuint32_t box[2] = {(cuuint32_t)kUmmaBK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_err(TS_ECUDA, "cuTensorMapEncodeTiled failed");
+  return TS_OK;
+}
+
+// GEMM probe: GT[n][m] = sum_k A[m][k] XT[n][k], one CTA (4 warps) per tile.
+__global__ void __launch_bounds__(128, 1)
+    k_umma_probe(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, float* GT, int M,
+                 int N, int K) {
+  extern __shared__ __align__(1024) unsigned char dsm[];
+  UmmaGemm g;
+  g.init(dsm);
+  if (threadIdx.x == 0) { u_prefetch_tmap(&tmA); u_prefetch_tmap(&tmB); }
+  const int mt = (M + kUmmaBM - 1) / kUmmaBM, nt = (N + kUmmaBN - 1) / kUmmaBN;
+  const int nkb = (K + kUmmaBK - 1) / kUmmaBK;
+  for (int tile = blockIdx.x; tile < mt * nt; tile += gridDim.x) {
+    const int m0 = (tile % mt) * kUmmaBM, n0 = (tile / mt) * kUmmaBN;
+    g.tile(&tmA, &tmB, m0, n0, nkb, GT, M, M - m0 < kUmmaBM ? M - m0 : kUmmaBM, N - n0 < kUmmaBN ? N - n0 : kUmmaBN);
+  }
+  g.release();
+}
+
+// ------------------------------------------------------------------ lockstep model
+// Dense Gaussian U(x) = 1/2 x^T A x, gradient A x, for C chains at once.
+// CTA = 4 GEMM warps (warps 0..3) + kDenseCW chain warps; each chain warp
+// runs one chain (Engine<WarpTeam>, vectors in a global workspace).  A model
+// evaluation is a lockstep step of the whole grid: every chain warp posts
+// its position (named barrier 2), the GEMM warps of all CTAs meet at a grid
+// barrier, compute their tiles of GT = X A^T (tcgen05 TF32, or SIMT fp64 in
+// the parity policy), meet again, and release the chain warps (barrier 3),
+// which read their gradient row and form U = 1/2 x.g.  Chains that finished
+// their run keep posting idle steps until every chain is done.
+constexpr int kDenseCW = 8;  // chain warps per CTA
+
+struct DenseW {
+  static constexpr bool kAsync = true;
+  int D;
+  int fp64;
+  float* xt;        // [Cpad][D] tf32-rounded positions (TF32 policy)
+  double* xt64;     // [Cpad][D] positions (FP64 policy)
+  const float* gt;  // [Cpad][D] gradients
+  const double* gt64;
+  int chain;
+  volatile int* cmd;  // smem: 1 = step done, 0 = exit
+  VecStore S;
+  int pq, pg;
+
+  __device__ void post(int q, int g) {
+    pq = q;
+    pg = g;
+    const int lane = threadIdx.x & 31;
+    const double* qv = S.v(q);
+    if (fp64) {
+      double* row = xt64 + (int64_t)chain * D;
+      for (int d = lane; d < D; d += 32) row[d] = qv[d];
+    } else {
+      float* row = xt + (int64_t)chain * D;
+      for (int d = lane; d < D; d += 32) {
+        uint32_t v;
+        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(v) : "f"((float)qv[d]));
+        row[d] = __uint_as_float(v);
+      }
+    }
+    // the GEMM reads the row through the async (TMA) proxy in another CTA
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    __threadfence();
+    __syncwarp();
+    cta_arrive(2);
+  }
+  __device__ double wait() {
+    cta_bar(3);
+    const int lane = threadIdx.x & 31;
+    const double* qv = S.v(pq);
+    double* gv = S.v(pg);
+    double acc = 0.0;
+    if (fp64) {
+      const double* row = gt64 + (int64_t)chain * D;
+      for (int d = lane; d < D; d += 32) {
+        const double g = __ldcg(row + d);
+        gv[d] = g;
+        acc = __dadd_rn(acc, __dmul_rn(qv[d], g));
+      }
+    } else {
+      const float* row = gt + (int64_t)chain * D;
+      for (int d = lane; d < D; d += 32) {
+        const double g = (double)__ldcg(row + d);
+        gv[d] = g;
+        acc = __dadd_rn(acc, __dmul_rn(qv[d], g));
+      }
+    }
+    __syncwarp();
+    return 0.5 * WarpTeam().sum(acc);
+  }
+  template <class Team>
+  __device__ double eval(const Team&, const VecStore&, int q, int g) {
+    post(q, g);
+    return wait();
+  }
+  // finished chains: take part in the step without a position; true = exit
+  __device__ bool idle_step() {
+    __syncwarp();
+    cta_arrive(2);
+    cta_bar(3);
+    return *cmd == 0;
+  }
+};
+
+struct DenseArgs {
+  int D, C, Cpad, fp64, nv;
+  float* xt;
+  double* xt64;
+  float* gt;
+  double* gt64;
+  const double* a64;        // [D][D] (FP64 policy)
+  double* ws;               // chain workspaces [C][nv][D]
+  unsigned long long* bar;  // grid barrier counter (zeroed before launch)
+  int* done;                // finished chain warps (zeroed before launch)
+  unsigned long long* prof;  // optional (TS_PROF): CTA-0 ns [wait for posts, GEMM, release], steps
+};
+
+__device__ __forceinline__ void gemm_grid_barrier(unsigned long long* bar, unsigned long long& epoch) {
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned long long target = (epoch + 1) * (unsigned long long)gridDim.x;
+    red_release_add_u64(bar, 1ULL);
+    while (ld_relaxed_u64(bar) < target) {
+    }
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  }
+  epoch += 1;
+  asm volatile("bar.sync 4, 128;" ::: "memory");
+}
+
+// SIMT fp64 tile (parity policy): thread = row m, 16 chains at a time, k in
+// order, multiply then add (oracle/turnstile_oracle.py restates it bit for bit)
+__device__ void dense_tile_fp64(const DenseArgs& a, int m0, int n0) {
+  const int m = m0 + (int)threadIdx.x;
+  if (m >= a.D) return;
+  const double* arow = a.a64 + (int64_t)m * a.D;
+  for (int nb = 0; nb < kUmmaBN; nb += 16) {
+    double acc[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) acc[j] = 0.0;
+    const int nmax = (a.Cpad - (n0 + nb)) < 16 ? (a.Cpad - (n0 + nb)) : 16;
+    if (nmax <= 0) break;
+    for (int k = 0; k < a.D; ++k) {
+      const double av = arow[k];
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (j < nmax) acc[j] = __dadd_rn(acc[j], __dmul_rn(av, __ldcg(a.xt64 + (int64_t)(n0 + nb + j) * a.D + k)));
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (j < nmax) a.gt64[(int64_t)(n0 + nb + j) * a.D + m] = acc[j];
+  }
+}
+
+__global__ void __launch_bounds__(128 + 32 * kDenseCW, 1)
+    k_dense_op(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmX, DenseArgs a,
+               int nslots, OpArgs A) {
+  extern __shared__ __align__(1024) unsigned char dsm[];
+  volatile int* cmd = reinterpret_cast<volatile int*>(dsm + kUmmaSmemBytes);
+  SlotScalars* ss_all = reinterpret_cast<SlotScalars*>(dsm + kUmmaSmemBytes + 64);
+  const int warp = threadIdx.x >> 5;
+  if (warp < 4) {
+    // ---------------- GEMM warps
+    UmmaGemm g;
+    if (!a.fp64) {
+      g.init(dsm);
+      if (threadIdx.x == 0) { u_prefetch_tmap(&tmA); u_prefetch_tmap(&tmX); }
+    }
+    const int mt = (a.D + kUmmaBM - 1) / kUmmaBM, nt = a.Cpad / kUmmaBN;
+    const int nkb = (a.D + kUmmaBK - 1) / kUmmaBK;
+    const int total = (int)gridDim.x * kDenseCW;
+    unsigned long long epoch = 0;
+    const bool prof = a.prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
+    unsigned long long tp0 = 0, tp1 = 0;
+    if (prof) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tp0));
+    for (;;) {
+      cta_bar(2);  // every chain warp of this CTA has posted
+      gemm_grid_barrier(a.bar, epoch);  // ... and of every CTA
+      if (prof) {
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tp1));
+        a.prof[0] += tp1 - tp0;
+        tp0 = tp1;
+      }
+      if (threadIdx.x == 0) *cmd = (*reinterpret_cast<volatile int*>(a.done) >= total) ? 0 : 1;
+      asm volatile("bar.sync 4, 128;" ::: "memory");
+      if (*cmd == 0) { cta_arrive(3); break; }
+      if (threadIdx.x == 0) asm volatile("fence.proxy.async.global;" ::: "memory");
+      for (int t = blockIdx.x; t < mt * nt; t += gridDim.x) {
+        const int m0 = (t % mt) * kUmmaBM, n0 = (t / mt) * kUmmaBN;
+        if (a.fp64) dense_tile_fp64(a, m0, n0);
+        else g.tile(&tmA, &tmX, m0, n0, nkb, a.gt, a.D, a.D - m0 < kUmmaBM ? a.D - m0 : kUmmaBM, kUmmaBN);
+      }
+      if (prof) {
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tp1));
+        a.prof[1] += tp1 - tp0;
+        tp0 = tp1;
+      }
+      gemm_grid_barrier(a.bar, epoch);  // all gradient tiles written
+      if (prof) {
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tp1));
+        a.prof[2] += tp1 - tp0;
+        a.prof[3] += 1;
+        tp0 = tp1;
+      }
+      cta_arrive(3);
+    }
+    if (!a.fp64) g.release();
+    return;
+  }
+  // ---------------- chain warps
+  const int cw = warp - 4;
+  const int chain = blockIdx.x * kDenseCW + cw;
+  DenseW M;
+  M.D = a.D;
+  M.fp64 = a.fp64;
+  M.xt = a.xt; M.xt64 = a.xt64; M.gt = a.gt; M.gt64 = a.gt64;
+  M.chain = chain;
+  M.cmd = cmd;
+  const int n_active = (A.op == OP_RUN) ? a.C : 1;
+  if (chain < n_active) {
+    Engine<WarpTeam, DenseW> E;
+    E.D = a.D;
+    E.S.base = a.ws + (int64_t)chain * a.nv * a.D;
+    E.S.vstride = a.D;
+    E.S.dstride = 1;
+    M.S = E.S;
+    E.M = M;
+    E.prof = nullptr;
+    E.prof_last = 0;
+    E.tr = nullptr;
+    E.ss = ss_all + cw * kMaxSlots;
+    __syncwarp();
+    do_op(E, A, A.op == OP_RUN ? chain : 0, chain == 0 || A.op == OP_RUN);
+  }
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) atomicAdd(a.done, 1);
+  __threadfence();
+  while (!M.idle_step()) {
+  }
+}
+
+int launch_dense(const ts_model* m, int nslots, OpArgs& A, int n_chains, cudaStream_t st) {
+  ts_model* mm = const_cast<ts_model*>(m);
+  const int D = m->dim;
+  const int C = (A.op == OP_RUN) ? n_chains : 1;
+  const int grid = (C + kDenseCW - 1) / kDenseCW;
+  const int Cpad = ((grid * kDenseCW + kUmmaBN - 1) / kUmmaBN) * kUmmaBN;
+  const int nv = num_vecs(nslots);
+  int dev = 0, nsm = 0;
+  TS_CUDA(cudaGetDevice(&dev));
+  TS_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  const size_t smem = kUmmaSmemBytes + 64 + kDenseCW * kMaxSlots * sizeof(SlotScalars);
+  auto kern = k_dense_op;
+  TS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int occ = 0;
+  TS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 128 + 32 * kDenseCW, smem));
+  if ((int64_t)occ * nsm < grid) return set_err(TS_EUNSUPPORTED, "dense model: too many chains for one co-resident grid");
+  // workspaces (grown on demand, owned by the model)
+  const size_t need = (size_t)Cpad * D * (m->fp64 ? 16 : 8) + (size_t)C * nv * D * 8 + 64;
+  if (mm->dws_size < need) {
+    if (mm->dws) cudaFree(mm->dws);
+    mm->dws = nullptr;
+    mm->dws_size = 0;
+    TS_CUDA(cudaMalloc((void**)&mm->dws, need));
+    mm->dws_size = need;
+    TS_CUDA(cudaMemset(mm->dws, 0, need));
+  }
+  DenseArgs a;
+  memset(&a, 0, sizeof a);
+  a.D = D; a.C = C; a.Cpad = Cpad; a.fp64 = m->fp64; a.nv = nv;
+  unsigned char* p = mm->dws;
+  a.bar = reinterpret_cast<unsigned long long*>(p);
+  a.done = reinterpret_cast<int*>(p + 8);
+  p += 64;
+  if (m->fp64) {
+    a.xt64 = reinterpret_cast<double*>(p); p += (size_t)Cpad * D * 8;
+    a.gt64 = reinterpret_cast<double*>(p); p += (size_t)Cpad * D * 8;
+  } else {
+    a.xt = reinterpret_cast<float*>(p); p += (size_t)Cpad * D * 4;
+    a.gt = reinterpret_cast<float*>(p); p += (size_t)Cpad * D * 4;
+  }
+  a.ws = reinterpret_cast<double*>(p);
+  a.a64 = m->params;
+  CUtensorMap ta, tx;
+  memset(&ta, 0, sizeof ta);
+  memset(&tx, 0, sizeof tx);
+  if (!m->fp64) {
+    int rc = make_tmap_f32(&ta, m->a32, D, D, kUmmaBM);
+    if (rc) return rc;
+    rc = make_tmap_f32(&tx, a.xt, Cpad, D, kUmmaBN);
+    if (rc) return rc;
+  }
+  TS_CUDA(cudaMemsetAsync(mm->dws, 0, 64, st));
+  const bool prof = getenv("TS_PROF") != nullptr;  // profiling aid: CTA-0 step phases to stderr
+  if (prof) a.prof = reinterpret_cast<unsigned long long*>(mm->dws + 16);
+  int ns = nslots;
+  void* args[] = {&ta, &tx, &a, &ns, &A};
+  TS_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3((unsigned)grid), dim3(128 + 32 * kDenseCW), args, smem, st));
+  if (prof) {
+    unsigned long long h[4];
+    TS_CUDA(cudaMemcpyAsync(h, a.prof, sizeof h, cudaMemcpyDeviceToHost, st));
+    TS_CUDA(cudaStreamSynchronize(st));
+    const double n = h[3] ? (double)h[3] : 1.0;
+    fprintf(stderr, "TS_PROF dense steps=%llu us/step: chains (post wait) %.2f  GEMM %.2f  release barrier %.2f\n", h[3],
+            h[0] / n / 1e3, h[1] / n / 1e3, h[2] / n / 1e3);
+  }
+  return TS_OK;
+}
+
+}  // namespace ts_internal
+
+using namespace ts_internal;
+
+extern "C" int ts_gemm_tf32_probe(const float* a_dev, const float* xt_dev, float* gt_dev, int M, int N, int K, int grid,
+                                  void* stream) {
+  if (!a_dev || !xt_dev || !gt_dev || M < 1 || N < 1 || K < 1) return set_err(TS_EINVAL, "bad GEMM probe arguments");
+  CUtensorMap ta, tb;
+  int rc = make_tmap_f32(&ta, a_dev, M, K, kUmmaBM);
+  if (rc) return rc;
+  rc = make_tmap_f32(&tb, xt_dev, N, K, kUmmaBN);
+  if (rc) return rc;
+  const int tiles = ((M + kUmmaBM - 1) / kUmmaBM) * ((N + kUmmaBN - 1) / kUmmaBN);
+  if (grid <= 0 || grid > tiles) grid = tiles;
+  TS_CUDA(cudaFuncSetAttribute(k_umma_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, kUmmaSmemBytes));
+  k_umma_probe<<<grid, 128, kUmmaSmemBytes, (cudaStream_t)stream>>>(ta, tb, gt_dev, M, N, K);
+  TS_CUDA(cudaGetLastError());
+  return TS_OK;
+}

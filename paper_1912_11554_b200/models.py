@@ -25,7 +25,7 @@ import numpy as np
 
 from . import _lib
 
-PRECISIONS = ("fp64", "fp32")
+PRECISIONS = ("fp64", "fp32", "tf32")
 
 
 class DeviceSpec:
@@ -43,6 +43,7 @@ class DeviceSpec:
         self._handles: dict = {}
         self._grid = 0
         self.row_shard = None  # (rank, world) once joined by rowshard.connect
+        self.reparam = None  # dense_gaussian with a dense mass: L (q = L x)
 
     def handle(self, device=None):
         """ts_model* for the given CUDA device (created on first use)."""
@@ -64,7 +65,7 @@ class DeviceSpec:
             params = self.params
             pp = params.ctypes.data if params is not None else 0
             npar = 0 if params is None else params.size
-            prec = _lib.TS_PREC_FP64 if self.precision == "fp64" else _lib.TS_PREC_FP32
+            prec = {"fp64": _lib.TS_PREC_FP64, "fp32": _lib.TS_PREC_FP32, "tf32": _lib.TS_PREC_TF32}[self.precision]
             _lib.check(lib.ts_model_create(self.kind, self.dim, pp, npar, _lib.ptr(xd), _lib.ptr(yd), n_rows, n_feat, prec,
                                            ctypes_byref(out)))
             if self._grid:
@@ -242,6 +243,57 @@ def eight_schools_model(y=EIGHT_SCHOOLS_Y, sigma=EIGHT_SCHOOLS_SIGMA) -> TargetM
     return _device_model("eight_schools", spec, {"y": y.tolist(), "sigma": s.tolist()})
 
 
+def dense_gaussian_model(precision_matrix, inv_mass=None, precision: str = "tf32") -> TargetModel:
+    """Correlated Gaussian U(q) = q'Pq/2 on the many-chain lockstep path
+    (no reference built-in, oracle twin in oracle/).
+
+    Every leapfrog of every chain needs g = P q: the device batches all
+    chains into one GEMM per lockstep step on the tcgen05 tensor cores
+    (``precision="tf32"``, stated tolerance) or on the SIMT fp64 pipe
+    (``"fp64"``, the parity policy).
+
+    ``inv_mass`` (optional, dense SPD M^-1): NUTS with mass matrix M on U is
+    run as identity-mass NUTS on x = L^-1 q, M^-1 = L L^T -- the same kinetic
+    energy (r'M^-1 r = r_x'r_x), U-turn criterion and leapfrog map -- so the
+    device model is U(x) = x'Ax/2 with A = L^T P L, and samples come back as
+    q = L x.  The reference itself is diagonal-mass only (integrator.py:21-31).
+    """
+    P = np.asarray(precision_matrix, dtype=np.float64)
+    if P.ndim != 2 or P.shape[0] != P.shape[1] or P.shape[0] < 1:
+        raise ValueError("precision_matrix must be a non-empty square matrix")
+    if not np.isfinite(P).all():
+        raise ValueError("precision_matrix must be finite")
+    D = P.shape[0]
+    L = None
+    if inv_mass is not None:
+        Minv = np.asarray(inv_mass, dtype=np.float64)
+        if Minv.shape != P.shape:
+            raise ValueError("inv_mass must have the shape of precision_matrix")
+        try:
+            L = np.linalg.cholesky(Minv)
+        except np.linalg.LinAlgError as e:
+            raise ValueError("inv_mass must be symmetric positive definite") from e
+        A = L.T @ P @ L
+    else:
+        A = P
+    spec = DeviceSpec(_lib.TS_DENSE_GAUSS, D, params=np.ascontiguousarray(A).ravel(), precision=precision)
+    spec.reparam = L
+    params = {"dim": D, "dense_mass": L is not None}
+    if L is None:
+        return _device_model("dense_gaussian", spec, params)
+
+    # user-facing potential / gradient in q coordinates (q = L x)
+    def potential(q):
+        x = np.linalg.solve(L, np.asarray(q, dtype=np.float64))
+        return float(potential_and_gradient(spec, x.reshape(1, -1))[0, 0])
+
+    def gradient(q):
+        x = np.linalg.solve(L, np.asarray(q, dtype=np.float64))
+        return np.linalg.solve(L.T, potential_and_gradient(spec, x.reshape(1, -1))[0, 1:])
+
+    return TargetModel("dense_gaussian", D, potential, gradient, params, spec)
+
+
 def fd_gradient(model: TargetModel, q: np.ndarray, h: float = 1e-5) -> np.ndarray:
     """Central-difference gradient oracle (models.py:147-160)."""
     if h <= 0:
@@ -308,4 +360,4 @@ def model_from_descriptor(descriptor, base_dir=None) -> TargetModel:
     raise ValueError(f"unknown model name: {name!r}")
 
 
-BUILTIN_MODELS = ("std_normal", "gaussian", "logistic_regression", "funnel", "eight_schools")
+BUILTIN_MODELS = ("std_normal", "gaussian", "logistic_regression", "funnel", "eight_schools", "dense_gaussian")

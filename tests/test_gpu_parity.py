@@ -500,3 +500,135 @@ def test_row_shard_mailbox_world1_identical(p):
         rb = t.run_device(shard, cfg, t.chain_keys(4, 1), 0)
         assert np.array_equal(ra.samples.cpu().numpy(), rb.samples.cpu().numpy())
         assert np.array_equal(ra.stats.cpu().numpy(), rb.stats.cpu().numpy())
+
+
+# ----------------------------------------------------------------------------- tcgen05 GEMM (config 4)
+
+
+def _tf32(a):
+    """Round fp32 to the nearest tf32 (10-bit mantissa), ties away (cvt.rna)."""
+    b = np.asarray(a, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    b = ((b + 0x1000) & 0xFFFFE000).astype(np.uint32)
+    return b.view(np.float32)
+
+
+@pytest.mark.parametrize("M,N,K,grid", [(128, 64, 32, 0), (200, 100, 60, 0), (1000, 1024, 1000, 0), (1000, 1024, 1000, 37)])
+def test_tcgen05_tf32_gemm_probe(M, N, K, grid):
+    import torch
+
+    t = ts()
+    lib = t._lib.load_library()
+    rng = np.random.default_rng(M + N + K)
+    a = _tf32(rng.standard_normal((M, K)).astype(np.float32))
+    xt = _tf32(rng.standard_normal((N, K)).astype(np.float32))
+    ad, xd = torch.from_numpy(a).cuda(), torch.from_numpy(xt).cuda()
+    gt = torch.full((N, M), float("nan"), dtype=torch.float32, device="cuda")
+    t._lib.check(lib.ts_gemm_tf32_probe(ad.data_ptr(), xd.data_ptr(), gt.data_ptr(), M, N, K, grid, 0))
+    torch.cuda.synchronize()
+    ref = xt.astype(np.float64) @ a.astype(np.float64).T
+    got = gt.cpu().numpy().astype(np.float64)
+    # tf32 x tf32 products are exact in fp32; only fp32 accumulation rounds
+    err = np.abs(got - ref).max() / np.abs(ref).max()
+    assert err < 1e-5, err
+
+
+def _spd(D, seed, cond=100.0):
+    rng = np.random.default_rng(seed)
+    q, _ = np.linalg.qr(rng.standard_normal((D, D)))
+    lam = np.logspace(-np.log10(cond) / 2, np.log10(cond) / 2, D)
+    return (q * lam) @ q.T
+
+
+@pytest.mark.parametrize("D", [16, 100])
+def test_dense_potential_gradient(D, oracle):
+    t = ts()
+    A = _spd(D, D)
+    om = oracle.Model("dense_gaussian", D, dense_a=A.tolist())
+    q = np.random.default_rng(1).standard_normal((3, D))
+    m64 = t.dense_gaussian_model(A, precision="fp64")
+    out = t.models.potential_and_gradient(m64.device_spec, q)
+    for k in range(3):
+        assert out[k, 0] == om.potential(q[k].tolist())  # SIMT fp64 policy: bit for bit
+        assert np.array_equal(out[k, 1:], np.asarray(om.gradient(q[k].tolist())))
+    if D % 4 == 0:
+        m32 = t.dense_gaussian_model(A, precision="tf32")
+        o32 = t.models.potential_and_gradient(m32.device_spec, q)
+        g = q @ A.T
+        # TF32 operands (10-bit mantissa): stated tolerance 2e-3 relative to |g|
+        assert np.abs(o32[:, 1:] - g).max() <= 2e-3 * np.abs(g).max()
+        assert np.allclose(o32[:, 0], 0.5 * np.einsum("kd,kd->k", q, g), rtol=2e-3)
+
+
+def test_dense_tree_fp64_matches_oracle(oracle):
+    t = ts()
+    D = 16
+    A = _spd(D, 3)
+    om = oracle.Model("dense_gaussian", D, dense_a=A.tolist())
+    m = t.dense_gaussian_model(A, precision="fp64")
+    rng = np.random.default_rng(9)
+    bad_int = 0
+    for case in range(12):
+        q, r = rng.standard_normal(D), rng.standard_normal(D)
+        U, g = om.potential(q.tolist()), om.gradient(q.tolist())
+        eps = [0.05, 0.2, 0.6][case % 3]
+        cfg = t.SamplerConfig(step_size=eps, mass=t.MassMatrix.identity(D), max_tree_depth=8)
+        key = t.RngKey.from_seed(100 + case)
+        z = t.PhasePoint(q, r, U, np.asarray(g))
+        h0 = t.hamiltonian(z, cfg.mass)
+        tr = t.TreeTrace()
+        depth = 1 + case % 6
+        tree = t.build_tree_iterative(z, depth, eps * (1 if case % 2 else -1), cfg, m, key, h_ref=h0, trace=tr)
+        ot = oracle.build_tree(oracle.Point(q.tolist(), r.tolist(), U, g), depth, eps * (1 if case % 2 else -1),
+                               [1.0] * D, om, (key.hi, key.lo), h0)
+        ints = (tree.leapfrog_count, tree.turning, tree.diverging, tree.proposal_leaf) == (
+            ot.sub.count, ot.turning, ot.diverging, ot.sub.prop_leaf) and [tuple(c) for c in tr.checks] == [
+            tuple(c) for c in ot.checks]
+        bad_int += not ints
+        if ints:
+            assert close(tree.right.position, ot.sub.last.q, BLOCK_REL, atol=BLOCK_REL)
+            assert close(tree.log_weight, ot.sub.lw, BLOCK_REL)
+    assert bad_int == 0
+
+
+def test_dense_many_chains_tf32_vs_fp64():
+    """Config-4 path at small scale: 64 chains in lockstep; the TF32 tensor-core
+    run agrees with the fp64 SIMT run statistically and in its first tree
+    decisions (acceptance/depth), and both recover the target moments."""
+    t = ts()
+    D, C = 32, 64
+    A = _spd(D, 5, cond=10.0)
+    cov = np.linalg.inv(A)
+    cfg = t.RunConfig(model={}, num_chains=C, num_warmup=200, num_samples=200, seed=11)
+    keys = t.chain_keys(11, C)
+    runs = {}
+    for prec in ("fp64", "tf32"):
+        m = t.dense_gaussian_model(A, precision=prec)
+        runs[prec] = t.run_device(m, cfg, keys, 0)
+    s64 = runs["fp64"].samples.cpu().numpy()
+    s32 = runs["tf32"].samples.cpu().numpy()
+    st64 = runs["fp64"].stats.cpu().numpy()
+    st32 = runs["tf32"].stats.cpu().numpy()
+    # first warmup transition of every chain: same start, same randomness
+    same_depth = np.mean(st64[:, 0, 0] == st32[:, 0, 0])
+    assert same_depth >= 0.9, same_depth
+    for s in (s64, s32):
+        flat = s.reshape(-1, D)
+        assert np.abs(flat.mean(0)).max() < 6 * np.sqrt(np.diag(cov).max() / (C * 200 / 5))
+        assert np.allclose(flat.var(0), np.diag(cov), rtol=0.15)
+    rhat = t.split_rhat(s32)
+    assert np.nanmax(rhat) < 1.05
+
+
+def test_dense_mass_reparametrisation():
+    """Dense inverse mass M^-1 = Sigma: the sampler runs on x = L^-1 q and
+    returns q; moments match Sigma."""
+    t = ts()
+    D, C = 16, 32
+    A = _spd(D, 7, cond=1000.0)
+    cov = np.linalg.inv(A)
+    m = t.dense_gaussian_model(A, inv_mass=cov, precision="fp64")
+    cfg = t.RunConfig(model={}, num_chains=C, num_warmup=100, num_samples=300, seed=2)
+    r = t.run_device(m, cfg, t.chain_keys(2, C), 0)
+    flat = r.samples.cpu().numpy().reshape(-1, D)
+    emp = np.cov(flat.T)
+    assert np.abs(emp - cov).max() <= 0.15 * np.abs(cov).max()

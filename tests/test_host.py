@@ -249,3 +249,28 @@ def test_chunked_generator_matches_one_shot():
         for a, b in ((0, n // 3), (n // 3, n), (n // 2, n // 2 + 1)):
             xs, ys = logistic_data_f32(n, p, 20191223, chunk_rows=chunk, rows=(a, b))
             assert np.array_equal(xs, x32[a:b]) and np.array_equal(ys, y8[a:b])
+
+
+def test_dense_gaussian_model_validation():
+    with pytest.raises(ValueError):
+        t.dense_gaussian_model(np.ones((3, 4)))
+    with pytest.raises(ValueError):
+        t.dense_gaussian_model(np.eye(3), inv_mass=-np.eye(3))
+    with pytest.raises(ValueError):
+        t.dense_gaussian_model(np.eye(3), precision="bf16")
+    m = t.dense_gaussian_model(np.eye(4) * 2.0, inv_mass=np.eye(4) * 0.25, precision="fp64")
+    assert m.name == "dense_gaussian" and m.dim == 4
+    # x = L^-1 q with L = 0.5 I: A = L' P L = 0.5 I
+    assert np.allclose(m.device_spec.params.reshape(4, 4), np.eye(4) * 0.5)
+    assert np.allclose(m.device_spec.reparam, np.eye(4) * 0.5)
+
+
+def test_oracle_dense_gaussian(oracle):
+    rng = np.random.default_rng(0)
+    a = rng.standard_normal((40, 40))
+    a = a @ a.T
+    x = rng.standard_normal(40)
+    m = oracle.Model("dense_gaussian", 40, dense_a=a.tolist())
+    g = np.asarray(m.gradient(x.tolist()))
+    assert np.allclose(g, a @ x, rtol=1e-12, atol=1e-12)
+    assert np.isclose(m.potential(x.tolist()), 0.5 * x @ a @ x, rtol=1e-12)

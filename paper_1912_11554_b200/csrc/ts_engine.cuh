@@ -46,6 +46,130 @@ constexpr int kTeamScratch = 64 + (kMaxSlots * 56 + 7) / 8;
 constexpr int kEngineSlotBytes = 1024;
 __device__ __forceinline__ int slot_vec(int s, int k) { return V_SLOT0 + kSlotVecs * s + k; }
 
+// Warp copy of n2 double2 (lane-strided, 8 loads in flight per lane).  A
+// separate function: its registers stay out of the engine's allocation.
+static __device__ __noinline__ void warp_copy2(double2* __restrict__ a, const double2* __restrict__ b, int n2) {
+  for (int base = (int)(threadIdx.x & 31); base < n2; base += 32 * 8) {
+    double2 t[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (base + 32 * u < n2) t[u] = b[base + 32 * u];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (base + 32 * u < n2) a[base + 32 * u] = t[u];
+  }
+}
+
+// Elementwise leaf updates for warp-owned large-D vectors: 16-byte accesses,
+// 4 x double2 per operand in flight per lane; per-component arithmetic is the
+// same as the scalar loops (so results are identical).
+static __device__ __noinline__ void warp_drift2(double2* __restrict__ nq, double2* __restrict__ nr,
+                                                const double2* __restrict__ q, const double2* __restrict__ r,
+                                                const double2* __restrict__ g, const double2* __restrict__ inv,
+                                                double half, double eps, int n2) {
+  for (int base = (int)(threadIdx.x & 31); base < n2; base += 32 * 4) {
+    double2 tq[4], tr[4], tg[4], ti[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (base + 32 * u < n2) { tq[u] = q[base + 32 * u]; tr[u] = r[base + 32 * u]; tg[u] = g[base + 32 * u]; ti[u] = inv[base + 32 * u]; }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (base + 32 * u < n2) {
+        double2 rh, nqv;
+        rh.x = __dsub_rn(tr[u].x, __dmul_rn(half, tg[u].x));
+        rh.y = __dsub_rn(tr[u].y, __dmul_rn(half, tg[u].y));
+        nqv.x = __dadd_rn(tq[u].x, __dmul_rn(eps, __dmul_rn(ti[u].x, rh.x)));
+        nqv.y = __dadd_rn(tq[u].y, __dmul_rn(eps, __dmul_rn(ti[u].y, rh.y)));
+        nr[base + 32 * u] = rh;
+        nq[base + 32 * u] = nqv;
+      }
+  }
+}
+static __device__ __noinline__ void warp_advance2(double2* __restrict__ q, double2* __restrict__ r,
+                                                  double2* __restrict__ g, const double2* __restrict__ nq,
+                                                  const double2* __restrict__ nr, const double2* __restrict__ ng,
+                                                  double half, int n2) {
+  for (int base = (int)(threadIdx.x & 31); base < n2; base += 32 * 4) {
+    double2 tq[4], tr[4], tg[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (base + 32 * u < n2) { tq[u] = nq[base + 32 * u]; tr[u] = nr[base + 32 * u]; tg[u] = ng[base + 32 * u]; }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (base + 32 * u < n2) {
+        double2 rv;
+        rv.x = __dsub_rn(tr[u].x, __dmul_rn(half, tg[u].x));
+        rv.y = __dsub_rn(tr[u].y, __dmul_rn(half, tg[u].y));
+        q[base + 32 * u] = tq[u];
+        g[base + 32 * u] = tg[u];
+        r[base + 32 * u] = rv;
+      }
+  }
+}
+static __device__ __noinline__ void warp_add2(double2* __restrict__ c, const double2* __restrict__ r, int n2) {
+  for (int base = (int)(threadIdx.x & 31); base < n2; base += 32 * 8) {
+    double2 tc[8], tr[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (base + 32 * u < n2) { tc[u] = c[base + 32 * u]; tr[u] = r[base + 32 * u]; }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (base + 32 * u < n2) {
+        double2 o;
+        o.x = __dadd_rn(tc[u].x, tr[u].x);
+        o.y = __dadd_rn(tc[u].y, tr[u].y);
+        c[base + 32 * u] = o;
+      }
+  }
+}
+// per-lane partial of kinetic_energy_impl over warp-owned vectors (lane's
+// components in order 2k, 2k+1 of each of its double2 slots)
+static __device__ __noinline__ double warp_kinetic2(const double2* __restrict__ r, const double2* __restrict__ inv, int n2) {
+  double acc = 0.0;
+  for (int base = (int)(threadIdx.x & 31); base < n2; base += 32 * 8) {
+    double2 tr[8], ti[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (base + 32 * u < n2) { tr[u] = r[base + 32 * u]; ti[u] = inv[base + 32 * u]; }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (base + 32 * u < n2) {
+        acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(__dmul_rn(0.5, tr[u].x), tr[u].x), ti[u].x));
+        acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(__dmul_rn(0.5, tr[u].y), tr[u].y), ti[u].y));
+      }
+  }
+  return acc;
+}
+// generalized U-turn dots of the running subtree with rho = (cum - cum_first) + r_first
+// formed on the fly: per-lane partials a = sum rho inv rl, b = sum rho inv rr
+static __device__ __noinline__ void warp_gen_uturn2(const double2* __restrict__ cum, const double2* __restrict__ cf,
+                                                    const double2* __restrict__ fr, const double2* __restrict__ inv,
+                                                    const double2* __restrict__ rr, int n2, double* ab) {
+  double a = 0.0, b = 0.0;
+  for (int base = (int)(threadIdx.x & 31); base < n2; base += 32 * 4) {
+    double2 tc[4], tf[4], trf[4], ti[4], trr[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (base + 32 * u < n2) {
+        tc[u] = cum[base + 32 * u]; tf[u] = cf[base + 32 * u]; trf[u] = fr[base + 32 * u];
+        ti[u] = inv[base + 32 * u]; trr[u] = rr[base + 32 * u];
+      }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (base + 32 * u < n2) {
+        const double wx = __dmul_rn(__dadd_rn(__dsub_rn(tc[u].x, tf[u].x), trf[u].x), ti[u].x);
+        const double wy = __dmul_rn(__dadd_rn(__dsub_rn(tc[u].y, tf[u].y), trf[u].y), ti[u].y);
+        a = __dadd_rn(a, __dmul_rn(wx, trf[u].x));
+        b = __dadd_rn(b, __dmul_rn(wx, trr[u].x));
+        a = __dadd_rn(a, __dmul_rn(wy, trf[u].y));
+        b = __dadd_rn(b, __dmul_rn(wy, trr[u].y));
+      }
+  }
+  ab[0] = a;
+  ab[1] = b;
+}
+__device__ __forceinline__ bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
 enum Stop : int { kStopNone = 0, kStopTurn = 1, kStopDiv = 2 };
 
 // trace event kinds (int32 x5 per event: kind, a, b, c, e)
@@ -173,6 +297,14 @@ struct Engine {
   __device__ __forceinline__ void copy(int dst, int src) {
     double* __restrict__ a = v(dst);
     const double* __restrict__ b = v(src);
+    if constexpr (Team::kWarp && Team::kUnitStride) {
+      // warp-owned contiguous vectors (large D in global memory): 16-byte
+      // accesses, 8 in flight per lane, so a copy costs ~D/512 round trips
+      if (((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15) == 0 && (D & 1) == 0 && D >= 128) {
+        warp_copy2(reinterpret_cast<double2*>(a), reinterpret_cast<const double2*>(b), D >> 1);
+        return;
+      }
+    }
     const int64_t s = ds();
     _Pragma("unroll 4") for (int d = T.rank(); d < D; d += T.size()) a[d * s] = b[d * s];
   }
@@ -218,6 +350,10 @@ struct Engine {
   __device__ double kinetic(int rid) {
     const double* __restrict__ r = v(rid);
     const double* __restrict__ inv = v(V_INV);
+    if constexpr (Team::kWarp && Team::kUnitStride) {
+      if (D >= 128 && (D & 1) == 0 && al16(r) && al16(inv))
+        return T.sum(warp_kinetic2(reinterpret_cast<const double2*>(r), reinterpret_cast<const double2*>(inv), D >> 1));
+    }
     const int64_t s = ds();
     double acc = 0.0;
     _Pragma("unroll 4") for (int d = T.rank(); d < D; d += T.size()) {
@@ -303,6 +439,19 @@ struct Engine {
       const double* __restrict__ cum = v(V_CUM);
       const double* __restrict__ cf = v(V_CUMF);
       const double* __restrict__ fr = v(V_FR);
+      if constexpr (Team::kWarp && Team::kUnitStride) {
+        const double* inv = v(V_INV);
+        const double* cr = v(V_CR);
+        if (D >= 128 && (D & 1) == 0 && al16(cum) && al16(cf) && al16(fr) && al16(inv) && al16(cr)) {
+          double ab[2];
+          warp_gen_uturn2(reinterpret_cast<const double2*>(cum), reinterpret_cast<const double2*>(cf),
+                          reinterpret_cast<const double2*>(fr), reinterpret_cast<const double2*>(inv),
+                          reinterpret_cast<const double2*>(cr), D >> 1, ab);
+          double a = ab[0], b = ab[1];
+          T.sum2(a, b);
+          return a < 0.0 || b < 0.0;
+        }
+      }
       _Pragma("unroll 4") for (int d = T.rank(); d < D; d += T.size()) rho[d * s] = __dadd_rn(__dsub_rn(cum[d * s], cf[d * s]), fr[d * s]);
       return uturn_dots(V_MSUM, V_FR, V_CR);
     }
@@ -326,6 +475,12 @@ struct Engine {
   __device__ void add_cum() {
     double* __restrict__ c = v(V_CUM);
     const double* __restrict__ r = v(V_CR);
+    if constexpr (Team::kWarp && Team::kUnitStride) {
+      if (D >= 128 && (D & 1) == 0 && al16(c) && al16(r)) {
+        warp_add2(reinterpret_cast<double2*>(c), reinterpret_cast<const double2*>(r), D >> 1);
+        return;
+      }
+    }
     const int64_t s = ds();
     _Pragma("unroll 4") for (int d = T.rank(); d < D; d += T.size()) c[d * s] = __dadd_rn(c[d * s], r[d * s]);
   }
@@ -341,6 +496,14 @@ struct Engine {
     double* __restrict__ nq = v(V_NQ);
     double* __restrict__ nr = v(V_NR);
     const double* __restrict__ inv = v(V_INV);
+    if constexpr (Team::kWarp && Team::kUnitStride) {
+      if (D >= 128 && (D & 1) == 0 && al16(q) && al16(r) && al16(g) && al16(nq) && al16(nr) && al16(inv)) {
+        warp_drift2(reinterpret_cast<double2*>(nq), reinterpret_cast<double2*>(nr), reinterpret_cast<const double2*>(q),
+                    reinterpret_cast<const double2*>(r), reinterpret_cast<const double2*>(g),
+                    reinterpret_cast<const double2*>(inv), half, eps, D >> 1);
+        return;
+      }
+    }
     const int64_t s = ds();
     _Pragma("unroll 4") for (int d = T.rank(); d < D; d += T.size()) {
       const double rh = __dsub_rn(r[d * s], __dmul_rn(half, g[d * s]));
@@ -356,6 +519,15 @@ struct Engine {
     const double* __restrict__ nq = v(V_NQ);
     const double* __restrict__ nr = v(V_NR);
     const double* __restrict__ ng = v(V_NG);
+    cur_U = u;
+    if constexpr (Team::kWarp && Team::kUnitStride) {
+      if (D >= 128 && (D & 1) == 0 && al16(q) && al16(r) && al16(g) && al16(nq) && al16(nr) && al16(ng)) {
+        warp_advance2(reinterpret_cast<double2*>(q), reinterpret_cast<double2*>(r), reinterpret_cast<double2*>(g),
+                      reinterpret_cast<const double2*>(nq), reinterpret_cast<const double2*>(nr),
+                      reinterpret_cast<const double2*>(ng), half, D >> 1);
+        return;
+      }
+    }
     const int64_t s = ds();
     _Pragma("unroll 4") for (int d = T.rank(); d < D; d += T.size()) {
       const double gg = ng[d * s];
@@ -363,7 +535,6 @@ struct Engine {
       g[d * s] = gg;
       r[d * s] = __dsub_rn(nr[d * s], __dmul_rn(half, gg));
     }
-    cur_U = u;
   }
 
   // Bookkeeping of leaf n (tree.py:403-450): divergence exit, even-leaf store

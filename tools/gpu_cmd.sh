@@ -1,1 +1,2 @@
-DENSE_ONLY_MASS=1 timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_dense_op -c 1 -o gpurun_out/dense1 python tools/dense_bench.py tf32 256 20 10 > gpurun_out/ncu_dense1.log 2>&1
+TS_PROF=1 timeout 300 python tools/dense_bench.py tf32 1024 20 10 > gpurun_out/d3.log 2>&1
+timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/t31.log 2>&1

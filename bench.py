@@ -525,14 +525,22 @@ def main():
         torch.cuda.synchronize()
         eval_us = float(out.cpu().numpy()[1]) / 1000.0 / 200
         eval_gbs = ALGO_BYTES_PER_PASS / (eval_us * 1e-6) / 1e9
+        # DRAM traffic per data pass from the committed ncu capture of this kernel
+        traffic = None
+        try:
+            with open(os.path.join(ROOT, "profiles", f"r1_ncu_run_{precision}.json")) as fh:
+                rec = json.load(fh)[0]
+            traffic = rec["dram_bytes_per_pass"]
+        except Exception:
+            pass
         return {
             "value": lf_total / (t_total_ms / 1000.0),
             "ms_per_step": t_total_ms / args.steps,
             "ess_per_sec": ess_total / (t_total_ms / 1000.0),
             "leapfrogs_per_step": lf_total / args.steps,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
-                         "bytes_per_pass": ALGO_BYTES_PER_PASS, "passes": sum(ev_list)},
+                         "frac": achieved / peak, "traffic": traffic, "traffic_per": "data pass (ncu, profiles/)",
+                         "peak_kind": peak_kind, "bytes_per_pass": ALGO_BYTES_PER_PASS, "passes": sum(ev_list)},
             "eval_only": {"us_per_pass": eval_us, "achieved_gbs": eval_gbs, "frac": eval_gbs / peak},
             "clocks": clocks.summary() if with_clocks else None,
             "last": last,

@@ -295,9 +295,9 @@ struct Engine {
 
   // ------------------------------------------------------- vector helpers
   __device__ __forceinline__ void copy(int dst, int src) {
-    double* __restrict__ a = v(dst);
-    const double* __restrict__ b = v(src);
-    if constexpr (Team::kWarp && Team::kUnitStride) {
+    double* a = v(dst);
+    const double* b = v(src);
+    if constexpr (Team::kWarp && Team::kUnitStride && Model::kVecOps) {
       // warp-owned contiguous vectors (large D in global memory): 16-byte
       // accesses, 8 in flight per lane, so a copy costs ~D/512 round trips
       if (((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15) == 0 && (D & 1) == 0 && D >= 128) {
@@ -306,12 +306,12 @@ struct Engine {
       }
     }
     const int64_t s = ds();
-    _Pragma("unroll 4") for (int d = T.rank(); d < D; d += T.size()) a[d * s] = b[d * s];
+    for (int d = T.rank(); d < D; d += T.size()) a[d * s] = b[d * s];
   }
   __device__ __forceinline__ void fill(int dst, double x) {
-    double* __restrict__ a = v(dst);
+    double* a = v(dst);
     const int64_t s = ds();
-    _Pragma("unroll 4") for (int d = T.rank(); d < D; d += T.size()) a[d * s] = x;
+    for (int d = T.rank(); d < D; d += T.size()) a[d * s] = x;
   }
 
   // model evaluation at vector qid -> U (non-finite -> +inf), gradient -> gid
@@ -348,15 +348,15 @@ struct Engine {
 
   // kinetic_energy_impl (kernels.py:125-130): sum 0.5 r r inv, left to right
   __device__ double kinetic(int rid) {
-    const double* __restrict__ r = v(rid);
-    const double* __restrict__ inv = v(V_INV);
-    if constexpr (Team::kWarp && Team::kUnitStride) {
+    const double* r = v(rid);
+    const double* inv = v(V_INV);
+    if constexpr (Team::kWarp && Team::kUnitStride && Model::kVecOps) {
       if (D >= 128 && (D & 1) == 0 && al16(r) && al16(inv))
         return T.sum(warp_kinetic2(reinterpret_cast<const double2*>(r), reinterpret_cast<const double2*>(inv), D >> 1));
     }
     const int64_t s = ds();
     double acc = 0.0;
-    _Pragma("unroll 4") for (int d = T.rank(); d < D; d += T.size()) {
+    for (int d = T.rank(); d < D; d += T.size()) {
       const double x = r[d * s];
       acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(__dmul_rn(0.5, x), x), inv[d * s]));
     }
@@ -371,13 +371,13 @@ struct Engine {
 
   // uturn_dots (kernels.py:132-139): (sum rho inv rl < 0) or (sum rho inv rr < 0)
   __device__ bool uturn_dots(int rho_id, int rl_id, int rr_id) {
-    const double* __restrict__ rho = v(rho_id);
-    const double* __restrict__ inv = v(V_INV);
-    const double* __restrict__ rl = v(rl_id);
-    const double* __restrict__ rr = v(rr_id);
+    const double* rho = v(rho_id);
+    const double* inv = v(V_INV);
+    const double* rl = v(rl_id);
+    const double* rr = v(rr_id);
     const int64_t s = ds();
     double a = 0.0, b = 0.0;
-    _Pragma("unroll 4") for (int d = T.rank(); d < D; d += T.size()) {
+    for (int d = T.rank(); d < D; d += T.size()) {
       const double w = __dmul_rn(rho[d * s], inv[d * s]);
       a = __dadd_rn(a, __dmul_rn(w, rl[d * s]));
       b = __dadd_rn(b, __dmul_rn(w, rr[d * s]));
@@ -389,18 +389,18 @@ struct Engine {
   // leapfrog on (CQ, CR, CG, cur_U) in place (integrator.py:90-103)
   __device__ void leapfrog(double eps) {
     const double half = __dmul_rn(0.5, eps);
-    double* __restrict__ q = v(V_CQ);
-    double* __restrict__ r = v(V_CR);
-    const double* __restrict__ g = v(V_CG);
-    const double* __restrict__ inv = v(V_INV);
+    double* q = v(V_CQ);
+    double* r = v(V_CR);
+    const double* g = v(V_CG);
+    const double* inv = v(V_INV);
     const int64_t s = ds();
-    _Pragma("unroll 4") for (int d = T.rank(); d < D; d += T.size()) {
+    for (int d = T.rank(); d < D; d += T.size()) {
       const double rh = __dsub_rn(r[d * s], __dmul_rn(half, g[d * s]));
       r[d * s] = rh;
       q[d * s] = __dadd_rn(q[d * s], __dmul_rn(eps, __dmul_rn(inv[d * s], rh)));
     }
     cur_U = eval(V_CQ, V_CG);
-    _Pragma("unroll 4") for (int d = T.rank(); d < D; d += T.size()) r[d * s] = __dsub_rn(r[d * s], __dmul_rn(half, g[d * s]));
+    for (int d = T.rank(); d < D; d += T.size()) r[d * s] = __dsub_rn(r[d * s], __dmul_rn(half, g[d * s]));
   }
 
   // ------------------------------------------------------- tree builder
@@ -435,11 +435,11 @@ struct Engine {
     const int64_t s = ds();
     if (cfg.generalized) {
       // rho = (cum_last - cum_first) + first.r  -> V_MSUM as scratch
-      double* __restrict__ rho = v(V_MSUM);
-      const double* __restrict__ cum = v(V_CUM);
-      const double* __restrict__ cf = v(V_CUMF);
-      const double* __restrict__ fr = v(V_FR);
-      if constexpr (Team::kWarp && Team::kUnitStride) {
+      double* rho = v(V_MSUM);
+      const double* cum = v(V_CUM);
+      const double* cf = v(V_CUMF);
+      const double* fr = v(V_FR);
+      if constexpr (Team::kWarp && Team::kUnitStride && Model::kVecOps) {
         const double* inv = v(V_INV);
         const double* cr = v(V_CR);
         if (D >= 128 && (D & 1) == 0 && al16(cum) && al16(cf) && al16(fr) && al16(inv) && al16(cr)) {
@@ -452,17 +452,17 @@ struct Engine {
           return a < 0.0 || b < 0.0;
         }
       }
-      _Pragma("unroll 4") for (int d = T.rank(); d < D; d += T.size()) rho[d * s] = __dadd_rn(__dsub_rn(cum[d * s], cf[d * s]), fr[d * s]);
+      for (int d = T.rank(); d < D; d += T.size()) rho[d * s] = __dadd_rn(__dsub_rn(cum[d * s], cf[d * s]), fr[d * s]);
       return uturn_dots(V_MSUM, V_FR, V_CR);
     }
-    double* __restrict__ dq = v(V_MSUM);
-    const double* __restrict__ lq = v(V_CQ);
-    const double* __restrict__ fq = v(V_FQ);
+    double* dq = v(V_MSUM);
+    const double* lq = v(V_CQ);
+    const double* fq = v(V_FQ);
     if (forward) {
-      _Pragma("unroll 4") for (int d = T.rank(); d < D; d += T.size()) dq[d * s] = __dsub_rn(lq[d * s], fq[d * s]);
+      for (int d = T.rank(); d < D; d += T.size()) dq[d * s] = __dsub_rn(lq[d * s], fq[d * s]);
       return uturn_dots(V_MSUM, V_FR, V_CR);
     }
-    _Pragma("unroll 4") for (int d = T.rank(); d < D; d += T.size()) dq[d * s] = __dsub_rn(fq[d * s], lq[d * s]);
+    for (int d = T.rank(); d < D; d += T.size()) dq[d * s] = __dsub_rn(fq[d * s], lq[d * s]);
     return uturn_dots(V_MSUM, V_CR, V_FR);
   }
 
@@ -473,16 +473,16 @@ struct Engine {
   }
 
   __device__ void add_cum() {
-    double* __restrict__ c = v(V_CUM);
-    const double* __restrict__ r = v(V_CR);
-    if constexpr (Team::kWarp && Team::kUnitStride) {
+    double* c = v(V_CUM);
+    const double* r = v(V_CR);
+    if constexpr (Team::kWarp && Team::kUnitStride && Model::kVecOps) {
       if (D >= 128 && (D & 1) == 0 && al16(c) && al16(r)) {
         warp_add2(reinterpret_cast<double2*>(c), reinterpret_cast<const double2*>(r), D >> 1);
         return;
       }
     }
     const int64_t s = ds();
-    _Pragma("unroll 4") for (int d = T.rank(); d < D; d += T.size()) c[d * s] = __dadd_rn(c[d * s], r[d * s]);
+    for (int d = T.rank(); d < D; d += T.size()) c[d * s] = __dadd_rn(c[d * s], r[d * s]);
   }
 
   // Split leapfrog for the speculative pipeline: drift from the current leaf
@@ -490,13 +490,13 @@ struct Engine {
   // gets its kick (same arithmetic as leapfrog()).
   __device__ void drift_next(double eps) {
     const double half = __dmul_rn(0.5, eps);
-    const double* __restrict__ q = v(V_CQ);
-    const double* __restrict__ r = v(V_CR);
-    const double* __restrict__ g = v(V_CG);
-    double* __restrict__ nq = v(V_NQ);
-    double* __restrict__ nr = v(V_NR);
-    const double* __restrict__ inv = v(V_INV);
-    if constexpr (Team::kWarp && Team::kUnitStride) {
+    const double* q = v(V_CQ);
+    const double* r = v(V_CR);
+    const double* g = v(V_CG);
+    double* nq = v(V_NQ);
+    double* nr = v(V_NR);
+    const double* inv = v(V_INV);
+    if constexpr (Team::kWarp && Team::kUnitStride && Model::kVecOps) {
       if (D >= 128 && (D & 1) == 0 && al16(q) && al16(r) && al16(g) && al16(nq) && al16(nr) && al16(inv)) {
         warp_drift2(reinterpret_cast<double2*>(nq), reinterpret_cast<double2*>(nr), reinterpret_cast<const double2*>(q),
                     reinterpret_cast<const double2*>(r), reinterpret_cast<const double2*>(g),
@@ -505,7 +505,7 @@ struct Engine {
       }
     }
     const int64_t s = ds();
-    _Pragma("unroll 4") for (int d = T.rank(); d < D; d += T.size()) {
+    for (int d = T.rank(); d < D; d += T.size()) {
       const double rh = __dsub_rn(r[d * s], __dmul_rn(half, g[d * s]));
       nr[d * s] = rh;
       nq[d * s] = __dadd_rn(q[d * s], __dmul_rn(eps, __dmul_rn(inv[d * s], rh)));
@@ -513,14 +513,14 @@ struct Engine {
   }
   __device__ void advance_leaf(double eps, double u) {
     const double half = __dmul_rn(0.5, eps);
-    double* __restrict__ q = v(V_CQ);
-    double* __restrict__ r = v(V_CR);
-    double* __restrict__ g = v(V_CG);
-    const double* __restrict__ nq = v(V_NQ);
-    const double* __restrict__ nr = v(V_NR);
-    const double* __restrict__ ng = v(V_NG);
+    double* q = v(V_CQ);
+    double* r = v(V_CR);
+    double* g = v(V_CG);
+    const double* nq = v(V_NQ);
+    const double* nr = v(V_NR);
+    const double* ng = v(V_NG);
     cur_U = u;
-    if constexpr (Team::kWarp && Team::kUnitStride) {
+    if constexpr (Team::kWarp && Team::kUnitStride && Model::kVecOps) {
       if (D >= 128 && (D & 1) == 0 && al16(q) && al16(r) && al16(g) && al16(nq) && al16(nr) && al16(ng)) {
         warp_advance2(reinterpret_cast<double2*>(q), reinterpret_cast<double2*>(r), reinterpret_cast<double2*>(g),
                       reinterpret_cast<const double2*>(nq), reinterpret_cast<const double2*>(nr),
@@ -529,11 +529,48 @@ struct Engine {
       }
     }
     const int64_t s = ds();
-    _Pragma("unroll 4") for (int d = T.rank(); d < D; d += T.size()) {
+    for (int d = T.rank(); d < D; d += T.size()) {
       const double gg = ng[d * s];
       q[d * s] = nq[d * s];
       g[d * s] = gg;
       r[d * s] = __dsub_rn(nr[d * s], __dmul_rn(half, gg));
+    }
+  }
+
+  // advance_leaf(eps, u) followed by drift_next(eps) in one pass over the
+  // vectors (same arithmetic, element by element)
+  __device__ void advance_drift(double eps, double u) {
+    const double half = __dmul_rn(0.5, eps);
+    double* q = v(V_CQ);
+    double* r = v(V_CR);
+    double* g = v(V_CG);
+    double* nq = v(V_NQ);
+    double* nr = v(V_NR);
+    const double* ng = v(V_NG);
+    const double* inv = v(V_INV);
+    cur_U = u;
+    if constexpr (Team::kWarp && Team::kUnitStride && Model::kVecOps) {
+      if (D >= 128 && (D & 1) == 0 && al16(q) && al16(r) && al16(g) && al16(nq) && al16(nr) && al16(ng) && al16(inv)) {
+        warp_advance2(reinterpret_cast<double2*>(q), reinterpret_cast<double2*>(r), reinterpret_cast<double2*>(g),
+                      reinterpret_cast<const double2*>(nq), reinterpret_cast<const double2*>(nr),
+                      reinterpret_cast<const double2*>(ng), half, D >> 1);
+        warp_drift2(reinterpret_cast<double2*>(nq), reinterpret_cast<double2*>(nr), reinterpret_cast<const double2*>(q),
+                    reinterpret_cast<const double2*>(r), reinterpret_cast<const double2*>(g),
+                    reinterpret_cast<const double2*>(inv), half, eps, D >> 1);
+        return;
+      }
+    }
+    const int64_t s = ds();
+    for (int d = T.rank(); d < D; d += T.size()) {
+      const double gg = ng[d * s];
+      const double qq = nq[d * s];
+      const double rr = __dsub_rn(nr[d * s], __dmul_rn(half, gg));
+      q[d * s] = qq;
+      g[d * s] = gg;
+      r[d * s] = rr;
+      const double rh = __dsub_rn(rr, __dmul_rn(half, gg));
+      nr[d * s] = rh;
+      nq[d * s] = __dadd_rn(qq, __dmul_rn(eps, __dmul_rn(inv[d * s], rh)));
     }
   }
 
@@ -619,15 +656,19 @@ struct Engine {
         post_eval(V_NQ, V_NG);
         for (unsigned long long n = 0; n < nleaves; ++n) {
           const double u = wait_eval();
-          advance_leaf(eps, u);
+          const bool spec = n + 1 < nleaves;
+          if (spec) {
+            // leaf n's kick fused with leaf n+1's drift: the next pass is
+            // posted after one vector loop; leaf n's energy, prefix sum and
+            // bookkeeping overlap with it
+            advance_drift(eps, u);
+            post_eval(V_NQ, V_NG);
+          } else {
+            advance_leaf(eps, u);
+          }
           add_cum();
           double h, delta;
           leaf_energy(h_ref, h, delta);
-          const bool spec = n + 1 < nleaves;
-          if (spec) {
-            drift_next(eps);
-            post_eval(V_NQ, V_NG);
-          }
           stop = leaf_book(n, h, delta, draws, forward);
           if (stop != kStopNone) {
             if (spec) { (void)wait_eval(); n_wasted += 1; }
@@ -647,12 +688,12 @@ struct Engine {
     }
     // momentum_sum = (cum_last - cum_first) + first.r   (tree.py:283-294)
     {
-      double* __restrict__ ms = v(V_MSUM);
-      const double* __restrict__ cum = v(V_CUM);
-      const double* __restrict__ cf = v(V_CUMF);
-      const double* __restrict__ fr = v(V_FR);
+      double* ms = v(V_MSUM);
+      const double* cum = v(V_CUM);
+      const double* cf = v(V_CUMF);
+      const double* fr = v(V_FR);
       const int64_t s = ds();
-      _Pragma("unroll 4") for (int d = T.rank(); d < D; d += T.size()) ms[d * s] = __dadd_rn(__dsub_rn(cum[d * s], cf[d * s]), fr[d * s]);
+      for (int d = T.rank(); d < D; d += T.size()) ms[d * s] = __dadd_rn(__dsub_rn(cum[d * s], cf[d * s]), fr[d * s]);
     }
     if (tr != nullptr && T.leader()) tr->counts[2] = __popc(occupied_mask);
     TreeOut o;
@@ -665,11 +706,11 @@ struct Engine {
   // Momentum refresh r0 = N(0,1) * momentum_std (sampler.py:95); normals from
   // fold(key, 0) (or injected, std normal, component-major with stride inj_ds).
   __device__ void draw_momentum(int rid, Key nkey, const double* inj, int64_t inj_ds) {
-    double* __restrict__ r = v(rid);
-    const double* __restrict__ inv = v(V_INV);
+    double* r = v(rid);
+    const double* inv = v(V_INV);
     const int64_t s = ds();
     if (inj != nullptr) {
-      _Pragma("unroll 4") for (int d = T.rank(); d < D; d += T.size())
+      for (int d = T.rank(); d < D; d += T.size())
         r[d * s] = __dmul_rn(inj[d * inj_ds], __ddiv_rn(1.0, __dsqrt_rn(inv[d * s])));
       return;
     }
@@ -762,10 +803,10 @@ struct Engine {
       ev(kEvProposal, j, t.pidx, take ? 1 : 0);
       lw = logaddexp_np(lw, t.lw);
       {
-        double* __restrict__ rho = v(V_RHO);
-        const double* __restrict__ ms = v(V_MSUM);
+        double* rho = v(V_RHO);
+        const double* ms = v(V_MSUM);
         const int64_t s = ds();
-        _Pragma("unroll 4") for (int d = T.rank(); d < D; d += T.size()) rho[d * s] = __dadd_rn(rho[d * s], ms[d * s]);
+        for (int d = T.rank(); d < D; d += T.size()) rho[d * s] = __dadd_rn(rho[d * s], ms[d * s]);
       }
       if (go_right) { copy(V_RQ, V_CQ); copy(V_RR, V_CR); copy(V_RG, V_CG); RU = cur_U; }
       else { copy(V_LQ, V_CQ); copy(V_LR, V_CR); copy(V_LG, V_CG); LU = cur_U; }
@@ -774,11 +815,11 @@ struct Engine {
       if (cfg.generalized) {
         turned = uturn_dots(V_RHO, V_LR, V_RR);
       } else {
-        double* __restrict__ dq = v(V_MSUM);
-        const double* __restrict__ rq = v(V_RQ);
-        const double* __restrict__ lq = v(V_LQ);
+        double* dq = v(V_MSUM);
+        const double* rq = v(V_RQ);
+        const double* lq = v(V_LQ);
         const int64_t s = ds();
-        _Pragma("unroll 4") for (int d = T.rank(); d < D; d += T.size()) dq[d * s] = __dsub_rn(rq[d * s], lq[d * s]);
+        for (int d = T.rank(); d < D; d += T.size()) dq[d * s] = __dsub_rn(rq[d * s], lq[d * s]);
         turned = uturn_dots(V_MSUM, V_LR, V_RR);
       }
       ev(kEvOuter, j, turned ? 1 : 0, 0);

@@ -81,6 +81,7 @@ struct OpArgs {
 
 struct SmallW {
   static constexpr bool kAsync = false;
+  static constexpr bool kVecOps = false;  // Engine: 16-byte warp vector paths (large-D models only)
   SmallModel m;
   template <class Team>
   __device__ double eval(const Team& T, const VecStore& S, int q, int g) { return small_model_eval(T, m, S, q, g); }
@@ -96,6 +97,7 @@ struct LogisticW {
   int* cmd;  // smem: [0] 1 = evaluate / 0 = exit, [1] q vector id, [2] gradient vector id
   unsigned long long epoch;
   static constexpr bool kAsync = true;
+  static constexpr bool kVecOps = false;
   // driver warp: post a pass (non-blocking arrive on barrier 2) ...
   __device__ void post(int q, int g) {
     if (threadIdx.x == 0) { cmd[0] = 1; cmd[1] = q; cmd[2] = g; }

@@ -72,6 +72,7 @@ constexpr int kDenseCW = 8;  // chain warps per CTA
 
 struct DenseW {
   static constexpr bool kAsync = true;
+  static constexpr bool kVecOps = true;  // D ~ 1000 vectors in global memory
   int D;
   int fp64;
   float* xt;        // [Cpad][D] tf32-rounded positions (TF32 policy)

@@ -58,17 +58,28 @@ __global__ void __launch_bounds__(128, 1)
   g.release();
 }
 
-// ------------------------------------------------------------------ lockstep model
+// ------------------------------------------------------------------ batched model
 // Dense Gaussian U(x) = 1/2 x^T A x, gradient A x, for C chains at once.
 // CTA = 4 GEMM warps (warps 0..3) + kDenseCW chain warps; each chain warp
-// runs one chain (Engine<WarpTeam>, vectors in a global workspace).  A model
-// evaluation is a lockstep step of the whole grid: every chain warp posts
-// its position (named barrier 2), the GEMM warps of all CTAs meet at a grid
-// barrier, compute their tiles of GT = X A^T (tcgen05 TF32, or SIMT fp64 in
-// the parity policy), meet again, and release the chain warps (barrier 3),
-// which read their gradient row and form U = 1/2 x.g.  Chains that finished
-// their run keep posting idle steps until every chain is done.
+// runs one chain (Engine<WarpTeam>, vectors in a global workspace).
+//
+// The GEMM warps of all CTAs run a continuous sequence of batched steps,
+// decoupled from the chains: a chain posts a request (its position row in
+// XT, then posted[c] = seq with release semantics) and spins on served[c].
+// Each step, every CTA snapshots which of its chains have a request
+// outstanding (posted > served), the GEMM warps meet at a grid barrier,
+// compute GT = X A^T for the N-tiles holding outstanding requests (tcgen05
+// TF32, or SIMT fp64 in the parity policy), storing only outstanding
+// columns, meet again, and release served[c].  A chain's row is stable from
+// its post until it is served, and GT[c] is written only while c is
+// outstanding, so reads and writes never race.  Chains therefore never
+// wait for the slowest chain (no lockstep): a request waits at most one
+// step (~GEMM + 2 grid barriers).
 constexpr int kDenseCW = 8;  // chain warps per CTA
+
+__device__ __forceinline__ void st_release_gpu_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 
 struct DenseW {
   static constexpr bool kAsync = true;
@@ -79,8 +90,10 @@ struct DenseW {
   double* xt64;     // [Cpad][D] positions (FP64 policy)
   const float* gt;  // [Cpad][D] gradients
   const double* gt64;
+  unsigned long long* posted;  // [Cpad] request sequence numbers
+  unsigned long long* served;  // [Cpad]
+  unsigned long long seq;
   int chain;
-  volatile int* cmd;  // smem: 1 = step done, 0 = exit
   VecStore S;
   int pq, pg;
 
@@ -104,11 +117,15 @@ struct DenseW {
     asm volatile("fence.proxy.async.global;" ::: "memory");
     __threadfence();
     __syncwarp();
-    cta_arrive(2);
+    seq += 1;
+    if (lane == 0) st_release_gpu_u64(posted + chain, seq);
   }
   __device__ double wait() {
-    cta_bar(3);
     const int lane = threadIdx.x & 31;
+    if (lane == 0)
+      while (ld_acquire_u64(served + chain) < seq) {
+      }
+    __syncwarp();
     const double* qv = S.v(pq);
     double* gv = S.v(pg);
     double acc = 0.0;
@@ -135,13 +152,6 @@ struct DenseW {
     post(q, g);
     return wait();
   }
-  // finished chains: take part in the step without a position; true = exit
-  __device__ bool idle_step() {
-    __syncwarp();
-    cta_arrive(2);
-    cta_bar(3);
-    return *cmd == 0;
-  }
 };
 
 struct DenseArgs {
@@ -154,10 +164,15 @@ struct DenseArgs {
   double* ws;               // chain workspaces [C][nv][D]
   unsigned long long* bar;  // grid barrier counter (zeroed before launch)
   int* done;                // finished chain warps (zeroed before launch)
-  unsigned long long* prof;  // optional (TS_PROF): CTA-0 ns [wait for posts, GEMM, release], steps
+  unsigned long long* prof;  // optional (TS_PROF): CTA-0 ns [snapshot+barrier, GEMM, release], steps, busy steps
+  unsigned long long* posted;   // [Cpad] (zeroed before launch)
+  unsigned long long* served;   // [Cpad]
+  unsigned long long* pending;  // [Cpad] request served by the current step (0 = none)
+  unsigned long long* npend;    // [2] outstanding requests of the step (rotating)
 };
 
 __device__ __forceinline__ void gemm_grid_barrier(unsigned long long* bar, unsigned long long& epoch) {
+  asm volatile("bar.sync 4, 128;" ::: "memory");  // every GEMM thread's stores precede the release
   if (threadIdx.x == 0) {
     __threadfence();
     const unsigned long long target = (epoch + 1) * (unsigned long long)gridDim.x;
@@ -190,7 +205,7 @@ __device__ void dense_tile_fp64(const DenseArgs& a, int m0, int n0) {
     }
 #pragma unroll
     for (int j = 0; j < 16; ++j)
-      if (j < nmax) a.gt64[(int64_t)(n0 + nb + j) * a.D + m] = acc[j];
+      if (j < nmax && __ldcg(a.pending + n0 + nb + j) != 0ULL) a.gt64[(int64_t)(n0 + nb + j) * a.D + m] = acc[j];
   }
 }
 
@@ -198,7 +213,7 @@ __global__ void __launch_bounds__(128 + 32 * kDenseCW, 1)
     k_dense_op(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmX, DenseArgs a,
                int nslots, OpArgs A) {
   extern __shared__ __align__(1024) unsigned char dsm[];
-  volatile int* cmd = reinterpret_cast<volatile int*>(dsm + kUmmaSmemBytes);
+  volatile int* flag = reinterpret_cast<volatile int*>(dsm + kUmmaSmemBytes);
   SlotScalars* ss_all = reinterpret_cast<SlotScalars*>(dsm + kUmmaSmemBytes + 64);
   const int warp = threadIdx.x >> 5;
   if (warp < 4) {
@@ -208,29 +223,53 @@ __global__ void __launch_bounds__(128 + 32 * kDenseCW, 1)
       g.init(dsm);
       if (threadIdx.x == 0) { u_prefetch_tmap(&tmA); u_prefetch_tmap(&tmX); }
     }
+    const int t = threadIdx.x;
     const int mt = (a.D + kUmmaBM - 1) / kUmmaBM, nt = a.Cpad / kUmmaBN;
     const int nkb = (a.D + kUmmaBK - 1) / kUmmaBK;
     const int total = (int)gridDim.x * kDenseCW;
+    const int my_chain = blockIdx.x * kDenseCW + t;  // t < kDenseCW: this CTA's chain t
+    unsigned long long srv = 0;                      // requests of my_chain served so far
     unsigned long long epoch = 0;
-    const bool prof = a.prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
-    unsigned long long tp0 = 0, tp1 = 0;
+    const bool prof = a.prof != nullptr && blockIdx.x == 0 && t == 0;
+    unsigned long long tp0 = 0, tp1 = 0, busy = 0;
     if (prof) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tp0));
-    for (;;) {
-      cta_bar(2);  // every chain warp of this CTA has posted
-      gemm_grid_barrier(a.bar, epoch);  // ... and of every CTA
+    for (int step = 0;; ++step) {
+      // snapshot: requests outstanding now are served by this step
+      unsigned long long mine = 0;
+      if (t < kDenseCW) {
+        const unsigned long long p = ld_acquire_u64(a.posted + my_chain);
+        mine = p > srv ? p : 0ULL;
+        a.pending[my_chain] = mine;
+        if (mine) atomicAdd(a.npend + (step & 1), 1ULL);
+      }
+      gemm_grid_barrier(a.bar, epoch);
+      if (t == 0) {
+        const unsigned long long np = ld_relaxed_u64(a.npend + (step & 1));
+        *flag = (np == 0ULL && *reinterpret_cast<volatile int*>(a.done) >= total) ? 0 : (np ? 1 : 2);
+        if (blockIdx.x == 0) a.npend[(step + 1) & 1] = 0ULL;  // next slot: last read before this barrier
+      }
+      asm volatile("bar.sync 4, 128;" ::: "memory");
+      const int f = *flag;
+      if (f == 0) break;
       if (prof) {
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tp1));
         a.prof[0] += tp1 - tp0;
         tp0 = tp1;
       }
-      if (threadIdx.x == 0) *cmd = (*reinterpret_cast<volatile int*>(a.done) >= total) ? 0 : 1;
-      asm volatile("bar.sync 4, 128;" ::: "memory");
-      if (*cmd == 0) { cta_arrive(3); break; }
-      if (threadIdx.x == 0) asm volatile("fence.proxy.async.global;" ::: "memory");
-      for (int t = blockIdx.x; t < mt * nt; t += gridDim.x) {
-        const int m0 = (t % mt) * kUmmaBM, n0 = (t / mt) * kUmmaBN;
-        if (a.fp64) dense_tile_fp64(a, m0, n0);
-        else g.tile(&tmA, &tmX, m0, n0, nkb, a.gt, a.D, a.D - m0 < kUmmaBM ? a.D - m0 : kUmmaBM, kUmmaBN);
+      if (f == 1) {  // at least one request in the grid
+        if (t == 0) asm volatile("fence.proxy.async.global;" ::: "memory");
+        for (int tile = blockIdx.x; tile < mt * nt; tile += gridDim.x) {
+          const int m0 = (tile % mt) * kUmmaBM, n0 = (tile / mt) * kUmmaBN;
+          // skip N-tiles without outstanding requests (uniform over the 128 threads)
+          int any = 0;
+          for (int j = t; j < kUmmaBN; j += 128) any |= __ldcg(a.pending + n0 + j) != 0ULL;
+          any = gemm_sync_or(any);
+          if (!any) continue;
+          if (a.fp64) dense_tile_fp64(a, m0, n0);
+          else
+            g.tile(&tmA, &tmX, m0, n0, nkb, a.gt, a.D, a.D - m0 < kUmmaBM ? a.D - m0 : kUmmaBM, kUmmaBN, a.pending + n0);
+        }
+        busy += 1;
       }
       if (prof) {
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tp1));
@@ -238,28 +277,34 @@ __global__ void __launch_bounds__(128 + 32 * kDenseCW, 1)
         tp0 = tp1;
       }
       gemm_grid_barrier(a.bar, epoch);  // all gradient tiles written
+      if (t < kDenseCW && mine) {
+        srv = mine;
+        st_release_gpu_u64(a.served + my_chain, mine);
+      }
       if (prof) {
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tp1));
         a.prof[2] += tp1 - tp0;
         a.prof[3] += 1;
         tp0 = tp1;
       }
-      cta_arrive(3);
     }
+    if (prof) a.prof[4] = busy;
     if (!a.fp64) g.release();
     return;
   }
   // ---------------- chain warps
   const int cw = warp - 4;
   const int chain = blockIdx.x * kDenseCW + cw;
-  DenseW M;
-  M.D = a.D;
-  M.fp64 = a.fp64;
-  M.xt = a.xt; M.xt64 = a.xt64; M.gt = a.gt; M.gt64 = a.gt64;
-  M.chain = chain;
-  M.cmd = cmd;
   const int n_active = (A.op == OP_RUN) ? a.C : 1;
   if (chain < n_active) {
+    DenseW M;
+    M.D = a.D;
+    M.fp64 = a.fp64;
+    M.xt = a.xt; M.xt64 = a.xt64; M.gt = a.gt; M.gt64 = a.gt64;
+    M.posted = a.posted;
+    M.served = a.served;
+    M.seq = 0;
+    M.chain = chain;
     Engine<WarpTeam, DenseW> E;
     E.D = a.D;
     E.S.base = a.ws + (int64_t)chain * a.nv * a.D;
@@ -275,10 +320,8 @@ __global__ void __launch_bounds__(128 + 32 * kDenseCW, 1)
     do_op(E, A, A.op == OP_RUN ? chain : 0, chain == 0 || A.op == OP_RUN);
   }
   __syncwarp();
-  if ((threadIdx.x & 31) == 0) atomicAdd(a.done, 1);
   __threadfence();
-  while (!M.idle_step()) {
-  }
+  if ((threadIdx.x & 31) == 0) atomicAdd(a.done, 1);
 }
 
 int launch_dense(const ts_model* m, int nslots, OpArgs& A, int n_chains, cudaStream_t st) {
@@ -298,7 +341,7 @@ int launch_dense(const ts_model* m, int nslots, OpArgs& A, int n_chains, cudaStr
   TS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 128 + 32 * kDenseCW, smem));
   if ((int64_t)occ * nsm < grid) return set_err(TS_EUNSUPPORTED, "dense model: too many chains for one co-resident grid");
   // workspaces (grown on demand, owned by the model)
-  const size_t need = (size_t)Cpad * D * (m->fp64 ? 16 : 8) + (size_t)C * nv * D * 8 + 64;
+  const size_t need = (size_t)Cpad * D * (m->fp64 ? 16 : 8) + (size_t)C * nv * D * 8 + 64 + (size_t)Cpad * 24 + 64;
   if (mm->dws_size < need) {
     if (mm->dws) cudaFree(mm->dws);
     mm->dws = nullptr;
@@ -322,6 +365,11 @@ int launch_dense(const ts_model* m, int nslots, OpArgs& A, int n_chains, cudaStr
     a.gt = reinterpret_cast<float*>(p); p += (size_t)Cpad * D * 4;
   }
   a.ws = reinterpret_cast<double*>(p);
+  p += (size_t)C * nv * D * 8;
+  a.posted = reinterpret_cast<unsigned long long*>(p);
+  a.served = a.posted + Cpad;
+  a.pending = a.served + Cpad;
+  a.npend = a.pending + Cpad;
   a.a64 = m->params;
   CUtensorMap ta, tx;
   memset(&ta, 0, sizeof ta);
@@ -333,18 +381,19 @@ int launch_dense(const ts_model* m, int nslots, OpArgs& A, int n_chains, cudaStr
     if (rc) return rc;
   }
   TS_CUDA(cudaMemsetAsync(mm->dws, 0, 64, st));
+  TS_CUDA(cudaMemsetAsync(a.posted, 0, ((size_t)Cpad * 3 + 2) * sizeof(unsigned long long), st));
   const bool prof = getenv("TS_PROF") != nullptr;  // profiling aid: CTA-0 step phases to stderr
-  if (prof) a.prof = reinterpret_cast<unsigned long long*>(mm->dws + 16);
+  if (prof) a.prof = reinterpret_cast<unsigned long long*>(mm->dws + 16);  // 5 words in the zeroed header
   int ns = nslots;
   void* args[] = {&ta, &tx, &a, &ns, &A};
   TS_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3((unsigned)grid), dim3(128 + 32 * kDenseCW), args, smem, st));
   if (prof) {
-    unsigned long long h[4];
+    unsigned long long h[5];
     TS_CUDA(cudaMemcpyAsync(h, a.prof, sizeof h, cudaMemcpyDeviceToHost, st));
     TS_CUDA(cudaStreamSynchronize(st));
     const double n = h[3] ? (double)h[3] : 1.0;
-    fprintf(stderr, "TS_PROF dense steps=%llu us/step: chains (post wait) %.2f  GEMM %.2f  release barrier %.2f\n", h[3],
-            h[0] / n / 1e3, h[1] / n / 1e3, h[2] / n / 1e3);
+    fprintf(stderr, "TS_PROF dense steps=%llu (with requests %llu) us/step: snapshot+barrier %.2f  GEMM %.2f  release barrier %.2f\n",
+            h[3], h[4], h[0] / n / 1e3, h[1] / n / 1e3, h[2] / n / 1e3);
   }
   return TS_OK;
 }

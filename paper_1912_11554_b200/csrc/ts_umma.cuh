@@ -113,6 +113,22 @@ __device__ __forceinline__ void u_tmem_ld16(uint32_t taddr, float (&v)[16]) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// OR-reduction barrier over the 128 GEMM threads (named barrier 4)
+__device__ __forceinline__ int gemm_sync_or(int v) {
+  int r;
+  asm volatile(
+      "{\n"
+      ".reg .pred p, q;\n"
+      "setp.ne.s32 p, %1, 0;\n"
+      "bar.red.or.pred q, 4, 128, p;\n"
+      "selp.s32 %0, 1, 0, q;\n"
+      "}\n"
+      : "=r"(r)
+      : "r"(v)
+      : "memory");
+  return r;
+}
+
 // Persistent-GEMM state of one CTA's 4 GEMM warps (warps 0..3 of the CTA).
 struct UmmaGemm {
   unsigned char* ring;  // 1024-B aligned: kUmmaStages x (A tile | B tile)
@@ -155,8 +171,9 @@ struct UmmaGemm {
 
   // One 128 x 64 output tile: rows m0.., chains n0..; nkb k-blocks.
   // Output GT[(n0 + j) * ldo + m0 + i] for i < m_valid, j < n_valid.
+  // pend (optional): output column j is stored only if pend[j] != 0.
   __device__ void tile(const void* tmA, const void* tmB, int m0, int n0, int nkb, float* GT, int64_t ldo, int m_valid,
-                       int n_valid) {
+                       int n_valid, const unsigned long long* pend = nullptr) {
     const int t = threadIdx.x;
     const uint32_t idesc = u_idesc_tf32(kUmmaBM, kUmmaBN);
     if (t == 0) {
@@ -202,7 +219,8 @@ struct UmmaGemm {
       if (row < m_valid) {
 #pragma unroll
         for (int j = 0; j < 16; ++j)
-          if (c + j < n_valid) GT[(int64_t)(n0 + c + j) * ldo + m0 + row] = v[j];
+          if (c + j < n_valid && (pend == nullptr || __ldcg(pend + c + j) != 0ULL))
+            GT[(int64_t)(n0 + c + j) * ldo + m0 + row] = v[j];
       }
     }
     u_fence_before();

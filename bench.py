@@ -420,7 +420,7 @@ def run_dense(args):
             "metric": "leapfrog_steps_per_sec", "value": lf / (t_ms / 1000.0), "unit": "chain-leapfrog/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": prec, "data": "synthetic",
-            "config": {"workload": f"1000-D correlated Gaussian, dense mass, {C} chains in lockstep, "
+            "config": {"workload": f"1000-D correlated Gaussian, dense mass, {C} chains, batched tcgen05 gradient steps, "
                                    f"{args.num_warmup}+{args.num_samples} draws", "parallelism": f"chains{world}"},
             "lockstep_steps_per_run": sum(steps) / args.steps, "us_per_lockstep_step": 1e3 * sum(times) / sum(steps),
             "roofline": {"bound": "tensor", "achieved": tflops, "peak": peak, "unit": "TFLOP/s", "frac": tflops / peak,

@@ -328,7 +328,18 @@ __device__ __forceinline__ void row_from_stage(const unsigned char* sb, int p_rt
 // Per-CTA streaming pass.  Writes this CTA's partial sums
 // red_out[0..p) = sum resid*x_j, red_out[p] = sum resid, red_out[p+1] = sum (y eta - log1pexp)
 // (wred: >= nwarps*(PMAX+2) doubles of scratch).
-template <int PMAX, bool FP64, int PE>
+// fp32 -> fp64 on the integer pipe (normal numbers and zeros only: callers
+// use it when X holds no fp32 subnormals, LogisticArgs::exact_cvt == 0).
+__device__ __forceinline__ double f2d_alu(float f) {
+  const uint32_t u = __float_as_uint(f);
+  const uint32_t mag = u & 0x7fffffffu;
+  const uint32_t hi = (u & 0x80000000u) | ((mag >> 3) + (mag ? 0x38000000u : 0u));
+  return __hiloint2double((int)hi, (int)(u << 29));
+}
+
+// MIX: half of the conversions (odd features) on the integer pipe, half on
+// the XU (F2F), which alone bounds the FP64 policy.
+template <int PMAX, bool FP64, int PE, bool MIX = false>
 __device__ __noinline__ void logistic_cta_pass(const LogisticArgs& a, const double* __restrict__ theta_s, double* wred,
                                                   double* red_out) {
   const int lane = threadIdx.x & 31, warp = wk_warp(), nwarps = wk_nwarps();
@@ -397,13 +408,16 @@ __device__ __noinline__ void logistic_cta_pass(const LogisticArgs& a, const doub
         // The fp32 -> fp64 conversions (F2F, ~4/clk/SM on the XU pipe) bound
         // this variant: ncu shows XU ~95% busy, FP64 ~17%.  An integer-ALU
         // conversion (6 instructions per element) measured slower.
+        double xd[PMAX];
+#pragma unroll
+        for (int k = 0; k < PMAX; ++k) xd[k] = (MIX && (k & 1)) ? f2d_alu(x[k]) : (double)x[k];
         double e0 = theta_s[p], e1 = 0.0, e2 = 0.0, e3 = 0.0;
 #pragma unroll
         for (int k = 0; k < PMAX; k += 4) {
-          e0 = __fma_rn((double)x[k], (k < p) ? theta_s[k] : 0.0, e0);
-          e1 = __fma_rn((double)x[k + 1], (k + 1 < p) ? theta_s[k + 1] : 0.0, e1);
-          e2 = __fma_rn((double)x[k + 2], (k + 2 < p) ? theta_s[k + 2] : 0.0, e2);
-          e3 = __fma_rn((double)x[k + 3], (k + 3 < p) ? theta_s[k + 3] : 0.0, e3);
+          e0 = __fma_rn(xd[k], (k < p) ? theta_s[k] : 0.0, e0);
+          e1 = __fma_rn(xd[k + 1], (k + 1 < p) ? theta_s[k + 1] : 0.0, e1);
+          e2 = __fma_rn(xd[k + 2], (k + 2 < p) ? theta_s[k + 2] : 0.0, e2);
+          e3 = __fma_rn(xd[k + 3], (k + 3 < p) ? theta_s[k + 3] : 0.0, e3);
         }
         const double eta = (e0 + e1) + (e2 + e3);
         const double e = exp(-fabs(eta));
@@ -413,7 +427,7 @@ __device__ __noinline__ void logistic_cta_pass(const LogisticArgs& a, const doub
         const double resid = valid ? yv - sig : 0.0;
         accl += valid ? (yv * eta - l) : 0.0;
 #pragma unroll
-        for (int k = 0; k < PMAX; ++k) acc[k] = __fma_rn(resid, (double)x[k], acc[k]);
+        for (int k = 0; k < PMAX; ++k) acc[k] = __fma_rn(resid, xd[k], acc[k]);
         acc[PMAX] += resid;
       } else {
         float e0 = thb32, e1 = 0.f, e2 = 0.f, e3 = 0.f;
@@ -785,7 +799,8 @@ static __device__ __forceinline__ void logistic_cta_dispatch(const LogisticArgs&
     return;
   }
   if (a.p == 54) {  // covtype's feature count: compile-time row layout
-    if (a.fp64) logistic_cta_pass<56, true, 54>(a, theta, wred, red_s);
+    if (a.fp64 && !a.exact_cvt) logistic_cta_pass<56, true, 54, true>(a, theta, wred, red_s);
+    else if (a.fp64) logistic_cta_pass<56, true, 54>(a, theta, wred, red_s);
     else logistic_cta_pass<56, false, 54>(a, theta, wred, red_s);
     return;
   }

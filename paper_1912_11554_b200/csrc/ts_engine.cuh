@@ -169,6 +169,39 @@ static __device__ __noinline__ void warp_gen_uturn2(const double2* __restrict__ 
   ab[1] = b;
 }
 __device__ __forceinline__ bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+// up to 5 vector copies in one pass (k pairs), 2 x double2 per operand in flight
+static __device__ __noinline__ void warp_copy_multi(double2* __restrict__ d0, const double2* __restrict__ s0,
+                                                    double2* __restrict__ d1, const double2* __restrict__ s1,
+                                                    double2* __restrict__ d2, const double2* __restrict__ s2,
+                                                    double2* __restrict__ d3, const double2* __restrict__ s3,
+                                                    double2* __restrict__ d4, const double2* __restrict__ s4, int k,
+                                                    int n2) {
+  for (int base = (int)(threadIdx.x & 31); base < n2; base += 32 * 2) {
+    double2 t[5][2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int i = base + 32 * u;
+      if (i < n2) {
+        t[0][u] = s0[i];
+        t[1][u] = s1[i];
+        t[2][u] = s2[i];
+        if (k > 3) t[3][u] = s3[i];
+        if (k > 4) t[4][u] = s4[i];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int i = base + 32 * u;
+      if (i < n2) {
+        d0[i] = t[0][u];
+        d1[i] = t[1][u];
+        d2[i] = t[2][u];
+        if (k > 3) d3[i] = t[3][u];
+        if (k > 4) d4[i] = t[4][u];
+      }
+    }
+  }
+}
 
 enum Stop : int { kStopNone = 0, kStopTurn = 1, kStopDiv = 2 };
 
@@ -268,7 +301,7 @@ struct Engine {
       if (S.slots != nullptr && id >= S.slot0) return S.slots + (id - S.slot0) * (int)S.vstride;
       return S.base + id * (int)S.vstride;
     } else {
-      return S.v(id);
+      return S.base + (int64_t)id * S.vstride;  // thread teams never use the slot region
     }
   }
   __device__ __forceinline__ int64_t ds() const {
@@ -307,6 +340,33 @@ struct Engine {
     }
     const int64_t s = ds();
     for (int d = T.rank(); d < D; d += T.size()) a[d * s] = b[d * s];
+  }
+  // 3 or 5 copies (d3 < 0: three); one fused pass for large-D warp vectors
+  __device__ void copy_group(int d0, int s0, int d1, int s1, int d2, int s2, int d3 = -1, int s3 = -1, int d4 = -1,
+                             int s4 = -1) {
+    if constexpr (Team::kWarp && Team::kUnitStride && Model::kVecOps) {
+      const int k = d3 < 0 ? 3 : 5;
+      double* a[5] = {v(d0), v(d1), v(d2), k > 3 ? v(d3) : v(d0), k > 3 ? v(d4) : v(d0)};
+      const double* b[5] = {v(s0), v(s1), v(s2), k > 3 ? v(s3) : v(s0), k > 3 ? v(s4) : v(s0)};
+      bool ok = D >= 128 && (D & 1) == 0;
+#pragma unroll
+      for (int i = 0; i < 5; ++i) ok = ok && al16(a[i]) && al16(b[i]);
+      if (ok) {
+        warp_copy_multi(reinterpret_cast<double2*>(a[0]), reinterpret_cast<const double2*>(b[0]),
+                        reinterpret_cast<double2*>(a[1]), reinterpret_cast<const double2*>(b[1]),
+                        reinterpret_cast<double2*>(a[2]), reinterpret_cast<const double2*>(b[2]),
+                        reinterpret_cast<double2*>(a[3]), reinterpret_cast<const double2*>(b[3]),
+                        reinterpret_cast<double2*>(a[4]), reinterpret_cast<const double2*>(b[4]), k, D >> 1);
+        return;
+      }
+    }
+    copy(d0, s0);
+    copy(d1, s1);
+    copy(d2, s2);
+    if (d3 >= 0) {
+      copy(d3, s3);
+      copy(d4, s4);
+    }
   }
   __device__ __forceinline__ void fill(int dst, double x) {
     double* a = v(dst);
@@ -405,8 +465,7 @@ struct Engine {
 
   // ------------------------------------------------------- tree builder
   __device__ void running_from_leaf(int n, double lw, double metro, double h) {
-    copy(V_FQ, V_CQ); copy(V_FR, V_CR); copy(V_CUMF, V_CUM);
-    copy(V_TPQ, V_CQ); copy(V_TPG, V_CG);
+    copy_group(V_FQ, V_CQ, V_FR, V_CR, V_CUMF, V_CUM, V_TPQ, V_CQ, V_TPG, V_CG);
     r_lw = lw; r_metro = metro; r_count = 1; r_pU = cur_U; r_pH = h; r_pidx = n; r_fU = cur_U;
   }
 
@@ -416,10 +475,12 @@ struct Engine {
     const double lw = logaddexp_inner(L.lw, r_lw);
     const double p_right = (r_lw == -kInf()) ? 0.0 : exp(__dsub_rn(r_lw, lw));
     if (!(u < p_right)) {
-      copy(V_TPQ, slot_vec(s, 3)); copy(V_TPG, slot_vec(s, 4));
+      copy_group(V_FQ, slot_vec(s, 0), V_FR, slot_vec(s, 1), V_CUMF, slot_vec(s, 2), V_TPQ, slot_vec(s, 3), V_TPG,
+                 slot_vec(s, 4));
       r_pU = L.pU; r_pH = L.pH; r_pidx = L.pidx;
+    } else {
+      copy_group(V_FQ, slot_vec(s, 0), V_FR, slot_vec(s, 1), V_CUMF, slot_vec(s, 2));
     }
-    copy(V_FQ, slot_vec(s, 0)); copy(V_FR, slot_vec(s, 1)); copy(V_CUMF, slot_vec(s, 2));
     r_fU = L.fU;
     r_lw = lw;
     r_count = L.count + r_count;
@@ -591,8 +652,8 @@ struct Engine {
     ev_lw(lw);
     if ((n & 1ULL) == 0) {
       const int slot = pc;
-      copy(slot_vec(slot, 0), V_CQ); copy(slot_vec(slot, 1), V_CR); copy(slot_vec(slot, 2), V_CUM);
-      copy(slot_vec(slot, 3), V_CQ); copy(slot_vec(slot, 4), V_CG);
+      copy_group(slot_vec(slot, 0), V_CQ, slot_vec(slot, 1), V_CR, slot_vec(slot, 2), V_CUM, slot_vec(slot, 3), V_CQ,
+                 slot_vec(slot, 4), V_CG);
       SlotScalars& L = ss[slot];
       L.lw = lw; L.metro = metro; L.pU = cur_U; L.pH = h; L.fU = cur_U;
       L.count = 1; L.pidx = (int)n; L.leaf = (int)n;

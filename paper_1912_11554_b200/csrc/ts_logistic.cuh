@@ -328,18 +328,7 @@ __device__ __forceinline__ void row_from_stage(const unsigned char* sb, int p_rt
 // Per-CTA streaming pass.  Writes this CTA's partial sums
 // red_out[0..p) = sum resid*x_j, red_out[p] = sum resid, red_out[p+1] = sum (y eta - log1pexp)
 // (wred: >= nwarps*(PMAX+2) doubles of scratch).
-// fp32 -> fp64 on the integer pipe (normal numbers and zeros only: callers
-// use it when X holds no fp32 subnormals, LogisticArgs::exact_cvt == 0).
-__device__ __forceinline__ double f2d_alu(float f) {
-  const uint32_t u = __float_as_uint(f);
-  const uint32_t mag = u & 0x7fffffffu;
-  const uint32_t hi = (u & 0x80000000u) | ((mag >> 3) + (mag ? 0x38000000u : 0u));
-  return __hiloint2double((int)hi, (int)(u << 29));
-}
-
-// MIX: half of the conversions (odd features) on the integer pipe, half on
-// the XU (F2F), which alone bounds the FP64 policy.
-template <int PMAX, bool FP64, int PE, bool MIX = false>
+template <int PMAX, bool FP64, int PE>
 __device__ __noinline__ void logistic_cta_pass(const LogisticArgs& a, const double* __restrict__ theta_s, double* wred,
                                                   double* red_out) {
   const int lane = threadIdx.x & 31, warp = wk_warp(), nwarps = wk_nwarps();
@@ -407,10 +396,11 @@ __device__ __noinline__ void logistic_cta_pass(const LogisticArgs& a, const doub
         // and reused for eta and for the gradient
         // The fp32 -> fp64 conversions (F2F, ~4/clk/SM on the XU pipe) bound
         // this variant: ncu shows XU ~95% busy, FP64 ~17%.  An integer-ALU
-        // conversion (6 instructions per element) measured slower.
+        // conversion (6 instructions per element) measured slower, for all
+        // elements and for every second one (47.4 vs 42.7 us per pass).
         double xd[PMAX];
 #pragma unroll
-        for (int k = 0; k < PMAX; ++k) xd[k] = (MIX && (k & 1)) ? f2d_alu(x[k]) : (double)x[k];
+        for (int k = 0; k < PMAX; ++k) xd[k] = (double)x[k];
         double e0 = theta_s[p], e1 = 0.0, e2 = 0.0, e3 = 0.0;
 #pragma unroll
         for (int k = 0; k < PMAX; k += 4) {
@@ -799,8 +789,7 @@ static __device__ __forceinline__ void logistic_cta_dispatch(const LogisticArgs&
     return;
   }
   if (a.p == 54) {  // covtype's feature count: compile-time row layout
-    if (a.fp64 && !a.exact_cvt) logistic_cta_pass<56, true, 54, true>(a, theta, wred, red_s);
-    else if (a.fp64) logistic_cta_pass<56, true, 54>(a, theta, wred, red_s);
+    if (a.fp64) logistic_cta_pass<56, true, 54>(a, theta, wred, red_s);
     else logistic_cta_pass<56, false, 54>(a, theta, wred, red_s);
     return;
   }

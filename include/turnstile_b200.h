@@ -122,6 +122,14 @@ int ts_transition(const ts_model* m, const ts_sampler_cfg* cfg, const double* in
                   const double* normals_or_null, uint64_t key_hi, uint64_t key_lo, double* out, int32_t* trace_ev,
                   int trace_cap, int32_t* trace_counts, int exec_mode, void* stream);
 
+/* Replaces sampler.hmc_transition (sampler.py:163-203): num_steps leapfrogs of
+ * cfg->step_size, then Metropolis accept with fold(key, 1).random().  z_in as
+ * for ts_transition.  out [2*dim + 7]: q, grad, U (the kept state), depth (0),
+ * leapfrogs, diverged, accept_stat, energy, accepted. */
+int ts_hmc_transition(const ts_model* m, const ts_sampler_cfg* cfg, const double* inv_dev, const double* z_in,
+                      const double* normals_or_null, uint64_t key_hi, uint64_t key_lo, int num_steps, double* out,
+                      int exec_mode, void* stream);
+
 /* Replaces adapt.find_reasonable_step_size (adapt.py:172-204). out[1]. */
 int ts_find_step_size(const ts_model* m, const double* inv_dev, const double* z_in, const double* normals_or_null,
                       uint64_t key_hi, uint64_t key_lo, double init, double* out, int exec_mode, void* stream);

@@ -176,6 +176,14 @@ def build_c():
                            "-lm"])
 
 
+def _exp(x):
+    """exp with IEEE overflow to +inf (numba's math.exp; Python's raises)."""
+    try:
+        return math.exp(x)
+    except OverflowError:
+        return math.inf
+
+
 @dataclass
 class Model:
     """Oracle model: kind + parameters; potential/gradient restate kernels.py."""
@@ -228,7 +236,7 @@ class Model:
             ssq = 0.0
             for x in q[1:]:
                 ssq += x * x
-            return v * v / 18.0 + 0.5 * (len(q) - 1) * v + 0.5 * math.exp(-v) * ssq
+            return v * v / 18.0 + 0.5 * (len(q) - 1) * v + 0.5 * _exp(-v) * ssq
         if k == "eight_schools":
             return eight_schools_potential(q, self.es_y, self.es_s)
         if k == "dense_gaussian":
@@ -250,7 +258,7 @@ class Model:
             return [v * iv for v, iv in zip(q, self.inv_var)]
         if k == "funnel":
             v = q[0]
-            inv_scale = math.exp(-v)
+            inv_scale = _exp(-v)
             out = [0.0] * len(q)
             ssq = 0.0
             for i in range(1, len(q)):
@@ -591,6 +599,34 @@ def transition(z0: Point, step, inv, model, key, max_depth=10, generalized=True,
 
 
 # ----------------------------------------------------------------------------- adaptation / run
+
+
+def hmc_transition(q, step, inv, model, key, num_steps, threshold=1000.0, normals=None):
+    """sampler.hmc_transition (sampler.py:163-203): returns (q, Stats, accepted)."""
+    if num_steps < 1:
+        raise ValueError("num_steps must be >= 1")
+    D = len(q)
+    if normals is None:
+        ns = Stream(key_fold(key, 0))
+        normals = [ns.normal() for _ in range(D)]
+    mstd = (1.0 / np.sqrt(np.asarray(inv, dtype=np.float64))).tolist()
+    r0 = [a * b for a, b in zip(normals, mstd)]
+    z = Point(list(q), r0, model.potential(list(q)), model.gradient(list(q)))
+    h0 = hamiltonian(z.U, z.r, inv)
+    z_new = z
+    steps = 0
+    for _ in range(num_steps):
+        z_new = leapfrog(z_new, step, inv, model)
+        steps += 1
+        if not math.isfinite(z_new.U):
+            break
+    h1 = hamiltonian(z_new.U, z_new.r, inv)
+    delta = h1 - h0
+    p_accept = math.exp(-delta) if math.isfinite(delta) and delta > 0 else (1.0 if math.isfinite(delta) else 0.0)
+    accept = Stream(key_fold(key, 1)).random() < p_accept
+    res = z_new if accept else z
+    st = Stats(0, steps, (not math.isfinite(delta)) or delta > threshold, p_accept, hamiltonian(res.U, res.r, inv))
+    return (list(z_new.q) if accept else list(q)), st, accept
 
 
 def find_step_size(z: Point, inv, model, key, init=1.0, target=0.5, normals=None):

@@ -387,6 +387,19 @@ extern "C" int ts_transition(const ts_model* m, const ts_sampler_cfg* cfg, const
   return launch(m, cfg->max_tree_depth - 1, A, 1, (ts_exec_mode)exec_mode, (cudaStream_t)stream);
 }
 
+extern "C" int ts_hmc_transition(const ts_model* m, const ts_sampler_cfg* cfg, const double* inv_dev, const double* z_in,
+                                 const double* normals_or_null, uint64_t key_hi, uint64_t key_lo, int num_steps,
+                                 double* out, int exec_mode, void* stream) {
+  if (!m || !inv_dev || !z_in || !out) return set_err(TS_EINVAL, "null argument");
+  if (num_steps < 1) return set_err(TS_EINVAL, "num_steps must be >= 1");
+  int rc = check_cfg(cfg);
+  if (rc) return rc;
+  OpArgs A = base_args(OP_HMC);
+  A.z_in = z_in; A.z_out = out; A.inv = inv_dev; A.cfg = to_cfg(cfg);
+  A.key_hi = key_hi; A.key_lo = key_lo; A.inj = normals_or_null; A.depth = num_steps;
+  return launch(m, 1, A, 1, (ts_exec_mode)exec_mode, (cudaStream_t)stream);
+}
+
 extern "C" int ts_find_step_size(const ts_model* m, const double* inv_dev, const double* z_in, const double* normals_or_null,
                                  uint64_t key_hi, uint64_t key_lo, double init, double* out, int exec_mode, void* stream) {
   if (!m || !inv_dev || !z_in || !out) return set_err(TS_EINVAL, "null argument");

@@ -828,6 +828,35 @@ struct Engine {
   }
 
   // nuts_transition_from (sampler.py:83-148): z0 = (Q0, G0, U0) -> proposal
+  // sampler.hmc_transition (sampler.py:163-203): fixed-length HMC baseline.
+  // State in (Q0, G0, U0); momentum from fold(key, 0), accept uniform from
+  // fold(key, 1).  On acceptance (Q0, G0, U0) move to the trajectory end.
+  __device__ __noinline__ Stats hmc(Key key, const double* inj, int64_t inj_ds, int num_steps, bool& accepted) {
+    draw_momentum(V_R0, key_fold(key, 0), inj, inj_ds);
+    const double h0 = hamiltonian(U0, V_R0);
+    copy(V_CQ, V_Q0); copy(V_CR, V_R0); copy(V_CG, V_G0); cur_U = U0;
+    int steps = 0;
+    for (int i = 0; i < num_steps; ++i) {
+      leapfrog(cfg.step);
+      steps += 1;
+      if (!isfinite(cur_U)) break;
+    }
+    const double h1 = hamiltonian(cur_U, V_CR);
+    const double delta = __dsub_rn(h1, h0);
+    const double p_accept = (isfinite(delta) && delta > 0) ? exp(-delta) : (isfinite(delta) ? 1.0 : 0.0);
+    Stream gen;
+    gen.init(key_fold(key, 1));
+    accepted = gen.next_double() < p_accept;
+    if (accepted) { copy(V_Q0, V_CQ); copy(V_G0, V_CG); U0 = cur_U; }
+    Stats st;
+    st.depth = 0;
+    st.leapfrogs = steps;
+    st.diverged = !isfinite(delta) || delta > cfg.threshold;
+    st.accept = p_accept;
+    st.energy = accepted ? h1 : h0;
+    return st;
+  }
+
   __device__ __noinline__ Stats transition(Key key, const double* inj, int64_t inj_ds) {
     draw_momentum(V_R0, key_fold(key, 0), inj, inj_ds);
     const double h0 = hamiltonian(U0, V_R0);

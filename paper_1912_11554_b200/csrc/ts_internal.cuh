@@ -52,7 +52,8 @@ int set_err(int code, const char* msg);
 
 
 // ------------------------------------------------------------------ op args
-enum OpCode : int { OP_POTGRAD = 0, OP_LEAPFROG = 1, OP_TREE = 2, OP_TRANSITION = 3, OP_STEPSEARCH = 4, OP_RUN = 5, OP_EVALBENCH = 6 };
+enum OpCode : int { OP_POTGRAD = 0, OP_LEAPFROG = 1, OP_TREE = 2, OP_TRANSITION = 3, OP_STEPSEARCH = 4, OP_RUN = 5, OP_EVALBENCH = 6,
+                    OP_HMC = 7 };
 
 struct OpArgs {
   int op;
@@ -216,6 +217,22 @@ __device__ void do_op(Engine<Team, Model>& E, const OpArgs& A, int chain, bool w
           double* o = A.z_out + 2 * (int64_t)D;
           o[0] = E.U0; o[1] = st.depth; o[2] = st.leapfrogs; o[3] = st.diverged; o[4] = st.accept; o[5] = st.energy;
           o[6] = E.p_tree; o[7] = E.p_leaf;
+        }
+      }
+      break;
+    }
+    case OP_HMC: {
+      double* q = E.v(V_Q0); double* g = E.v(V_G0);
+      for (int d = rk; d < D; d += sz) { q[d * s] = A.z_in[d]; g[d * s] = A.z_in[2 * D + d]; }
+      E.U0 = A.z_in[3 * D];
+      bool acc = false;
+      const Stats st = E.hmc(Key{A.key_hi, A.key_lo}, A.inj, 1, A.depth, acc);
+      if (writer) {
+        for (int d = rk; d < D; d += sz) { A.z_out[d] = q[d * s]; A.z_out[D + d] = g[d * s]; }
+        if (E.T.leader()) {
+          double* o = A.z_out + 2 * (int64_t)D;
+          o[0] = E.U0; o[1] = st.depth; o[2] = st.leapfrogs; o[3] = st.diverged; o[4] = st.accept; o[5] = st.energy;
+          o[6] = acc ? 1.0 : 0.0;
         }
       }
       break;

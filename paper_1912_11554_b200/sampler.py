@@ -140,6 +140,35 @@ def nuts_transition(q: np.ndarray, config: SamplerConfig, model: TargetModel, rn
     return z_new.position, stats
 
 
-def hmc_transition(q, config, model, rng, num_steps):
-    """Fixed-length HMC is outside the NUTS hot path."""
-    raise NotImplementedError("hmc_transition is not part of the device NUTS path")
+def hmc_transition(q, config: SamplerConfig, model: TargetModel, rng: RngKey, num_steps: int, normals=None,
+                   device=None, exec_mode=None):
+    """Fixed-length HMC baseline (sampler.py:163-203), on the device:
+    ``num_steps`` leapfrogs then accept/reject.  Returns (position, stats)."""
+    if num_steps < 1:
+        raise ValueError("num_steps must be >= 1")
+    if not isinstance(rng, RngKey):
+        raise ValueError("rng must be an RngKey")
+    spec = require_device(model)
+    torch = _lib.torch_cuda()
+    dev = _lib.cuda_device(torch, device)
+    h = spec.handle(dev)
+    D = model.dim
+    q = np.asarray(q, dtype=np.float64)
+    z0 = PhasePoint.from_position(model, q, np.zeros(D))
+    zin = torch.from_numpy(pack(z0)).to(dev)
+    inv = torch.from_numpy(config.mass.inv_diag).to(dev)
+    nrm = None
+    if normals is not None:
+        nrm = torch.from_numpy(np.ascontiguousarray(normals, dtype=np.float64).ravel()).to(dev)
+        if nrm.numel() != D:
+            raise ValueError("normals must have the model dimension")
+    out = torch.empty(2 * D + 7, dtype=torch.float64, device=dev)
+    lib = _lib.load_library()
+    with torch.cuda.device(dev):
+        _lib.check(lib.ts_hmc_transition(h, sampler_cfg_c(config), _lib.ptr(inv), _lib.ptr(zin), _lib.ptr(nrm), rng.hi,
+                                         rng.lo, int(num_steps), _lib.ptr(out), exec_mode_for(model, exec_mode),
+                                         _lib.stream_ptr(torch)))
+    o = out.cpu().numpy()
+    s = o[2 * D:]
+    stats = TransitionStats(int(s[1]), int(s[2]), bool(s[3]), float(s[4]), float(s[5]))
+    return (o[:D].copy() if s[6] != 0 else q), stats

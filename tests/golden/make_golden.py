@@ -14,6 +14,7 @@ its default (numba) kernel path.  Outputs, committed under tests/golden/:
   runs.json         full run() results (samples, stats, adaptation) for small
                     models, incl. eight-schools through the TargetModel plugin API
   logistic.json     logistic potential/gradient at fixed points (fp32-exact data)
+  hmc.json          hmc_transition chains (fixed-length HMC baseline, sampler.py:163-203)
 Nothing here is read by the GPU box at run time except these JSON files.
 """
 
@@ -318,9 +319,34 @@ def gen_rng():
     return out
 
 
+def gen_hmc():
+    """sampler.hmc_transition (sampler.py:163-203) on small models: chains of
+    fixed-length HMC draws (accept/reject, stats) from fixed seeds."""
+    out = []
+    models = [std_normal_model(5), gaussian_model(np.logspace(-1, 1, 6)), funnel_model(4)]
+    for mi, model in enumerate(models):
+        for steps, eps in ((1, 0.3), (7, 0.25), (20, 0.9)):
+            cfg = SamplerConfig(step_size=eps, mass=MassMatrix.identity(model.dim))
+            q = np.linspace(-1.0, 1.2, model.dim)
+            base = RngKey.from_seed(900 + 10 * mi + steps)
+            draws = []
+            for i in range(6):
+                key = base.fold(i)
+                q_new, st = tsampler.hmc_transition(q, cfg, model, key, steps)
+                draws.append({"key": [str(key.hi), str(key.lo)], "q_in": fl(q), "q_out": fl(q_new),
+                              "leapfrogs": st.leapfrog_calls, "diverged": bool(st.diverged),
+                              "accept_stat": f(st.accept_stat), "energy": f(st.energy)})
+                q = q_new
+            out.append({"model": model_desc(model), "step": eps, "num_steps": steps, "draws": draws})
+    return out
+
+
 def main():
+    only = sys.argv[1:]
     for name, fn in (("rng", gen_rng), ("trees", gen_trees), ("transitions", gen_transitions), ("runs", gen_runs),
-                     ("logistic", gen_logistic)):
+                     ("logistic", gen_logistic), ("hmc", gen_hmc)):
+        if only and name not in only:
+            continue
         data = fn()
         with open(os.path.join(OUT, f"{name}.json"), "w") as fh:
             json.dump(data, fh)

@@ -632,3 +632,23 @@ def test_dense_mass_reparametrisation():
     flat = r.samples.cpu().numpy().reshape(-1, D)
     emp = np.cov(flat.T)
     assert np.abs(emp - cov).max() <= 0.15 * np.abs(cov).max()
+
+
+# ----------------------------------------------------------------------------- HMC baseline
+
+
+def test_hmc_transition_matches_reference():
+    """Device hmc_transition (sampler.py:163-203) vs the reference's draws:
+    accept decisions and leapfrog counts exact, floats at the thread-team
+    tolerance."""
+    t = ts()
+    for case in golden("hmc"):
+        m = device_model(case["model"])
+        cfg = t.SamplerConfig(step_size=num(case["step"]), mass=t.MassMatrix.identity(m.dim))
+        for d in case["draws"]:
+            key = t.RngKey(int(d["key"][0]), int(d["key"][1]))
+            q, st = t.hmc_transition(np.asarray(nums(d["q_in"])), cfg, m, key, case["num_steps"])
+            assert st.leapfrog_calls == d["leapfrogs"] and st.diverged == d["diverged"]
+            assert close(q, nums(d["q_out"]), SMALL_REL, atol=SMALL_REL)
+            assert close(st.accept_stat, num(d["accept_stat"]), SMALL_REL)
+            assert close(st.energy, num(d["energy"]), SMALL_REL)

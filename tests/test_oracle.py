@@ -166,3 +166,16 @@ def test_logistic_omp_close_to_sequential(oracle):
     g = np.asarray(m.gradient(q.tolist()))
     assert abs(out[0] - U) <= 1e-10 * abs(U)
     assert np.allclose(out[1:], g, rtol=1e-9, atol=1e-9)
+
+
+def test_hmc_golden_bitwise(oracle):
+    """Oracle restatement of sampler.hmc_transition vs the reference's own draws."""
+    for case in golden("hmc"):
+        m = oracle.model_from_desc(case["model"])
+        inv = [1.0] * m.dim
+        for d in case["draws"]:
+            key = (int(d["key"][0]), int(d["key"][1]))
+            q, st, _ = oracle.hmc_transition(nums(d["q_in"]), num(case["step"]), inv, m, key, case["num_steps"])
+            assert q == nums(d["q_out"])
+            assert st.leapfrogs == d["leapfrogs"] and st.diverged == d["diverged"]
+            assert st.accept == num(d["accept_stat"]) and st.energy == num(d["energy"])

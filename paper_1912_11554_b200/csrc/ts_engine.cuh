@@ -42,8 +42,6 @@ __host__ __device__ inline int num_vecs(int nslots) { return V_SLOT0 + kSlotVecs
 // shared-memory scratch of a team (doubles): 64 for reductions / commands,
 // then the NodeStore scalars (kMaxSlots SlotScalars)
 constexpr int kTeamScratch = 64 + (kMaxSlots * 56 + 7) / 8;
-// shared-memory slot per driver-warp lane for its Engine object (grid mode)
-constexpr int kEngineSlotBytes = 1024;
 __device__ __forceinline__ int slot_vec(int s, int k) { return V_SLOT0 + kSlotVecs * s + k; }
 
 // Warp copy of n2 double2 (lane-strided, 8 loads in flight per lane).  A

@@ -21,8 +21,6 @@ int launch_block_logistic(const ts_model* m, int nslots, OpArgs& A, cudaStream_t
   mw.a.prof = m->prof;
   mw.a.exact_cvt = m->exact_cvt;
   mw.a.dump = m->dump;
-  mw.a.nrep = 4;
-  if (const char* e = getenv("TS_NREP")) mw.a.nrep = atoi(e) < 1 ? 1 : (atoi(e) > 8 ? 8 : atoi(e));  // profiling
   if (m->world > 0) {
     mw.a.world = m->world;
     mw.a.rank = m->rank;
@@ -53,8 +51,6 @@ int launch_block_logistic(const ts_model* m, int nslots, OpArgs& A, cudaStream_t
     return set_err(TS_EUNSUPPORTED, "logistic model: shared memory too small for D / max_tree_depth");
   mw.a.nstage = nstage;
   mw.a.stage_bytes = stage_bytes;
-  if (const char* e = getenv("TS_L2_PREFETCH")) mw.a.l2_prefetch = atoi(e);
-  if (const char* e = getenv("TS_L2_KEEP_FRAC")) mw.a.l2_keep_tiles = (int)(atof(e) * (double)m->ntiles);
   const size_t smem = need(nstage);
   auto kern = k_block_op<LogisticW>;
   TS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -78,8 +74,8 @@ int launch_block_logistic(const ts_model* m, int nslots, OpArgs& A, cudaStream_t
     mw.a.slotws = mm->slotws;
   }
   TS_CUDA(cudaMemsetAsync(m->bar, 0, sizeof(unsigned long long), st));
-  // rotating fixed-point accumulators start at zero (3 x nrep x (2*(p+2) + 2) words)
-  TS_CUDA(cudaMemsetAsync(m->pbuf, 0, 3 * (size_t)mw.a.nrep * (2 * (size_t)(m->p + 2) + 2) * sizeof(unsigned long long), st));
+  // rotating fixed-point accumulators start at zero (3 x (2*(p+2) + 2) words)
+  TS_CUDA(cudaMemsetAsync(m->pbuf, 0, 3 * (2 * (size_t)(m->p + 2) + 2) * sizeof(unsigned long long), st));
   int Dv = D, ns = nslots, sc = scratch;
   void* args[] = {&mw, &Dv, &ns, &sc, &A};
   TS_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3((unsigned)grid), dim3(threads), args, smem, st));

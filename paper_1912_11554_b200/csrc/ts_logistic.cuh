@@ -60,8 +60,6 @@ struct LogisticArgs {
   WarpPipe* pipe;           // [nwarps]
   int nstage;
   int stage_bytes;
-  int l2_keep_tiles;        // tiles [0, l2_keep_tiles) loaded with L2::evict_last, rest evict_first
-  int l2_prefetch;          // tiles per warp prefetched into L2 at the end of a pass
   int exact_cvt;            // X holds fp32 subnormals (informational)
   int wide;                 // p > 64: 8-row row-major tiles (logistic_cta_pass_wide)
   double* slotws;           // wide p: NodeStore slot vectors in global memory [grid][5*nslots][D]
@@ -72,7 +70,6 @@ struct LogisticArgs {
   unsigned long long* mail_epoch; // this rank's exchange counter, persistent across launches
   unsigned long long xbase;       // *mail_epoch at kernel start
   unsigned long long* dump;       // optional: raw local totals of the first pass (ts_logistic_partial_sums)
-  int nrep;                       // replicas of each cross-CTA accumulator buffer
 };
 
 // Mailbox of one rank: kMailFlags words of flags (flag[src] = 1 + the last
@@ -828,16 +825,7 @@ static __device__ void logistic_eval_grid(const LogisticArgs& a, const VecStore&
   // is independent of the order in which CTAs arrive -- deterministic.
   unsigned long long* accb = reinterpret_cast<unsigned long long*>(a.pbuf);
   const int64_t bstride = 2 * (int64_t)P2 + 2;
-  // a.nrep replicas per buffer (CTA b adds into replica b % nrep) spread the
-  // same-address atomics; readers add the replicas (integers: exact)
-  const int nrep = a.nrep;
-  unsigned long long* buf = accb + (int64_t)(epoch % 3ULL) * nrep * bstride;
-  unsigned long long* cur = buf + (int64_t)(blockIdx.x % nrep) * bstride;
-  auto rd = [&](int64_t i) {
-    unsigned long long v = 0ULL;
-    for (int r = 0; r < nrep; ++r) v += __ldcg(buf + r * bstride + i);
-    return v;
-  };
+  unsigned long long* cur = accb + (int64_t)(epoch % 3ULL) * bstride;
   if (a.wide) {  // the wide pass leaves exact fixed-point CTA totals in wred
     const unsigned long long* tot = reinterpret_cast<const unsigned long long*>(wred);
     for (int d = wk_tid(); d < P2; d += wk_threads()) {
@@ -875,14 +863,14 @@ static __device__ void logistic_eval_grid(const LogisticArgs& a, const VecStore&
   // buffer (epoch+2)%3 was last read before this barrier by every CTA and is
   // next accumulated after the following barrier: CTA 0 clears it now.
   if (blockIdx.x == 0) {
-    unsigned long long* nxt = accb + (int64_t)((epoch + 2) % 3ULL) * nrep * bstride;
-    for (int i = wk_tid(); i < nrep * bstride; i += wk_threads()) nxt[i] = 0ULL;
+    unsigned long long* nxt = accb + (int64_t)((epoch + 2) % 3ULL) * bstride;
+    for (int i = wk_tid(); i < bstride; i += wk_threads()) nxt[i] = 0ULL;
   }
   epoch += 1;
   if (prof) { c1 = clock64(); a.prof[2] += c1 - c0; c0 = c1; }
 
   if (a.dump && epoch == 1 && blockIdx.x == 0)  // test hook: this GPU's totals of the first pass
-    for (int i = wk_tid(); i < 2 * P2 + 1; i += wk_threads()) a.dump[i] = rd(i);
+    for (int i = wk_tid(); i < 2 * P2 + 1; i += wk_threads()) a.dump[i] = __ldcg(cur + i);
 
   double* g = S.v(gid);
   if (a.world > 0) {
@@ -900,11 +888,11 @@ static __device__ void logistic_eval_grid(const LogisticArgs& a, const VecStore&
         const int r = i / nwords, w = i - r * nwords;
         unsigned long long v;
         if (w < 2 * P2) {  // canonical pair
-          unsigned long long hi = rd(w & ~1), lo = rd(w | 1);
+          unsigned long long hi = __ldcg(cur + (w & ~1)), lo = __ldcg(cur + (w | 1));
           fx_canon(hi, lo);
           v = (w & 1) ? lo : hi;
         } else {
-          v = rd(w);
+          v = __ldcg(cur + w);
         }
         a.mail[r][kMailFlags + (slot * W + a.rank) * bstride + w] = v;
       }
@@ -932,9 +920,9 @@ static __device__ void logistic_eval_grid(const LogisticArgs& a, const VecStore&
       else red_s[0] = s;
     }
   } else {
-    const bool bad = rd(2 * P2) != 0ULL;
+    const bool bad = __ldcg(cur + 2 * P2) != 0ULL;
     for (int d = wk_tid(); d < P2; d += wk_threads()) {
-      unsigned long long hi = rd(2 * d), lo = rd(2 * d + 1);
+      unsigned long long hi = __ldcg(cur + 2 * d), lo = __ldcg(cur + 2 * d + 1);
       fx_canon(hi, lo);  // both words exact in double
       const double s = bad ? __longlong_as_double(0x7ff8000000000000LL) : fx_join((long long)hi, lo);
       if (d <= p) g[d] = theta[d] - s;

@@ -81,6 +81,12 @@ __device__ __forceinline__ void st_release_gpu_u64(unsigned long long* p, unsign
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+__device__ __forceinline__ float tf32r(double x) {
+  uint32_t v;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(v) : "f"((float)x));
+  return __uint_as_float(v);
+}
+
 struct DenseW {
   static constexpr bool kAsync = true;
   static constexpr bool kVecOps = true;  // D ~ 1000 vectors in global memory
@@ -106,11 +112,19 @@ struct DenseW {
       double* row = xt64 + (int64_t)chain * D;
       for (int d = lane; d < D; d += 32) row[d] = qv[d];
     } else {
-      float* row = xt + (int64_t)chain * D;
-      for (int d = lane; d < D; d += 32) {
-        uint32_t v;
-        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(v) : "f"((float)qv[d]));
-        row[d] = __uint_as_float(v);
+      // 4 consecutive components per lane and iteration (16-B stores, 2 x
+      // 16-B loads), 4 iterations in flight (D % 4 == 0, checked at creation)
+      float4* row = reinterpret_cast<float4*>(xt + (int64_t)chain * D);
+      const double2* q2 = reinterpret_cast<const double2*>(qv);
+      const int n4 = D >> 2;
+      for (int base = lane; base < n4; base += 32 * 4) {
+        double2 a[4], b[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (base + 32 * u < n4) { a[u] = q2[2 * (base + 32 * u)]; b[u] = q2[2 * (base + 32 * u) + 1]; }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (base + 32 * u < n4) row[base + 32 * u] = make_float4(tf32r(a[u].x), tf32r(a[u].y), tf32r(b[u].x), tf32r(b[u].y));
       }
     }
     // the GEMM reads the row through the async (TMA) proxy in another CTA
@@ -122,9 +136,13 @@ struct DenseW {
   }
   __device__ double wait() {
     const int lane = threadIdx.x & 31;
-    if (lane == 0)
-      while (ld_acquire_u64(served + chain) < seq) {
+    if (lane == 0) {
+      // relaxed polling (an acquire load per iteration would invalidate the
+      // SM's L1 every time), then one acquire
+      while (ld_relaxed_u64(served + chain) < seq) {
       }
+      (void)ld_acquire_u64(served + chain);
+    }
     __syncwarp();
     const double* qv = S.v(pq);
     double* gv = S.v(pg);
@@ -137,11 +155,32 @@ struct DenseW {
         acc = __dadd_rn(acc, __dmul_rn(qv[d], g));
       }
     } else {
-      const float* row = gt + (int64_t)chain * D;
-      for (int d = lane; d < D; d += 32) {
-        const double g = (double)__ldcg(row + d);
-        gv[d] = g;
-        acc = __dadd_rn(acc, __dmul_rn(qv[d], g));
+      const float4* row = reinterpret_cast<const float4*>(gt + (int64_t)chain * D);
+      const double2* q2 = reinterpret_cast<const double2*>(qv);
+      double2* g2 = reinterpret_cast<double2*>(gv);
+      const int n4 = D >> 2;
+      for (int base = lane; base < n4; base += 32 * 4) {
+        float4 f[4];
+        double2 a[4], b[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (base + 32 * u < n4) {
+            f[u] = __ldcg(row + base + 32 * u);
+            a[u] = q2[2 * (base + 32 * u)];
+            b[u] = q2[2 * (base + 32 * u) + 1];
+          }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (base + 32 * u < n4) {
+            const double2 g0 = make_double2((double)f[u].x, (double)f[u].y);
+            const double2 g1 = make_double2((double)f[u].z, (double)f[u].w);
+            g2[2 * (base + 32 * u)] = g0;
+            g2[2 * (base + 32 * u) + 1] = g1;
+            acc = __dadd_rn(acc, __dmul_rn(a[u].x, g0.x));
+            acc = __dadd_rn(acc, __dmul_rn(a[u].y, g0.y));
+            acc = __dadd_rn(acc, __dmul_rn(b[u].x, g1.x));
+            acc = __dadd_rn(acc, __dmul_rn(b[u].y, g1.y));
+          }
       }
     }
     __syncwarp();

@@ -23,12 +23,13 @@
 namespace ts {
 
 constexpr int kUmmaBM = 128;
-constexpr int kUmmaBN = 64;
+constexpr int kUmmaBN = 64;  // chains per tile (128 measured slower: fewer CTAs share the step)
 constexpr int kUmmaBK = 32;  // fp32/tf32 elements per k-block = one 128-B swizzle row
 constexpr int kUmmaStages = 4;
 constexpr int kUmmaABytes = kUmmaBM * kUmmaBK * 4;  // 16 KB
 constexpr int kUmmaBBytes = kUmmaBN * kUmmaBK * 4;  // 8 KB
 constexpr int kUmmaStageBytes = kUmmaABytes + kUmmaBBytes;
+static_assert(kUmmaBN <= 128, "the stored-column mask gives one chain per GEMM thread");
 // shared memory of the GEMM: 1024-B aligned ring + mbarriers (full, empty, accum) + TMEM address
 constexpr int kUmmaSmemBytes = kUmmaStages * kUmmaStageBytes + 1024 + 256;
 
@@ -169,7 +170,7 @@ struct UmmaGemm {
     if (threadIdx.x < 32) u_tmem_dealloc(tmem, kUmmaBN);
   }
 
-  // One 128 x 64 output tile: rows m0.., chains n0..; nkb k-blocks.
+  // One 128 x kUmmaBN output tile: rows m0.., chains n0..; nkb k-blocks.
   // Output GT[(n0 + j) * ldo + m0 + i] for i < m_valid, j < n_valid.
   // pend (optional): output column j is stored only if pend[j] != 0.
   __device__ void tile(const void* tmA, const void* tmB, int m0, int n0, int nkb, float* GT, int64_t ldo, int m_valid,
@@ -206,6 +207,14 @@ struct UmmaGemm {
       (void)idesc;
     }
     __syncwarp();
+    // stored-column mask (one bit per chain of the tile) while the MMAs run
+    const uint32_t smask = accum + 16;  // 4 words after the TMEM address slot
+    if (pend != nullptr) {
+      const bool want = t < n_valid && __ldcg(pend + t) != 0ULL;
+      const uint32_t b = __ballot_sync(0xffffffffu, want);
+      if ((t & 31) == 0) asm volatile("st.shared.u32 [%0], %1;" ::"r"(smask + 4 * (t >> 5)), "r"(b) : "memory");
+      asm volatile("bar.sync 4, 128;" ::: "memory");
+    }
     // epilogue: all 4 warps
     u_mbar_wait(accum, tiles_done & 1);
     u_fence_after();
@@ -216,11 +225,13 @@ struct UmmaGemm {
     for (int c = 0; c < kUmmaBN; c += 16) {
       float v[16];
       u_tmem_ld16(tmem + ((uint32_t)(w * 32) << 16) + (uint32_t)c, v);
+      uint32_t mw = 0xffffffffu;
+      if (pend != nullptr) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(mw) : "r"(smask + 4 * (c >> 5)));
+      mw >>= (c & 31);
       if (row < m_valid) {
 #pragma unroll
         for (int j = 0; j < 16; ++j)
-          if (c + j < n_valid && (pend == nullptr || __ldcg(pend + c + j) != 0ULL))
-            GT[(int64_t)(n0 + c + j) * ldo + m0 + row] = v[j];
+          if (c + j < n_valid && ((mw >> j) & 1u)) GT[(int64_t)(n0 + c + j) * ldo + m0 + row] = v[j];
       }
     }
     u_fence_before();

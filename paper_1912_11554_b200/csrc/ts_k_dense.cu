@@ -195,6 +195,7 @@ struct DenseW {
 
 struct DenseArgs {
   int D, C, Cpad, fp64, nv;
+  int chain0;  // first chain of this launch (runs with more chains than one grid holds are chunked)
   float* xt;
   double* xt64;
   float* gt;
@@ -356,17 +357,37 @@ __global__ void __launch_bounds__(128 + 32 * kDenseCW, 1)
     E.tr = nullptr;
     E.ss = ss_all + cw * kMaxSlots;
     __syncwarp();
-    do_op(E, A, A.op == OP_RUN ? chain : 0, chain == 0 || A.op == OP_RUN);
+    do_op(E, A, A.op == OP_RUN ? a.chain0 + chain : 0, chain == 0 || A.op == OP_RUN);
   }
   __syncwarp();
   __threadfence();
   if ((threadIdx.x & 31) == 0) atomicAdd(a.done, 1);
 }
 
+static int launch_dense_chunk(const ts_model* m, int nslots, OpArgs& A, int C, int chain0, cudaStream_t st);
+
 int launch_dense(const ts_model* m, int nslots, OpArgs& A, int n_chains, cudaStream_t st) {
+  if (A.op != OP_RUN) return launch_dense_chunk(m, nslots, A, 1, 0, st);
+  // one co-resident grid holds (CTAs per SM x SMs) x kDenseCW chains; larger
+  // runs go in chunks (each chain is a pure function of its key)
+  int dev = 0, nsm = 0, occ = 0;
+  TS_CUDA(cudaGetDevice(&dev));
+  TS_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  const size_t smem = kUmmaSmemBytes + 64 + kDenseCW * kMaxSlots * sizeof(SlotScalars);
+  TS_CUDA(cudaFuncSetAttribute(k_dense_op, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  TS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_dense_op, 128 + 32 * kDenseCW, smem));
+  const int cap = occ * nsm * kDenseCW;
+  if (cap < 1) return set_err(TS_EUNSUPPORTED, "dense model kernel cannot be resident");
+  for (int c0 = 0; c0 < n_chains; c0 += cap) {
+    const int rc = launch_dense_chunk(m, nslots, A, n_chains - c0 < cap ? n_chains - c0 : cap, c0, st);
+    if (rc) return rc;
+  }
+  return TS_OK;
+}
+
+static int launch_dense_chunk(const ts_model* m, int nslots, OpArgs& A, int C, int chain0, cudaStream_t st) {
   ts_model* mm = const_cast<ts_model*>(m);
   const int D = m->dim;
-  const int C = (A.op == OP_RUN) ? n_chains : 1;
   const int grid = (C + kDenseCW - 1) / kDenseCW;
   const int Cpad = ((grid * kDenseCW + kUmmaBN - 1) / kUmmaBN) * kUmmaBN;
   const int nv = num_vecs(nslots);
@@ -391,7 +412,7 @@ int launch_dense(const ts_model* m, int nslots, OpArgs& A, int n_chains, cudaStr
   }
   DenseArgs a;
   memset(&a, 0, sizeof a);
-  a.D = D; a.C = C; a.Cpad = Cpad; a.fp64 = m->fp64; a.nv = nv;
+  a.D = D; a.C = C; a.Cpad = Cpad; a.fp64 = m->fp64; a.nv = nv; a.chain0 = chain0;
   unsigned char* p = mm->dws;
   a.bar = reinterpret_cast<unsigned long long*>(p);
   a.done = reinterpret_cast<int*>(p + 8);

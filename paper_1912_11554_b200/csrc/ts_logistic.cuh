@@ -135,6 +135,11 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned 
   asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ unsigned long long ld_relaxed_sys_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ void st_release_sys_u64(unsigned long long* p, unsigned long long v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
@@ -901,9 +906,11 @@ static __device__ void logistic_eval_grid(const LogisticArgs& a, const VecStore&
       if (wk_tid() < W) st_release_sys_u64(a.mail[wk_tid()] + a.rank, x + 1);
     }
     const unsigned long long* box = a.mail[a.rank];
-    if (wk_tid() < W)
-      while (ld_acquire_sys_u64(box + wk_tid()) < x + 1) {
+    if (wk_tid() < W) {  // relaxed polling, then one acquire (each acquire load invalidates L1)
+      while (ld_relaxed_sys_u64(box + wk_tid()) < x + 1) {
       }
+      (void)ld_acquire_sys_u64(box + wk_tid());
+    }
     wk_sync();
     const unsigned long long* sl = box + kMailFlags + slot * W * bstride;
     unsigned long long badw = 0;

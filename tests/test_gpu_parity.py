@@ -652,3 +652,19 @@ def test_hmc_transition_matches_reference():
             assert close(q, nums(d["q_out"]), SMALL_REL, atol=SMALL_REL)
             assert close(st.accept_stat, num(d["accept_stat"]), SMALL_REL)
             assert close(st.energy, num(d["energy"]), SMALL_REL)
+
+
+def test_dense_run_chunks_beyond_one_grid():
+    """More chains than one co-resident grid holds (148 SMs x 8 chain warps):
+    the run is chunked; every chain is a pure function of its key."""
+    t = ts()
+    D, C = 16, 1500
+    A = _spd(D, 9, cond=10.0)
+    m = t.dense_gaussian_model(A, precision="fp64")
+    cfg = t.RunConfig(model={}, num_chains=C, num_warmup=20, num_samples=5, seed=8)
+    keys = t.chain_keys(8, C)
+    big = t.run_device(m, cfg, keys, 0).samples.cpu().numpy()
+    assert np.isfinite(big).all()
+    for c in (0, 1, 1199, 1499):
+        one = t.run_device(m, cfg, [keys[c]], 0).samples.cpu().numpy()[0]
+        assert np.array_equal(big[c], one), c

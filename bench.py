@@ -256,7 +256,7 @@ def run_eight_schools(args):
         dist.all_reduce(tl, op=dist.ReduceOp.SUM)
         t = torch.cat([tm, tl])
     t_ms, lf = float(t[0]), float(t[1])
-    ess = ts.ess(last.samples.cpu().numpy())
+    ess = ts.ess_device(last.samples)  # on the GPU: no host copy of the 8192-chain samples
     if rank == 0:
         print(json.dumps({
             "metric": "leapfrog_steps_per_sec", "value": lf / (t_ms / 1000.0), "unit": "leapfrog/s",

@@ -668,3 +668,12 @@ def test_dense_run_chunks_beyond_one_grid():
     for c in (0, 1, 1199, 1499):
         one = t.run_device(m, cfg, [keys[c]], 0).samples.cpu().numpy()[0]
         assert np.array_equal(big[c], one), c
+
+
+def test_ess_device_on_gpu_samples():
+    """Device ESS on a many-chain run's samples in HBM."""
+    t = ts()
+    m = t.eight_schools_model()
+    cfg = t.RunConfig(model={}, num_chains=256, num_warmup=100, num_samples=200, seed=3)
+    r = t.run_device(m, cfg, t.chain_keys(3, 256), 0)
+    assert np.allclose(t.ess_device(r.samples), t.ess(r.samples.cpu().numpy()), rtol=1e-10)

@@ -274,3 +274,14 @@ def test_oracle_dense_gaussian(oracle):
     g = np.asarray(m.gradient(x.tolist()))
     assert np.allclose(g, a @ x, rtol=1e-12, atol=1e-12)
     assert np.isclose(m.potential(x.tolist()), 0.5 * x @ a @ x, rtol=1e-12)
+
+
+def test_ess_device_matches_host_estimator():
+    import torch
+
+    rng = np.random.default_rng(0)
+    for shape in ((4, 100, 3), (16, 1000, 10), (1, 50, 2), (3, 7, 1)):
+        x = rng.standard_normal(shape)
+        for i in range(1, shape[1]):
+            x[:, i] = 0.7 * x[:, i - 1] + x[:, i]
+        assert np.allclose(t.ess_device(torch.from_numpy(x)), t.ess(x), rtol=1e-12)

@@ -462,8 +462,11 @@ struct Engine {
   }
 
   // ------------------------------------------------------- tree builder
-  __device__ void running_from_leaf(int n, double lw, double metro, double h) {
-    copy_group(V_FQ, V_CQ, V_FR, V_CR, V_CUMF, V_CUM, V_TPQ, V_CQ, V_TPG, V_CG);
+  // with_first = false: the caller merges a stored subtree next, which
+  // replaces first / cum_first, so only the proposal is materialised
+  __device__ void running_from_leaf(int n, double lw, double metro, double h, bool with_first = true) {
+    if (with_first) copy_group(V_FQ, V_CQ, V_FR, V_CR, V_CUMF, V_CUM, V_TPQ, V_CQ, V_TPG, V_CG);
+    else { copy(V_TPQ, V_CQ); copy(V_TPG, V_CG); }
     r_lw = lw; r_metro = metro; r_count = 1; r_pU = cur_U; r_pH = h; r_pidx = n; r_fU = cur_U;
   }
 
@@ -661,7 +664,7 @@ struct Engine {
     }
     int slot = pc - 1;
     const int i_min = slot - __popcll(((n + 1) & ~n) - 1) + 1;
-    running_from_leaf((int)n, lw, metro, h);
+    running_from_leaf((int)n, lw, metro, h, false);  // odd n: at least one merge follows
     while (slot >= i_min) {
       ev(kEvCheck, (int)n, slot, ss[slot].leaf);
       merge_slot(slot, draws.next_double());

@@ -208,7 +208,7 @@ struct DenseArgs {
   unsigned long long* posted;   // [Cpad] (zeroed before launch)
   unsigned long long* served;   // [Cpad]
   unsigned long long* pending;  // [Cpad] request served by the current step (0 = none)
-  unsigned long long* npend;    // [2] outstanding requests of the step (rotating)
+  unsigned long long* npend;    // [2] outstanding requests of the step, [2..4) all-done flags (rotating)
 };
 
 __device__ __forceinline__ void gemm_grid_barrier(unsigned long long* bar, unsigned long long& epoch) {
@@ -282,10 +282,16 @@ __global__ void __launch_bounds__(128 + 32 * kDenseCW, 1)
         a.pending[my_chain] = mine;
         if (mine) atomicAdd(a.npend + (step & 1), 1ULL);
       }
+      // the exit decision must be the same in every CTA: CTA 0 samples the
+      // finished-chain count BEFORE the barrier (chains keep finishing
+      // asynchronously, so reading it after the barrier could differ per CTA)
+      if (t == 0 && blockIdx.x == 0)
+        a.npend[2 + (step & 1)] = (*reinterpret_cast<volatile int*>(a.done) >= total) ? 1ULL : 0ULL;
       gemm_grid_barrier(a.bar, epoch);
       if (t == 0) {
         const unsigned long long np = ld_relaxed_u64(a.npend + (step & 1));
-        *flag = (np == 0ULL && *reinterpret_cast<volatile int*>(a.done) >= total) ? 0 : (np ? 1 : 2);
+        const bool all_done = ld_relaxed_u64(a.npend + 2 + (step & 1)) != 0ULL;
+        *flag = (np == 0ULL && all_done) ? 0 : (np ? 1 : 2);
         if (blockIdx.x == 0) a.npend[(step + 1) & 1] = 0ULL;  // next slot: last read before this barrier
       }
       asm volatile("bar.sync 4, 128;" ::: "memory");
@@ -401,7 +407,7 @@ static int launch_dense_chunk(const ts_model* m, int nslots, OpArgs& A, int C, i
   TS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 128 + 32 * kDenseCW, smem));
   if ((int64_t)occ * nsm < grid) return set_err(TS_EUNSUPPORTED, "dense model: too many chains for one co-resident grid");
   // workspaces (grown on demand, owned by the model)
-  const size_t need = (size_t)Cpad * D * (m->fp64 ? 16 : 8) + (size_t)C * nv * D * 8 + 64 + (size_t)Cpad * 24 + 64;
+  const size_t need = (size_t)Cpad * D * (m->fp64 ? 16 : 8) + (size_t)C * nv * D * 8 + 64 + (size_t)Cpad * 24 + 64;  // + flags
   if (mm->dws_size < need) {
     if (mm->dws) cudaFree(mm->dws);
     mm->dws = nullptr;
@@ -441,7 +447,7 @@ static int launch_dense_chunk(const ts_model* m, int nslots, OpArgs& A, int C, i
     if (rc) return rc;
   }
   TS_CUDA(cudaMemsetAsync(mm->dws, 0, 64, st));
-  TS_CUDA(cudaMemsetAsync(a.posted, 0, ((size_t)Cpad * 3 + 2) * sizeof(unsigned long long), st));
+  TS_CUDA(cudaMemsetAsync(a.posted, 0, ((size_t)Cpad * 3 + 4) * sizeof(unsigned long long), st));
   const bool prof = getenv("TS_PROF") != nullptr;  // profiling aid: CTA-0 step phases to stderr
   if (prof) a.prof = reinterpret_cast<unsigned long long*>(mm->dws + 16);  // 5 words in the zeroed header
   int ns = nslots;

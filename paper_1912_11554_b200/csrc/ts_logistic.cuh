@@ -206,6 +206,14 @@ __device__ __forceinline__ void cta_bar(int id) { asm volatile("bar.sync %0, %1;
 __device__ __forceinline__ void cta_arrive(int id) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"((int)blockDim.x) : "memory"); }
 
 // ------------------------------------------------------------- tile pipeline
+// Ring-position arithmetic: 32-bit div/mod while the counters fit (64-bit
+// division is a long emulated sequence on the per-pass entry path).
+__device__ __forceinline__ uint32_t umod(unsigned long long a, uint32_t b) {
+  return (a >> 32) ? (uint32_t)(a % b) : (uint32_t)a % b;
+}
+__device__ __forceinline__ uint32_t udiv(unsigned long long a, uint32_t b) {
+  return (a >> 32) ? (uint32_t)(a / b) : (uint32_t)a / b;
+}
 struct WarpTiles {
   int64_t first;  // first tile of this warp
   int64_t count;  // number of tiles (stride nwarps)
@@ -246,9 +254,9 @@ struct Producer {
     stage_bytes = a.stage_bytes;
     ring = a.stages + (int64_t)warp * nstage * stage_bytes;
     bars = a.mbar + warp * nstage;
-    s = (int)(issued % (unsigned long long)nstage);
+    s = (int)(umod(issued, nstage));
     count = wt.count;
-    tj = (int64_t)(issued % (unsigned long long)count);
+    tj = (int64_t)(umod(issued, (uint32_t)count));
     xb = 128u * (uint32_t)a.p;
     xfirst = a.xt + wt.first * 32 * (int64_t)a.p;
     yfirst = a.yt + wt.first * 32;
@@ -374,9 +382,9 @@ __device__ __noinline__ void logistic_cta_pass(const LogisticArgs& a, const doub
       while (issued < c0 + (unsigned long long)a.nstage) { prod.issue(); ++issued; }
     }
     // ring position and periodic tile index, advanced incrementally
-    int s = (int)(c0 % (unsigned long long)a.nstage);
-    uint32_t parity = (uint32_t)((c0 / a.nstage) & 1ULL);
-    int64_t tj = (int64_t)(c0 % (unsigned long long)wt.count);
+    int s = (int)(umod(c0, a.nstage));
+    uint32_t parity = udiv(c0, a.nstage) & 1u;
+    int64_t tj = (int64_t)(umod(c0, (uint32_t)wt.count));
     const unsigned char* ring = a.stages + (int64_t)warp * a.nstage * a.stage_bytes;
     uint64_t* bars = a.mbar + warp * a.nstage;
     if (prof) { pc1 = clock64(); a.prof[4] += pc1 - pc0; pc0 = pc1; }
@@ -553,9 +561,9 @@ struct WideProducer {
     stage_bytes = (uint32_t)a.stage_bytes;
     ring = smem_u32(a.stages) + (uint32_t)(warp * nstage) * stage_bytes;
     bars = smem_u32(a.mbar + warp * nstage);
-    s = (int)(issued % (unsigned long long)nstage);
+    s = (int)(umod(issued, nstage));
     count = wt.count;
-    const unsigned long long i = issued % (unsigned long long)(count * kWideGroup);
+    const unsigned long long i = umod(issued, (uint32_t)(count * kWideGroup));
     gj = (int64_t)(i / kWideGroup);
     k = (int)(i % kWideGroup);
     tb = (uint32_t)wide_tile_bytes(a.p);
@@ -642,9 +650,9 @@ __device__ __noinline__ void logistic_cta_pass_wide(const LogisticArgs& a, const
       prod.init(a, wt, issued);
       while (issued < c0 + (unsigned long long)nstage) { prod.issue(); ++issued; }
     }
-    int s = (int)(c0 % (unsigned long long)nstage);
-    uint32_t parity = (uint32_t)((c0 / nstage) & 1ULL);
-    const unsigned long long i0 = c0 % (unsigned long long)ntile_w;
+    int s = (int)(umod(c0, nstage));
+    uint32_t parity = udiv(c0, nstage) & 1u;
+    const unsigned long long i0 = umod(c0, (uint32_t)ntile_w);
     int64_t gj = (int64_t)(i0 / kWideGroup);
     int k = (int)(i0 % kWideGroup);
     const uint32_t ring_off = (uint32_t)(a.stages - ts_dyn_smem) + (uint32_t)(warp * nstage * stage_bytes);

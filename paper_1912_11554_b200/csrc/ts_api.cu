@@ -116,7 +116,7 @@ static int launch(const ts_model* m, int nslots, OpArgs& A, int n_threads_chains
   sm.dim = m->dim;
   sm.params = m->params;
   const int D = m->dim;
-  if (mode == TS_EXEC_BLOCK) return launch_block_small(sm, D, nslots, A, st);
+  if (mode == TS_EXEC_BLOCK) return launch_block_small(sm, D, nslots, A, n_threads_chains, st);
   return launch_thread(sm, D, n_threads_chains, nslots, A, st);
 }
 

@@ -280,7 +280,9 @@ __global__ void __launch_bounds__(256, 1) k_block_op(MW mw, int D, int nslots, i
     E.M = mw;
     E.D = D;
     E.S = S;
-    do_op(E, A, chain, writer);
+    // small models: one CTA per chain for runs (chain = launch offset + CTA)
+    if (A.op == OP_RUN) do_op(E, A, A.n_points + (int)blockIdx.x, true);
+    else do_op(E, A, chain, writer);
   } else {
     // wide-p models keep the NodeStore slot vectors in a per-CTA global
     // workspace (their data pass is long; shared memory goes to the ring)
@@ -327,7 +329,7 @@ __global__ void __launch_bounds__(256, 1) k_block_op(MW mw, int D, int nslots, i
 
 
 int launch_thread(const SmallModel& sm, int D, int C, int nslots, OpArgs& A, cudaStream_t st);
-int launch_block_small(const SmallModel& sm, int D, int nslots, OpArgs& A, cudaStream_t st);
+int launch_block_small(const SmallModel& sm, int D, int nslots, OpArgs& A, int C, cudaStream_t st);
 int launch_block_logistic(const ts_model* m, int nslots, OpArgs& A, cudaStream_t st);
 int launch_dense(const ts_model* m, int nslots, OpArgs& A, int n_chains, cudaStream_t st);
 

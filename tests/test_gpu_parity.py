@@ -677,3 +677,17 @@ def test_ess_device_on_gpu_samples():
     cfg = t.RunConfig(model={}, num_chains=256, num_warmup=100, num_samples=200, seed=3)
     r = t.run_device(m, cfg, t.chain_keys(3, 256), 0)
     assert np.allclose(t.ess_device(r.samples), t.ess(r.samples.cpu().numpy()), rtol=1e-10)
+
+
+def test_block_team_runs_every_chain():
+    """exec_mode='block' runs one CTA per chain: every chain's draws match the
+    thread-team run (same keys) to the block-reduction tolerance."""
+    t = ts()
+    m = t.gaussian_model(np.logspace(-1, 1, 10))
+    cfg = t.RunConfig(model={}, num_chains=5, num_warmup=0, num_samples=4, seed=12,
+                      sampler=t.SamplerConfig(step_size=0.3, mass=t.MassMatrix.identity(10)))
+    keys = t.chain_keys(12, 5)
+    a = t.run_device(m, cfg, keys, 0, exec_mode="thread").samples.cpu().numpy()
+    b = t.run_device(m, cfg, keys, 0, exec_mode="block").samples.cpu().numpy()
+    assert np.isfinite(b).all()
+    assert close(b[:, :3], a[:, :3], BLOCK_REL, atol=BLOCK_REL)

@@ -167,6 +167,59 @@ static __device__ __noinline__ void warp_gen_uturn2(const double2* __restrict__ 
   ab[1] = b;
 }
 __device__ __forceinline__ bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+// One pass over a leaf for warp-owned large-D vectors (batched models):
+// advance_leaf (kick of leaf n from its pass), add_cum, the kinetic-energy
+// partial of leaf n (same lane order as warp_kinetic2), drift_next (leaf
+// n+1) and the request row for leaf n+1 (tf32 floats, or doubles).  Every
+// element gets the same arithmetic as the separate loops.
+template <bool F64ROW>
+static __device__ __noinline__ double warp_leaf_fused(double2* __restrict__ q, double2* __restrict__ r,
+                                                      double2* __restrict__ g, double2* __restrict__ nq,
+                                                      double2* __restrict__ nr, const double2* __restrict__ ng,
+                                                      const double2* __restrict__ inv, double2* __restrict__ cum,
+                                                      void* __restrict__ row, double half, double eps, int n2) {
+  double kin = 0.0;
+  for (int base = (int)(threadIdx.x & 31); base < n2; base += 32 * 4) {
+    double2 tq[4], tr[4], tg[4], ti[4], tc[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (base + 32 * u < n2) {
+        const int i = base + 32 * u;
+        tq[u] = nq[i]; tr[u] = nr[i]; tg[u] = ng[i]; ti[u] = inv[i]; tc[u] = cum[i];
+      }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (base + 32 * u < n2) {
+        const int i = base + 32 * u;
+        double2 rr, rh, nqv, cv;
+        rr.x = __dsub_rn(tr[u].x, __dmul_rn(half, tg[u].x));
+        rr.y = __dsub_rn(tr[u].y, __dmul_rn(half, tg[u].y));
+        q[i] = tq[u];
+        g[i] = tg[u];
+        r[i] = rr;
+        cv.x = __dadd_rn(tc[u].x, rr.x);
+        cv.y = __dadd_rn(tc[u].y, rr.y);
+        cum[i] = cv;
+        kin = __dadd_rn(kin, __dmul_rn(__dmul_rn(__dmul_rn(0.5, rr.x), rr.x), ti[u].x));
+        kin = __dadd_rn(kin, __dmul_rn(__dmul_rn(__dmul_rn(0.5, rr.y), rr.y), ti[u].y));
+        rh.x = __dsub_rn(rr.x, __dmul_rn(half, tg[u].x));
+        rh.y = __dsub_rn(rr.y, __dmul_rn(half, tg[u].y));
+        nqv.x = __dadd_rn(tq[u].x, __dmul_rn(eps, __dmul_rn(ti[u].x, rh.x)));
+        nqv.y = __dadd_rn(tq[u].y, __dmul_rn(eps, __dmul_rn(ti[u].y, rh.y)));
+        nr[i] = rh;
+        nq[i] = nqv;
+        if constexpr (F64ROW) {
+          reinterpret_cast<double2*>(row)[i] = nqv;
+        } else {
+          uint32_t a, b;
+          asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(a) : "f"((float)nqv.x));
+          asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(b) : "f"((float)nqv.y));
+          reinterpret_cast<float2*>(row)[i] = make_float2(__uint_as_float(a), __uint_as_float(b));
+        }
+      }
+  }
+  return kin;
+}
 // up to 5 vector copies in one pass (k pairs), 2 x double2 per operand in flight
 static __device__ __noinline__ void warp_copy_multi(double2* __restrict__ d0, const double2* __restrict__ s0,
                                                     double2* __restrict__ d1, const double2* __restrict__ s1,
@@ -719,18 +772,51 @@ struct Engine {
         for (unsigned long long n = 0; n < nleaves; ++n) {
           const double u = wait_eval();
           const bool spec = n + 1 < nleaves;
-          if (spec) {
-            // leaf n's kick fused with leaf n+1's drift: the next pass is
-            // posted after one vector loop; leaf n's energy, prefix sum and
-            // bookkeeping overlap with it
-            advance_drift(eps, u);
-            post_eval(V_NQ, V_NG);
-          } else {
-            advance_leaf(eps, u);
-          }
-          add_cum();
           double h, delta;
-          leaf_energy(h_ref, h, delta);
+          bool fused = false;
+          if constexpr (Team::kWarp && Team::kUnitStride && Model::kVecOps) {
+            // batched large-D model: kick, prefix sum, kinetic energy, next
+            // drift and the request row in one pass over the vectors
+            if (spec && D >= 128 && (D & 1) == 0) {
+              cur_U = u;
+              const double half = __dmul_rn(0.5, eps);
+              void* row = M.request_row();
+              double2* q2 = reinterpret_cast<double2*>(v(V_CQ));
+              double2* r2 = reinterpret_cast<double2*>(v(V_CR));
+              double2* g2 = reinterpret_cast<double2*>(v(V_CG));
+              double2* nq2 = reinterpret_cast<double2*>(v(V_NQ));
+              double2* nr2 = reinterpret_cast<double2*>(v(V_NR));
+              const double2* ng2 = reinterpret_cast<const double2*>(v(V_NG));
+              const double2* inv2 = reinterpret_cast<const double2*>(v(V_INV));
+              double2* c2 = reinterpret_cast<double2*>(v(V_CUM));
+              const double kin = M.fp64
+                  ? warp_leaf_fused<true>(q2, r2, g2, nq2, nr2, ng2, inv2, c2, row, half, eps, D >> 1)
+                  : warp_leaf_fused<false>(q2, r2, g2, nq2, nr2, ng2, inv2, c2, row, half, eps, D >> 1);
+              T.sync();
+              M.post_written(V_NQ, V_NG);
+              const double ke = T.sum(kin);
+              if (!isfinite(cur_U)) h = kInf();
+              else {
+                h = __dadd_rn(cur_U, ke);
+                if (!isfinite(h)) h = kInf();
+              }
+              delta = __dsub_rn(h, h_ref);
+              fused = true;
+            }
+          }
+          if (!fused) {
+            if (spec) {
+              // leaf n's kick fused with leaf n+1's drift: the next pass is
+              // posted after one vector loop; leaf n's energy, prefix sum and
+              // bookkeeping overlap with it
+              advance_drift(eps, u);
+              post_eval(V_NQ, V_NG);
+            } else {
+              advance_leaf(eps, u);
+            }
+            add_cum();
+            leaf_energy(h_ref, h, delta);
+          }
           stop = leaf_book(n, h, delta, draws, forward);
           if (stop != kStopNone) {
             if (spec) { (void)wait_eval(); n_wasted += 1; }

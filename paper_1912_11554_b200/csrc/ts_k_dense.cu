@@ -191,6 +191,19 @@ struct DenseW {
     post(q, g);
     return wait();
   }
+  // the engine's fused leaf pass writes the request row itself
+  __device__ void* request_row() const {
+    return fp64 ? (void*)(xt64 + (int64_t)chain * D) : (void*)(xt + (int64_t)chain * D);
+  }
+  __device__ void post_written(int q, int g) {
+    pq = q;
+    pg = g;
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    __threadfence();
+    __syncwarp();
+    seq += 1;
+    if ((threadIdx.x & 31) == 0) st_release_gpu_u64(posted + chain, seq);
+  }
 };
 
 struct DenseArgs {

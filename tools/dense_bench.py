@@ -17,7 +17,7 @@ q, _ = np.linalg.qr(rng.standard_normal((D, D)))
 lam = np.logspace(-2, 2, D)
 Sigma = (q * lam) @ q.T
 P = (q / lam) @ q.T
-for dense_mass in ((True,) if os.environ.get("DENSE_ONLY_MASS") else (False, True)):
+for dense_mass in ((True,) if os.environ.get("DENSE_ONLY_MASS") else ((False,) if os.environ.get("DENSE_NO_MASS") else (False, True))):
     m = ts.dense_gaussian_model(P, inv_mass=Sigma if dense_mass else None, precision=prec)
     cfg = ts.RunConfig(model={}, num_chains=C, num_warmup=W, num_samples=S, seed=4)
     for it in range(2):

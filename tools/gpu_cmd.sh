@@ -1,2 +1,2 @@
-timeout 300 python tools/single_chain.py > gpurun_out/sc1.log 2>&1
-timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/t43.log 2>&1
+timeout 600 python -m pytest tests -m gpu -q -x -k "dense or tcgen05" > gpurun_out/t44.log 2>&1
+for i in 1 2 3; do TS_PROF=1 timeout 120 python tools/dense_bench.py tf32 1024 20 10 >> gpurun_out/d10.log 2>&1; echo "rc=$?" >> gpurun_out/d10.log; done

@@ -338,6 +338,9 @@ struct Engine {
   // for CTA/warp teams (every team thread writes the identical value), which
   // keeps them out of the local-memory path when shared memory crowds L1.
   SlotScalars* ss;
+  // running subtree's first leaf / prefix sum live in NodeStore slot f_alias
+  // (instead of V_FQ/V_FR/V_CUMF) after a merge; materialised at tree end
+  int f_alias = -1;
   unsigned long long n_evals;
   unsigned long long n_wasted;  // speculative passes discarded (tree stopped early)
   double pending_u;
@@ -517,9 +520,17 @@ struct Engine {
   // ------------------------------------------------------- tree builder
   // with_first = false: the caller merges a stored subtree next, which
   // replaces first / cum_first, so only the proposal is materialised
+  __device__ int fq_id() const { return f_alias < 0 ? (int)V_FQ : slot_vec(f_alias, 0); }
+  __device__ int fr_id() const { return f_alias < 0 ? (int)V_FR : slot_vec(f_alias, 1); }
+  __device__ int cumf_id() const { return f_alias < 0 ? (int)V_CUMF : slot_vec(f_alias, 2); }
   __device__ void running_from_leaf(int n, double lw, double metro, double h, bool with_first = true) {
-    if (with_first) copy_group(V_FQ, V_CQ, V_FR, V_CR, V_CUMF, V_CUM, V_TPQ, V_CQ, V_TPG, V_CG);
-    else { copy(V_TPQ, V_CQ); copy(V_TPG, V_CG); }
+    if (with_first) {
+      copy_group(V_FQ, V_CQ, V_FR, V_CR, V_CUMF, V_CUM, V_TPQ, V_CQ, V_TPG, V_CG);
+      f_alias = -1;
+    } else {
+      copy(V_TPQ, V_CQ);
+      copy(V_TPG, V_CG);
+    }
     r_lw = lw; r_metro = metro; r_count = 1; r_pU = cur_U; r_pH = h; r_pidx = n; r_fU = cur_U;
   }
 
@@ -529,12 +540,12 @@ struct Engine {
     const double lw = logaddexp_inner(L.lw, r_lw);
     const double p_right = (r_lw == -kInf()) ? 0.0 : exp(__dsub_rn(r_lw, lw));
     if (!(u < p_right)) {
-      copy_group(V_FQ, slot_vec(s, 0), V_FR, slot_vec(s, 1), V_CUMF, slot_vec(s, 2), V_TPQ, slot_vec(s, 3), V_TPG,
-                 slot_vec(s, 4));
+      copy(V_TPQ, slot_vec(s, 3));
+      copy(V_TPG, slot_vec(s, 4));
       r_pU = L.pU; r_pH = L.pH; r_pidx = L.pidx;
-    } else {
-      copy_group(V_FQ, slot_vec(s, 0), V_FR, slot_vec(s, 1), V_CUMF, slot_vec(s, 2));
     }
+    // first / cum_first come from the left (stored) subtree: alias, no copy
+    f_alias = s;
     r_fU = L.fU;
     r_lw = lw;
     r_count = L.count + r_count;
@@ -552,8 +563,8 @@ struct Engine {
       // rho = (cum_last - cum_first) + first.r  -> V_MSUM as scratch
       double* rho = v(V_MSUM);
       const double* cum = v(V_CUM);
-      const double* cf = v(V_CUMF);
-      const double* fr = v(V_FR);
+      const double* cf = v(cumf_id());
+      const double* fr = v(fr_id());
       if constexpr (Team::kWarp && Team::kUnitStride && Model::kVecOps) {
         const double* inv = v(V_INV);
         const double* cr = v(V_CR);
@@ -568,17 +579,17 @@ struct Engine {
         }
       }
       for (int d = T.rank(); d < D; d += T.size()) rho[d * s] = __dadd_rn(__dsub_rn(cum[d * s], cf[d * s]), fr[d * s]);
-      return uturn_dots(V_MSUM, V_FR, V_CR);
+      return uturn_dots(V_MSUM, fr_id(), V_CR);
     }
     double* dq = v(V_MSUM);
     const double* lq = v(V_CQ);
-    const double* fq = v(V_FQ);
+    const double* fq = v(fq_id());
     if (forward) {
       for (int d = T.rank(); d < D; d += T.size()) dq[d * s] = __dsub_rn(lq[d * s], fq[d * s]);
-      return uturn_dots(V_MSUM, V_FR, V_CR);
+      return uturn_dots(V_MSUM, fr_id(), V_CR);
     }
     for (int d = T.rank(); d < D; d += T.size()) dq[d * s] = __dsub_rn(fq[d * s], lq[d * s]);
-    return uturn_dots(V_MSUM, V_CR, V_FR);
+    return uturn_dots(V_MSUM, V_CR, fr_id());
   }
 
   // leaf energy bookkeeping shared by both branches
@@ -833,6 +844,10 @@ struct Engine {
           if (stop != kStopNone) break;
         }
       }
+    }
+    if (f_alias >= 0) {  // the tree's first leaf / prefix sum into V_FQ/V_FR/V_CUMF
+      copy_group(V_FQ, slot_vec(f_alias, 0), V_FR, slot_vec(f_alias, 1), V_CUMF, slot_vec(f_alias, 2));
+      f_alias = -1;
     }
     // momentum_sum = (cum_last - cum_first) + first.r   (tree.py:283-294)
     {

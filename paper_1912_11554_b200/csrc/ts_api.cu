@@ -442,8 +442,8 @@ extern "C" int ts_run_chains(const ts_model* m, const ts_run_cfg* rc, const uint
     static unsigned long long* prof_buf = nullptr;
     const bool prof = getenv("TS_PROF") != nullptr;
     if (prof) {
-      if (!prof_buf) TS_CUDA(cudaMalloc((void**)&prof_buf, 16 * sizeof(unsigned long long)));
-      TS_CUDA(cudaMemsetAsync(prof_buf, 0, 16 * sizeof(unsigned long long), st));
+      if (!prof_buf) TS_CUDA(cudaMalloc((void**)&prof_buf, 24 * sizeof(unsigned long long)));
+      TS_CUDA(cudaMemsetAsync(prof_buf, 0, 24 * sizeof(unsigned long long), st));
       const_cast<ts_model*>(m)->prof = prof_buf;
     }
     for (int c = 0; c < n_chains; ++c) {
@@ -453,7 +453,7 @@ extern "C" int ts_run_chains(const ts_model* m, const ts_run_cfg* rc, const uint
     }
     if (prof) {
       const_cast<ts_model*>(m)->prof = nullptr;
-      unsigned long long h[16];
+      unsigned long long h[24];
       TS_CUDA(cudaMemcpyAsync(h, prof_buf, sizeof h, cudaMemcpyDeviceToHost, st));
       TS_CUDA(cudaStreamSynchronize(st));
       const double n = h[10] ? (double)h[10] : 1.0;
@@ -461,6 +461,9 @@ extern "C" int ts_run_chains(const ts_model* m, const ts_run_cfg* rc, const uint
               "TS_PROF evals=%llu wasted=%llu cycles/eval: post-to-result %.0f (pass %.0f [entry %.0f loop %.0f "
               "warpred %.0f ctared %.0f] barrier %.0f reduce %.0f) result-to-next-post %.0f\n",
               h[10], h[11], h[8] / n, h[1] / n, h[4] / n, h[5] / n, h[6] / n, h[7] / n, h[2] / n, h[3] / n, h[9] / n);
+      const double nt = h[14] ? (double)h[14] : 1.0, nx = h[15] ? (double)h[15] : 1.0;
+      fprintf(stderr, "TS_PROF transitions=%llu trees=%llu cycles: prologue/transition %.0f (momentum %.0f)  between-trees/tree %.0f\n",
+              h[15], h[14], h[12] / nx, h[16] / nx, h[13] / nt);
     }
     return TS_OK;
   }

@@ -34,6 +34,7 @@ enum Vid : int {
   V_MSUM,                             // tree momentum sum (output of build_tree)
   V_WMEAN, V_WM2,                     // Welford accumulator
   V_NQ, V_NR, V_NG,                   // speculative next leaf (drifted q, r_half, gradient)
+  V_MSTD,                             // momentum_std = 1/sqrt(inv), refreshed at every mass install
   V_SLOT0                             // NodeStore slots: 5 vectors each
 };
 constexpr int kSlotVecs = 5;  // FQ, FR, CUMF, PQ, PG
@@ -421,6 +422,14 @@ struct Engine {
       copy(d3, s3);
       copy(d4, s4);
     }
+  }
+  // momentum_std (sampler.py:95 draws r0 = N(0,1) * mass.momentum_std)
+  __device__ void refresh_mstd() {
+    const double* inv = v(V_INV);
+    double* m = v(V_MSTD);
+    const int64_t s = ds();
+    for (int d = T.rank(); d < D; d += T.size()) m[d * s] = __ddiv_rn(1.0, __dsqrt_rn(inv[d * s]));
+    T.sync();
   }
   __device__ __forceinline__ void fill(int dst, double x) {
     double* a = v(dst);
@@ -870,11 +879,10 @@ struct Engine {
   // fold(key, 0) (or injected, std normal, component-major with stride inj_ds).
   __device__ void draw_momentum(int rid, Key nkey, const double* inj, int64_t inj_ds) {
     double* r = v(rid);
-    const double* inv = v(V_INV);
+    const double* mstd = v(V_MSTD);  // 1/sqrt(inv), exactly as computed per draw before
     const int64_t s = ds();
     if (inj != nullptr) {
-      for (int d = T.rank(); d < D; d += T.size())
-        r[d * s] = __dmul_rn(inj[d * inj_ds], __ddiv_rn(1.0, __dsqrt_rn(inv[d * s])));
+      for (int d = T.rank(); d < D; d += T.size()) r[d * s] = __dmul_rn(inj[d * inj_ds], mstd[d * s]);
       return;
     }
     if constexpr (Team::kWarp) {
@@ -903,7 +911,7 @@ struct Engine {
         const int want = min(32, D - done);
         const unsigned slow = __ballot_sync(0xffffffffu, !fast) & (want == 32 ? 0xffffffffu : ((1u << want) - 1u));
         const int nfast = slow ? __ffs(slow) - 1 : want;
-        if (lane < nfast) r[(done + lane) * s] = __dmul_rn(z, __ddiv_rn(1.0, __dsqrt_rn(inv[(done + lane) * s])));
+        if (lane < nfast) r[(done + lane) * s] = __dmul_rn(z, mstd[(done + lane) * s]);
         done += nfast;
         w += (uint64_t)nfast;
         if (slow) {  // normal `done` leaves the fast path: replay it sequentially
@@ -913,7 +921,7 @@ struct Engine {
           for (int k = 0; k < (int)(w & 3); ++k) (void)ns.next_u64();
           if ((w & 3) == 0) ns.pos = 4;
           const double zs = ns.normal();
-          if (lane == 0) r[done * s] = __dmul_rn(zs, __ddiv_rn(1.0, __dsqrt_rn(inv[done * s])));
+          if (lane == 0) r[done * s] = __dmul_rn(zs, mstd[done * s]);
           w = (ns.pos == 4) ? ns.c0 * 4 : (ns.c0 - 1) * 4 + (uint64_t)ns.pos;
           done += 1;
         }
@@ -925,7 +933,7 @@ struct Engine {
     ns.init(nkey);
     for (int d = 0; d < D; ++d) {
       const double z = ns.normal();
-      if ((d % T.size()) == T.rank()) r[d * s] = __dmul_rn(z, __ddiv_rn(1.0, __dsqrt_rn(inv[d * s])));
+      if ((d % T.size()) == T.rank()) r[d * s] = __dmul_rn(z, mstd[d * s]);
     }
   }
 
@@ -960,7 +968,13 @@ struct Engine {
   }
 
   __device__ __noinline__ Stats transition(Key key, const double* inj, int64_t inj_ds) {
+    // profiling (CTA 0 driver lane 0): [12] transition prologue, [13] between
+    // trees, [14] trees, [15] transitions
+    const bool tp = prof != nullptr && T.leader();
+    long long t_last = tp ? clock64() : 0;
+    if (tp) prof[15] += 1;
     draw_momentum(V_R0, key_fold(key, 0), inj, inj_ds);
+    if (tp) prof[16] += clock64() - t_last;
     const double h0 = hamiltonian(U0, V_R0);
     Stream gen;
     gen.init(key_fold(key, 1));
@@ -978,7 +992,9 @@ struct Engine {
       const double eps = go_right ? cfg.step : -cfg.step;
       if (go_right) { copy(V_CQ, V_RQ); copy(V_CR, V_RR); copy(V_CG, V_RG); cur_U = RU; }
       else { copy(V_CQ, V_LQ); copy(V_CR, V_LR); copy(V_CG, V_LG); cur_U = LU; }
+      if (tp) { const long long c = clock64(); prof[j == 0 ? 12 : 13] += c - t_last; prof[14] += 1; }
       const TreeOut t = build_tree(j, eps, h0, key_fold(key, 2 + (uint64_t)j));
+      if (tp) t_last = clock64();
       leapfrogs += t.count;
       sum_metro = __dadd_rn(sum_metro, t.sum_metro);
       ev(kEvTreeEnd, j, t.count, t.stop * 16 + (go_right ? 1 : 0), __popc(occupied_mask));
@@ -1155,6 +1171,7 @@ __device__ void run_chain(Engine<Team, Model>& E, Key ck, const RunCfg& rc, cons
         }
         wcount = 0;
         if (E.T.sum(bad) != 0.0) { status = 1; break; }
+        E.refresh_mstd();
       }
     }
     step = exp(log_eps_bar);

@@ -138,6 +138,8 @@ __device__ void do_op(Engine<Team, Model>& E, const OpArgs& A, int chain, bool w
   {
     double* inv = E.v(V_INV);
     for (int d = rk; d < D; d += sz) inv[d * s] = A.inv[d];
+    E.T.sync();
+    E.refresh_mstd();
   }
   E.tr = (A.has_trace && writer) ? const_cast<TraceBuf*>(&A.trace) : nullptr;
   E.n_evals = 0;

@@ -16,10 +16,11 @@ P = int(sys.argv[5]) if len(sys.argv) > 5 else 54
 seed = int(sys.argv[6]) if len(sys.argv) > 6 else 20191222
 x, y = logistic_data_f32(N, P, seed)
 m = ts.logistic_regression_model(ts.LogisticRegressionData(x, y), precision=prec)
-cfg = ts.RunConfig(model={}, num_chains=1, num_warmup=W, num_samples=S, seed=1)
+RUN_SEED = int(os.environ.get("RUN_SEED", "1"))
+cfg = ts.RunConfig(model={}, num_chains=1, num_warmup=W, num_samples=S, seed=RUN_SEED)
 algo = 4 * N * P + N
 for it in range(2):
-    r = ts.run_device(m, cfg, ts.chain_keys(1, 1), 0)
+    r = ts.run_device(m, cfg, ts.chain_keys(RUN_SEED, 1), 0)
     lf = float(r.stats.cpu().numpy()[0][:, 1].sum()); ev = float(r.evals.cpu().numpy()[0])
     print(f"{prec} {N}x{P} run W={W} S={S}: {r.event_ms:.1f} ms, {lf:.0f} leapfrogs, {ev:.0f} passes, "
           f"{r.event_ms*1000/lf:.2f} us/leapfrog, {algo*ev/(r.event_ms/1e3)/1e9:.0f} GB/s", flush=True)

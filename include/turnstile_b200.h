@@ -168,6 +168,12 @@ int ts_run_chains(const ts_model* m, const ts_run_cfg* rc, const uint64_t* chain
 int ts_peer_mailbox_create(ts_model* m, int rank, int world, void* ipc_handle_out);
 int ts_peer_mailbox_connect(ts_model* m, const void* ipc_handles);
 
+/* Test helper for row sharding on one GPU: emulate `vranks` row-sharded ranks
+ * inside one cooperative launch (equal groups of CTAs, each with its own rows,
+ * grid barrier and accumulators, exchanging through in-memory mailboxes with
+ * the same device code as ts_peer_mailbox_*).  1 = off. */
+int ts_model_set_virtual_ranks(ts_model* m, int vranks);
+
 /* Test helper for row sharding: the raw cross-CTA fixed-point totals of ONE
  * potential/gradient evaluation at q_dev over this model's rows (before any
  * peer exchange): words_dev[2*(p+2)+1] uint64 = (hi, lo) pairs for the p

@@ -45,6 +45,7 @@ EXPORTS = (
     "ts_logistic_partial_sums",
     "ts_gemm_tf32_probe",
     "ts_hmc_transition",
+    "ts_model_set_virtual_ranks",
 )
 
 
@@ -100,6 +101,7 @@ def _declare(lib):
     lib.ts_logistic_partial_sums.argtypes = [_P, _P, _P, _P]
     lib.ts_gemm_tf32_probe.argtypes = [_P, _P, _P, _I, _I, _I, _I, _P]
     lib.ts_hmc_transition.argtypes = [_P, ctypes.POINTER(SamplerCfgC), _P, _P, _P, _U64, _U64, _I, _P, _I, _P]
+    lib.ts_model_set_virtual_ranks.argtypes = [_P, _I]
     for name in EXPORTS:
         if name not in ("ts_last_error",):
             getattr(lib, name).restype = _I

@@ -188,8 +188,9 @@ extern "C" int ts_model_create(int kind, int dim, const double* params, int n_pa
       if (cudaMalloc((void**)&m->xt, xbytes) != cudaSuccess) return fail(TS_ECUDA, "cudaMalloc X failed");
       // wide tiles carry their labels; the separate label array is then unused
       if (cudaMalloc((void**)&m->yt, m->wide ? 16 : (size_t)m->ntiles * 32) != cudaSuccess) return fail(TS_ECUDA, "cudaMalloc y failed");
-      if (cudaMalloc((void**)&m->bar, sizeof(unsigned long long)) != cudaSuccess) return fail(TS_ECUDA, "cudaMalloc barrier failed");
-      if (cudaMemset(m->bar, 0, sizeof(unsigned long long)) != cudaSuccess) return fail(TS_ECUDA, "memset barrier failed");
+      // grid-barrier counters: one cache line per (emulated) rank, up to 8
+      if (cudaMalloc((void**)&m->bar, 16 * 8 * sizeof(unsigned long long)) != cudaSuccess) return fail(TS_ECUDA, "cudaMalloc barrier failed");
+      if (cudaMemset(m->bar, 0, 16 * 8 * sizeof(unsigned long long)) != cudaSuccess) return fail(TS_ECUDA, "memset barrier failed");
       // the barrier word doubles as the "X has fp32 subnormals" flag during re-tiling
       if (m->wide)
         k_retile_wide<<<1184, 256>>>(x_dev, y_dev, n_rows, n_feat, m->ntiles, reinterpret_cast<unsigned char*>(m->xt),
@@ -234,6 +235,7 @@ extern "C" int ts_model_destroy(ts_model* m) {
   for (int r = 0; r < m->world; ++r)
     if (m->mail[r] && m->mail[r] != m->mail_local) cudaIpcCloseMemHandle(m->mail[r]);
   if (m->mail_local) cudaFree(m->mail_local);
+  if (m->vmail) cudaFree(m->vmail);
   delete m;
   return TS_OK;
 }
@@ -306,6 +308,15 @@ extern "C" int ts_peer_mailbox_connect(ts_model* m, const void* ipc_handles) {
     m->mail[r] = (unsigned long long*)p;
   }
   m->world = world;
+  return TS_OK;
+}
+
+extern "C" int ts_model_set_virtual_ranks(ts_model* m, int vranks) {
+  if (!m) return set_err(TS_EINVAL, "null model");
+  if (m->kind != TS_LOGISTIC) return set_err(TS_EINVAL, "logistic model only");
+  if (vranks < 1 || vranks > TS_MAX_PEERS) return set_err(TS_EINVAL, "vranks must be in [1, 8]");
+  if (m->world != 0) return set_err(TS_EINVAL, "model already joined a multi-GPU group");
+  m->vranks = vranks;
   return TS_OK;
 }
 

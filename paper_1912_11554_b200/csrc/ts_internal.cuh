@@ -39,6 +39,9 @@ struct ts_model {
   unsigned long long* mail_local;  // this rank's mailbox (+ exchange counter after it)
   unsigned long long* mail[TS_MAX_PEERS];
   unsigned long long* dump;        // transient: ts_logistic_partial_sums output
+  int vranks;                      // test mode: row-sharded ranks emulated in one launch
+  unsigned long long* vmail;       // their mailboxes
+  size_t vmail_words;
   // dense Gaussian (TS_DENSE_GAUSS): params = A (dim x dim, fp64), a32 = tf32-rounded copy
   float* a32;
   unsigned char* dws;  // lockstep workspaces (grown on demand)
@@ -297,6 +300,29 @@ __global__ void __launch_bounds__(256, 1) k_block_op(MW mw, int D, int nslots, i
     mw.red_s = mw.wred + model_scratch;
     mw.cmd = reinterpret_cast<int*>(smem + (int64_t)nvs * D);   // team scratch area
     mw.epoch = 0;
+    {
+      // this CTA's rank-local index and the rank's row range
+      const int64_t units = mw.a.wide ? mw.a.ntiles / kWideGroup : mw.a.ntiles;
+      if (mw.a.vranks > 1) {  // test mode: ranks emulated by groups of CTAs
+        const int V = mw.a.vranks, Gc = (int)gridDim.x / V, vg = (int)blockIdx.x / Gc;
+        mw.a.cta = (int)blockIdx.x % Gc;
+        mw.a.ncta = Gc;
+        mw.a.u_lo = units * vg / V;
+        mw.a.u_hi = units * (vg + 1) / V;
+        mw.a.world = V;
+        mw.a.rank = vg;
+        const int64_t mwords = mail_words(mw.a.p, V);
+        for (int r = 0; r < V; ++r) mw.a.mail[r] = mw.a.vmail + r * mwords;
+        mw.a.mail_epoch = mw.a.vmail + V * mwords;
+        mw.a.pbuf += (int64_t)vg * 3 * (2 * (int64_t)(mw.a.p + 2) + 2);
+        mw.a.bar += 16 * vg;
+      } else {
+        mw.a.cta = (int)blockIdx.x;
+        mw.a.ncta = (int)gridDim.x;
+        mw.a.u_lo = 0;
+        mw.a.u_hi = units;
+      }
+    }
     // exchange index base (row sharding): the pass count of earlier launches
     if (mw.a.world > 0) mw.a.xbase = __ldcg(mw.a.mail_epoch);
     // TMA pipeline region: stages (128-B aligned) | mbarriers | per-ring counters;

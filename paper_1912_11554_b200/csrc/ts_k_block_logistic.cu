@@ -21,6 +21,7 @@ int launch_block_logistic(const ts_model* m, int nslots, OpArgs& A, cudaStream_t
   mw.a.prof = m->prof;
   mw.a.exact_cvt = m->exact_cvt;
   mw.a.dump = m->dump;
+  mw.a.vranks = m->vranks;
   if (m->world > 0) {
     mw.a.world = m->world;
     mw.a.rank = m->rank;
@@ -61,6 +62,21 @@ int launch_block_logistic(const ts_model* m, int nslots, OpArgs& A, cudaStream_t
   if (m->grid > 0 && m->grid < grid) grid = m->grid;
   if (grid > m->ntiles) grid = m->ntiles;
   if (grid < 1) grid = 1;
+  if (m->vranks > 1) {  // emulated ranks: equal CTA groups, one mailbox set per launch
+    grid = grid / m->vranks * m->vranks;
+    if (grid < m->vranks) return set_err(TS_EUNSUPPORTED, "too few CTAs for the emulated ranks");
+    ts_model* mm = const_cast<ts_model*>(m);
+    const size_t words = (size_t)m->vranks * mail_words(m->p, m->vranks) + 16;
+    if (mm->vmail_words < words) {
+      if (mm->vmail) cudaFree(mm->vmail);
+      mm->vmail = nullptr;
+      mm->vmail_words = 0;
+      TS_CUDA(cudaMalloc((void**)&mm->vmail, words * sizeof(unsigned long long)));
+      mm->vmail_words = words;
+    }
+    TS_CUDA(cudaMemsetAsync(mm->vmail, 0, words * sizeof(unsigned long long), st));
+    mw.a.vmail = mm->vmail;
+  }
   if (m->wide) {  // per-CTA NodeStore slot vectors in global memory
     ts_model* mm = const_cast<ts_model*>(m);
     const size_t need_ws = (size_t)grid * kSlotVecs * (nslots < 1 ? 1 : nslots) * D;
@@ -73,9 +89,10 @@ int launch_block_logistic(const ts_model* m, int nslots, OpArgs& A, cudaStream_t
     }
     mw.a.slotws = mm->slotws;
   }
-  TS_CUDA(cudaMemsetAsync(m->bar, 0, sizeof(unsigned long long), st));
-  // rotating fixed-point accumulators start at zero (3 x (2*(p+2) + 2) words)
-  TS_CUDA(cudaMemsetAsync(m->pbuf, 0, 3 * (2 * (size_t)(m->p + 2) + 2) * sizeof(unsigned long long), st));
+  const int nranks = m->vranks > 1 ? m->vranks : 1;
+  TS_CUDA(cudaMemsetAsync(m->bar, 0, 16 * nranks * sizeof(unsigned long long), st));
+  // rotating fixed-point accumulators start at zero (3 x (2*(p+2) + 2) words per rank)
+  TS_CUDA(cudaMemsetAsync(m->pbuf, 0, nranks * 3 * (2 * (size_t)(m->p + 2) + 2) * sizeof(unsigned long long), st));
   int Dv = D, ns = nslots, sc = scratch;
   void* args[] = {&mw, &Dv, &ns, &sc, &A};
   TS_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3((unsigned)grid), dim3(threads), args, smem, st));

@@ -70,6 +70,14 @@ struct LogisticArgs {
   unsigned long long* mail_epoch; // this rank's exchange counter, persistent across launches
   unsigned long long xbase;       // *mail_epoch at kernel start
   unsigned long long* dump;       // optional: raw local totals of the first pass (ts_logistic_partial_sums)
+  // this CTA within its rank: index, CTA count, and the rank's row range in
+  // units of tiles (p <= 64) or of kWideGroup-tile groups (wide); set per CTA
+  int cta, ncta;
+  int64_t u_lo, u_hi;
+  // test mode: `vranks` row-sharded ranks emulated inside one launch (groups
+  // of CTAs exchanging through vmail), see ts_model_set_virtual_ranks
+  int vranks;
+  unsigned long long* vmail;
 };
 
 // Mailbox of one rank: kMailFlags words of flags (flag[src] = 1 + the last
@@ -222,9 +230,9 @@ struct WarpTiles {
 
 __device__ __forceinline__ WarpTiles warp_tiles(const LogisticArgs& a) {
   const int warp = wk_warp(), nwarps = wk_nwarps();
-  const int64_t G = gridDim.x;
-  const int64_t t_begin = (a.ntiles * (int64_t)blockIdx.x) / G;
-  const int64_t t_end = (a.ntiles * ((int64_t)blockIdx.x + 1)) / G;
+  const int64_t G = a.ncta, span = a.u_hi - a.u_lo;
+  const int64_t t_begin = a.u_lo + (span * (int64_t)a.cta) / G;
+  const int64_t t_end = a.u_lo + (span * ((int64_t)a.cta + 1)) / G;
   WarpTiles w;
   w.first = t_begin + warp;
   w.count = (t_end - w.first + nwarps - 1) / nwarps;
@@ -606,8 +614,8 @@ __device__ __noinline__ void logistic_cta_pass_wide(const LogisticArgs& a, const
   WarpTiles wt;
   {
     const int nwarps = wk_nwarps();
-    const int64_t G = gridDim.x, ng = a.ntiles / kWideGroup;
-    const int64_t g_begin = (ng * (int64_t)blockIdx.x) / G, g_end = (ng * ((int64_t)blockIdx.x + 1)) / G;
+    const int64_t G = a.ncta, ng = a.u_hi - a.u_lo;
+    const int64_t g_begin = a.u_lo + (ng * (int64_t)a.cta) / G, g_end = a.u_lo + (ng * ((int64_t)a.cta + 1)) / G;
     wt.first = g_begin + warp;
     wt.count = (g_end - wt.first + nwarps - 1) / nwarps;
     if (wt.count < 0) wt.count = 0;
@@ -825,7 +833,7 @@ static __device__ void logistic_eval_grid(const LogisticArgs& a, const VecStore&
                                           double* red_s, unsigned long long& epoch) {
   const int p = a.p;
   const int P2 = p + 2;
-  const int64_t G = gridDim.x;
+  const int64_t G = a.ncta;  // CTAs of this rank
   const double* theta = S.v(qid);  // smem, contiguous (dstride 1)
   const bool prof = a.prof != nullptr && blockIdx.x == 0 && wk_tid() == 0;
   long long c0 = prof ? clock64() : 0, c1;
@@ -875,7 +883,7 @@ static __device__ void logistic_eval_grid(const LogisticArgs& a, const VecStore&
   wk_sync();
   // buffer (epoch+2)%3 was last read before this barrier by every CTA and is
   // next accumulated after the following barrier: CTA 0 clears it now.
-  if (blockIdx.x == 0) {
+  if (a.cta == 0) {
     unsigned long long* nxt = accb + (int64_t)((epoch + 2) % 3ULL) * bstride;
     for (int i = wk_tid(); i < bstride; i += wk_threads()) nxt[i] = 0ULL;
   }
@@ -896,7 +904,7 @@ static __device__ void logistic_eval_grid(const LogisticArgs& a, const VecStore&
     const unsigned long long x = a.xbase + (epoch - 1);
     const int64_t slot = (int64_t)(x % 3ULL);
     const int nwords = 2 * P2 + 1;
-    if (blockIdx.x == 0) {
+    if (a.cta == 0) {
       for (int i = wk_tid(); i < W * nwords; i += wk_threads()) {
         const int r = i / nwords, w = i - r * nwords;
         unsigned long long v;

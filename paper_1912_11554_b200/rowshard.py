@@ -75,6 +75,15 @@ def connect(spec, rank: int, world: int, all_gather: Callable[[bytes], Sequence[
     spec.row_shard = (rank, world)
 
 
+def emulate_ranks(spec, vranks: int, device=None) -> None:
+    """Test mode: run `vranks` row-sharded ranks inside ONE cooperative launch
+    on one GPU (groups of CTAs with their own rows, barriers and accumulators,
+    exchanging through the same mailbox device code as connect()).  The
+    wide-p model's chain is then bit-identical to the unsharded run."""
+    lib = _lib.load_library()
+    _lib.check(lib.ts_model_set_virtual_ranks(spec.handle(device), int(vranks)))
+
+
 # ----------------------------------------------------------------------------- fixed-point totals
 
 

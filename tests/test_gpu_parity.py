@@ -691,3 +691,28 @@ def test_block_team_runs_every_chain():
     b = t.run_device(m, cfg, keys, 0, exec_mode="block").samples.cpu().numpy()
     assert np.isfinite(b).all()
     assert close(b[:, :3], a[:, :3], BLOCK_REL, atol=BLOCK_REL)
+
+
+def test_row_shard_exchange_emulated_ranks_bitwise():
+    """The multi-GPU exchange device code with 2/4/8 ranks emulated as CTA
+    groups of one launch (row shards, per-rank barriers and accumulators,
+    mailbox push/flags/sum): the wide-p chain is bit-identical to the
+    unsharded one, across launches."""
+    t = ts()
+    from tests_data import logistic_data
+
+    x, y = logistic_data(20005, 255, 21)
+    base = t.logistic_regression_model(t.LogisticRegressionData(x, y), precision="fp32")
+    cfg = t.RunConfig(model={}, num_chains=1, num_warmup=30, num_samples=20, seed=6)
+    keys = t.chain_keys(6, 1)
+    ref = t.run_device(base, cfg, keys, 0)
+    q = np.random.default_rng(2).standard_normal((2, 256)) * 0.05
+    ref_ug = t.models.potential_and_gradient(base.device_spec, q)
+    for V in (2, 4, 8):
+        m = t.logistic_regression_model(t.LogisticRegressionData(x, y), precision="fp32")
+        t.rowshard.emulate_ranks(m.device_spec, V)
+        assert np.array_equal(t.models.potential_and_gradient(m.device_spec, q), ref_ug), V
+        for _ in range(2):
+            r = t.run_device(m, cfg, keys, 0)
+            assert np.array_equal(r.samples.cpu().numpy(), ref.samples.cpu().numpy()), V
+            assert np.array_equal(r.stats.cpu().numpy(), ref.stats.cpu().numpy()), V

@@ -22,6 +22,7 @@ int launch_block_logistic(const ts_model* m, int nslots, OpArgs& A, cudaStream_t
   mw.a.exact_cvt = m->exact_cvt;
   mw.a.dump = m->dump;
   mw.a.vranks = m->vranks;
+  if (const char* e = getenv("TS_ICVT")) mw.a.icvt = atoi(e);  // profiling A/B
   if (m->world > 0) {
     mw.a.world = m->world;
     mw.a.rank = m->rank;

@@ -78,6 +78,7 @@ struct LogisticArgs {
   // of CTAs exchanging through vmail), see ts_model_set_virtual_ranks
   int vranks;
   unsigned long long* vmail;
+  int icvt;  // profiling switch (TS_ICVT): fp64 wide pass converts half of X on the integer pipe
 };
 
 // Mailbox of one rank: kMailFlags words of flags (flag[src] = 1 + the last
@@ -599,7 +600,16 @@ struct WideProducer {
   }
 };
 
-template <bool FP64, int KL>  // KL = features per lane (p <= 32 KL)
+// fp32 -> fp64 on the integer pipe for normal numbers and zeros (X without
+// fp32 subnormals, LogisticArgs::exact_cvt == 0): sign | (exponent + 896) |
+// mantissa, in 5 integer operations, no XU conversion
+__device__ __forceinline__ double f2d_int(float f) {
+  const uint32_t u = __float_as_uint(f);
+  const uint32_t hi = ((uint32_t)((int32_t)u >> 3) & 0x8fffffffu) + ((u << 1) ? 0x38000000u : 0u);
+  return __hiloint2double((int)hi, (int)(u << 29));
+}
+
+template <bool FP64, int KL, bool ICVT = false>  // KL = features per lane (p <= 32 KL); ICVT: odd m on the ALU
 __device__ __noinline__ void logistic_cta_pass_wide(const LogisticArgs& a, const double* __restrict__ theta_s,
                                                     double* wred, double* red_out) {
   using acc_t = typename std::conditional<FP64, double, float>::type;
@@ -686,7 +696,10 @@ __device__ __noinline__ void logistic_cta_pass_wide(const LogisticArgs& a, const
         for (int r = 0; r < R; ++r) {
           const float* xr = xs + (g + r) * p + lane;
 #pragma unroll
-          for (int m = 0; m < KL; ++m) xv[r][m] = (acc_t)xr[32 * m];
+          for (int m = 0; m < KL; ++m) {
+            if constexpr (FP64 && ICVT) xv[r][m] = (m & 1) ? (acc_t)f2d_int(xr[32 * m]) : (acc_t)xr[32 * m];
+            else xv[r][m] = (acc_t)xr[32 * m];
+          }
         }
         const int yr = g + my_r;
         const acc_t yv = (acc_t)sb[32 * p + yr];
@@ -802,7 +815,8 @@ static __device__ __forceinline__ void logistic_cta_dispatch(const LogisticArgs&
       if (a.fp64) logistic_cta_pass_wide<true, 4>(a, theta, wred, red_s);
       else logistic_cta_pass_wide<false, 4>(a, theta, wred, red_s);
     } else {
-      if (a.fp64) logistic_cta_pass_wide<true, 8>(a, theta, wred, red_s);
+      if (a.fp64 && !a.exact_cvt && a.icvt) logistic_cta_pass_wide<true, 8, true>(a, theta, wred, red_s);
+      else if (a.fp64) logistic_cta_pass_wide<true, 8>(a, theta, wred, red_s);
       else logistic_cta_pass_wide<false, 8>(a, theta, wred, red_s);
     }
     return;

@@ -1,2 +1,3 @@
-timeout 600 python -m pytest tests -m gpu -q -x -k "dense or tcgen05" > gpurun_out/t52.log 2>&1
-for i in 1 2 3 4 5 6; do TS_PROF=1 timeout 60 python tools/dense_bench.py tf32 1024 20 10 >> gpurun_out/d13.log 2>&1; echo "iter $i rc=$?" >> gpurun_out/d13.log; done
+TS_ICVT=0 timeout 300 python tools/prof_eval.py fp64 30 8000000 255 20191223 > gpurun_out/ic.log 2>&1
+TS_ICVT=1 timeout 300 python tools/prof_eval.py fp64 30 8000000 255 20191223 >> gpurun_out/ic.log 2>&1
+TS_ICVT=1 timeout 600 python -m pytest tests -m gpu -q -x -k "wide or row_shard" > gpurun_out/t54.log 2>&1

@@ -78,7 +78,7 @@ struct LogisticArgs {
   // of CTAs exchanging through vmail), see ts_model_set_virtual_ranks
   int vranks;
   unsigned long long* vmail;
-  int icvt;  // profiling switch (TS_ICVT): fp64 wide pass converts half of X on the integer pipe
+  int icvt;  // fp64 wide pass: 1 = odd features converted on the integer pipe (default), 0 = all F2F, 2 = all ALU
 };
 
 // Mailbox of one rank: kMailFlags words of flags (flag[src] = 1 + the last
@@ -609,7 +609,7 @@ __device__ __forceinline__ double f2d_int(float f) {
   return __hiloint2double((int)hi, (int)(u << 29));
 }
 
-template <bool FP64, int KL, bool ICVT = false>  // KL = features per lane (p <= 32 KL); ICVT: odd m on the ALU
+template <bool FP64, int KL, int ICVT = 0>  // KL = features per lane (p <= 32 KL); ICVT: 1 odd m / 2 all on the ALU
 __device__ __noinline__ void logistic_cta_pass_wide(const LogisticArgs& a, const double* __restrict__ theta_s,
                                                     double* wred, double* red_out) {
   using acc_t = typename std::conditional<FP64, double, float>::type;
@@ -697,7 +697,7 @@ __device__ __noinline__ void logistic_cta_pass_wide(const LogisticArgs& a, const
           const float* xr = xs + (g + r) * p + lane;
 #pragma unroll
           for (int m = 0; m < KL; ++m) {
-            if constexpr (FP64 && ICVT) xv[r][m] = (m & 1) ? (acc_t)f2d_int(xr[32 * m]) : (acc_t)xr[32 * m];
+            if constexpr (FP64 && ICVT > 0) xv[r][m] = (ICVT == 2 || (m & 1)) ? (acc_t)f2d_int(xr[32 * m]) : (acc_t)xr[32 * m];
             else xv[r][m] = (acc_t)xr[32 * m];
           }
         }
@@ -815,7 +815,8 @@ static __device__ __forceinline__ void logistic_cta_dispatch(const LogisticArgs&
       if (a.fp64) logistic_cta_pass_wide<true, 4>(a, theta, wred, red_s);
       else logistic_cta_pass_wide<false, 4>(a, theta, wred, red_s);
     } else {
-      if (a.fp64 && !a.exact_cvt && a.icvt) logistic_cta_pass_wide<true, 8, true>(a, theta, wred, red_s);
+      if (a.fp64 && !a.exact_cvt && a.icvt == 1) logistic_cta_pass_wide<true, 8, 1>(a, theta, wred, red_s);
+      else if (a.fp64 && !a.exact_cvt && a.icvt == 2) logistic_cta_pass_wide<true, 8, 2>(a, theta, wred, red_s);
       else if (a.fp64) logistic_cta_pass_wide<true, 8>(a, theta, wred, red_s);
       else logistic_cta_pass_wide<false, 8>(a, theta, wred, red_s);
     }

@@ -1,2 +1,2 @@
-for v in 0 1 2; do TS_ICVT=$v timeout 300 python tools/prof_eval.py fp64 30 8000000 255 20191223 >> gpurun_out/ic2.log 2>&1; done
-TS_ICVT=2 timeout 600 python -m pytest tests -m gpu -q -x -k "wide or row_shard" > gpurun_out/t55.log 2>&1
+timeout 600 python -m pytest tests -m gpu -q -x -k "dense or tcgen05" > gpurun_out/t56.log 2>&1
+for i in 1 2; do TS_PROF=1 timeout 120 python tools/dense_bench.py tf32 1024 20 10 >> gpurun_out/d14.log 2>&1; echo "rc=$?" >> gpurun_out/d14.log; done

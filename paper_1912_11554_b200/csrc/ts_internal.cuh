@@ -96,6 +96,7 @@ struct SmallW {
 // command word in shared memory and joins the pass with them.
 struct LogisticW {
   LogisticArgs a;
+  VecStore S;  // the chain's vectors (driver side of post)
   double* wred;
   double* red_s;
   int* cmd;  // smem: [0] 1 = evaluate / 0 = exit, [1] q vector id, [2] gradient vector id
@@ -105,6 +106,15 @@ struct LogisticW {
   // driver warp: post a pass (non-blocking arrive on barrier 2) ...
   __device__ void post(int q, int g) {
     if (threadIdx.x == 0) { cmd[0] = 1; cmd[1] = q; cmd[2] = g; }
+    if (a.th32 != nullptr) {
+      // theta rounded to float for the FP32 pass, by the driver lanes (the
+      // workers then start streaming without a conversion round and two syncs)
+      const double* th = S.v(q);
+      float* t32 = const_cast<float*>(a.th32);
+      for (int j = (int)(threadIdx.x & 31); j <= a.pmax; j += 32)
+        t32[j] = (j < a.p) ? (float)th[j] : (j == a.pmax ? (float)th[a.p] : 0.f);
+      __syncwarp();
+    }
     cta_arrive(2);  // publishes q and the command to the worker warps
   }
   // ... and collect it (barrier 3: gradient written to vector g, U in red_s)
@@ -328,7 +338,10 @@ __global__ void __launch_bounds__(256, 1) k_block_op(MW mw, int D, int nslots, i
     // TMA pipeline region: stages (128-B aligned) | mbarriers | per-ring counters;
     // one ring per worker warp
     const int rings = (int)(blockDim.x >> 5) - 1;
-    uintptr_t pb = reinterpret_cast<uintptr_t>(mw.red_s + mw.a.p + 2);
+    // float copy of theta for the FP32 narrow pass (written by the driver in post)
+    mw.a.th32 = (!mw.a.fp64 && !mw.a.wide) ? reinterpret_cast<const float*>(mw.red_s + ((mw.a.p + 3) & ~1)) : nullptr;
+    mw.S = S;
+    uintptr_t pb = reinterpret_cast<uintptr_t>(mw.red_s + mw.a.p + 2 + (kWideMax + 8) / 2);
     pb = (pb + 127) & ~(uintptr_t)127;
     mw.a.stages = reinterpret_cast<unsigned char*>(pb);
     mw.a.mbar = reinterpret_cast<uint64_t*>(pb + (size_t)rings * mw.a.nstage * mw.a.stage_bytes);

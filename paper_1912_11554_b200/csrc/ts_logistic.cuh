@@ -79,6 +79,7 @@ struct LogisticArgs {
   int vranks;
   unsigned long long* vmail;
   int icvt;  // fp64 wide pass: 1 = odd features converted on the integer pipe (default), 0 = all F2F, 2 = all ALU
+  const float* th32;  // FP32 narrow pass: theta as floats [pmax + 1] (smem, written by the driver before each pass)
 };
 
 // Mailbox of one rank: kMailFlags words of flags (flag[src] = 1 + the last
@@ -367,18 +368,22 @@ __device__ __noinline__ void logistic_cta_pass(const LogisticArgs& a, const doub
   float th32[PMAX];
   float thb32 = 0.f;
   if constexpr (!FP64) {
-    // theta rounded to float once per pass (PMAX+1 conversions per CTA, not
-    // per thread), then broadcast with LDS.128 (wred is free until the end)
-    float* t32 = reinterpret_cast<float*>(wred);
-    for (int j = wk_tid(); j <= PMAX; j += wk_threads()) t32[j] = (j < p) ? (float)theta_s[j] : (j == PMAX ? (float)theta_s[p] : 0.f);
-    wk_sync();
+    // theta as floats, broadcast with LDS.128: prepared by the driver warp
+    // before the post (a.th32), else rounded here once per CTA
+    const float* t32 = a.th32;
+    if (t32 == nullptr || a.pmax != PMAX) {
+      float* w32 = reinterpret_cast<float*>(wred);  // wred is free until the end
+      for (int j = wk_tid(); j <= PMAX; j += wk_threads()) w32[j] = (j < p) ? (float)theta_s[j] : (j == PMAX ? (float)theta_s[p] : 0.f);
+      wk_sync();
+      t32 = w32;
+    }
 #pragma unroll
     for (int j = 0; j < PMAX; j += 4) {
       const float4 v = reinterpret_cast<const float4*>(t32)[j / 4];
       th32[j] = v.x; th32[j + 1] = v.y; th32[j + 2] = v.z; th32[j + 3] = v.w;
     }
     thb32 = t32[PMAX];
-    wk_sync();
+    if (t32 != a.th32 || a.pmax != PMAX) wk_sync();
   }
 
   if (wt.count > 0) {

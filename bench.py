@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--single-precision", action="store_true", help="measure only --precision")
     ap.add_argument("--config", choices=("covtype", "eight_schools", "gauss10", "rowshard", "dense"), default="covtype")
     ap.add_argument("--chains", type=int, default=8192, help="eight_schools: total chains")
+    ap.add_argument("--exec-mode", choices=("thread", "block", "warp"), default=None,
+                    help="eight_schools/gauss10 team layout (default: block for <=16 chains, else thread)")
     ap.add_argument("--num-warmup", type=int, default=1000)
     ap.add_argument("--num-samples", type=int, default=1000)
     ap.add_argument("--seed", type=int, default=1)
@@ -237,6 +239,7 @@ def run_eight_schools(args):
                            num_samples=args.num_samples, seed=3)
         keys = ts.chain_keys(3, C)
     mine = [keys[c] for c in ts.chains.shard_range(C, rank, world)]
+    mode = args.exec_mode or ("block" if len(mine) <= 16 else "thread")
     times, lfs = [], []
     last = None
     for s in range(args.warmup + args.steps):
@@ -245,7 +248,7 @@ def run_eight_schools(args):
         torch.cuda.synchronize()
         # one chain: a CTA per chain (vectors in shared memory) is 2x faster than
         # the one-thread-per-chain layout built for thousands of chains
-        r = ts.run_device(model, cfg, mine, dev, exec_mode="block" if len(mine) <= 16 else "thread")
+        r = ts.run_device(model, cfg, mine, dev, exec_mode=mode)
         if s >= args.warmup:
             times.append(r.event_ms)
             lfs.append(float(r.stats.cpu().numpy()[:, :, 1].sum()))
@@ -267,7 +270,8 @@ def run_eight_schools(args):
             "config": {"workload": (f"eight schools NC, {C} chains" if args.config == "eight_schools"
                                     else "10-D diagonal Gaussian, 1 chain")
                                    + f" x ({args.num_warmup}+{args.num_samples}), "
-                                   + ("one CTA per chain" if len(mine) <= 16 else "one chain per thread")},
+                                   + {"block": "one CTA per chain", "warp": "one warp per chain",
+                                      "thread": "one chain per thread"}[mode]},
             "min_ess_rank0_shard": float(np.nanmin(ess)),
             "ess_per_sec_rank0_shard": float(np.nanmin(ess)) / (t_ms / 1000.0 / args.steps),
         }), flush=True)

@@ -45,8 +45,10 @@ enum { TS_PREC_FP64 = 0, TS_PREC_FP32 = 1, TS_PREC_TF32 = 2 };
 /* U-turn criterion (tree.py:36-37). */
 enum { TS_GENERALIZED = 0, TS_CLASSIC = 1 };
 
-/* Team layout for small models: one chain per thread (default) or per CTA. */
-typedef enum { TS_EXEC_THREAD = 0, TS_EXEC_BLOCK = 1 } ts_exec_mode;
+/* Team layout for small models: one chain per thread (default; the
+ * reference's summation order, bit for bit), per CTA, or per warp (vectors in
+ * shared memory, shuffle-tree reductions: fastest for many small chains). */
+typedef enum { TS_EXEC_THREAD = 0, TS_EXEC_BLOCK = 1, TS_EXEC_WARP = 2 } ts_exec_mode;
 
 /* SamplerConfig (sampler.py:38-59). */
 typedef struct {

@@ -117,6 +117,7 @@ static int launch(const ts_model* m, int nslots, OpArgs& A, int n_threads_chains
   sm.params = m->params;
   const int D = m->dim;
   if (mode == TS_EXEC_BLOCK) return launch_block_small(sm, D, nslots, A, n_threads_chains, st);
+  if (mode == TS_EXEC_WARP) return launch_warp_small(sm, D, nslots, A, n_threads_chains, st);
   return launch_thread(sm, D, n_threads_chains, nslots, A, st);
 }
 
@@ -448,20 +449,28 @@ extern "C" int ts_run_chains(const ts_model* m, const ts_run_cfg* rc, const uint
   A.samples = samples; A.stats = stats; A.adapt = adapt; A.status = status; A.evals = evals;
   cudaStream_t st = (cudaStream_t)stream;
   const int nslots = rc->sampler.max_tree_depth - 1;
-  if (m->kind == TS_LOGISTIC) {
-    // TS_PROF=1: CTA-0 cycle counters of the run, printed to stderr (profiling aid)
-    static unsigned long long* prof_buf = nullptr;
-    const bool prof = getenv("TS_PROF") != nullptr;
-    if (prof) {
-      if (!prof_buf) TS_CUDA(cudaMalloc((void**)&prof_buf, 24 * sizeof(unsigned long long)));
-      TS_CUDA(cudaMemsetAsync(prof_buf, 0, 24 * sizeof(unsigned long long), st));
-      const_cast<ts_model*>(m)->prof = prof_buf;
-    }
+  // TS_PROF=1: chain-0 cycle counters of the run, printed to stderr (profiling
+  // aid; logistic runs and warp-team small-model runs)
+  static unsigned long long* prof_buf = nullptr;
+  const bool prof = getenv("TS_PROF") != nullptr &&
+                    (m->kind == TS_LOGISTIC || (m->kind != TS_DENSE_GAUSS && exec_mode == TS_EXEC_WARP));
+  if (prof) {
+    if (!prof_buf) TS_CUDA(cudaMalloc((void**)&prof_buf, 24 * sizeof(unsigned long long)));
+    TS_CUDA(cudaMemsetAsync(prof_buf, 0, 24 * sizeof(unsigned long long), st));
+  }
+  if (m->kind != TS_LOGISTIC) {
+    A.prof = prof ? prof_buf : nullptr;
+    int e = launch(m, nslots, A, n_chains, (ts_exec_mode)exec_mode, st);
+    if (e || !prof) return e;
+  } else {
+    if (prof) const_cast<ts_model*>(m)->prof = prof_buf;
     for (int c = 0; c < n_chains; ++c) {
       A.n_points = c;
       int e = launch(m, nslots, A, 1, TS_EXEC_BLOCK, st);
       if (e) { const_cast<ts_model*>(m)->prof = nullptr; return e; }
     }
+  }
+  {
     if (prof) {
       const_cast<ts_model*>(m)->prof = nullptr;
       unsigned long long h[24];
@@ -478,7 +487,6 @@ extern "C" int ts_run_chains(const ts_model* m, const ts_run_cfg* rc, const uint
     }
     return TS_OK;
   }
-  return launch(m, nslots, A, n_chains, (ts_exec_mode)exec_mode, st);
 }
 
 // ------------------------------------------------------------------ rng probe

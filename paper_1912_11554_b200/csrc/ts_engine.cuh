@@ -760,6 +760,20 @@ struct Engine {
   // (noinline: separate register allocation per phase keeps the chain state
   // out of local memory, which shares the L1 left over by the TMA stages)
   __device__ __noinline__ TreeOut build_tree(int depth, double eps, double h_ref, Key key) {
+    if constexpr (!Model::kAsync) {
+      // Synchronous (small) models: run the tree on a private copy of the
+      // engine.  Its address never escapes, so the engine's fields stay in
+      // registers instead of being reloaded from the stack after every
+      // vector store (which may alias it through a generic pointer).
+      Engine L = *this;
+      const TreeOut o = L.build_tree_body(depth, eps, h_ref, key);
+      *this = L;
+      return o;
+    } else {
+      return build_tree_body(depth, eps, h_ref, key);
+    }
+  }
+  __device__ __forceinline__ TreeOut build_tree_body(int depth, double eps, double h_ref, Key key) {
     Stream draws;
     draws.init(key);
     occupied_mask = 0;

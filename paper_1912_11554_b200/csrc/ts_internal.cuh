@@ -81,6 +81,7 @@ struct OpArgs {
   double* adapt;    // [C][2+W+D]
   int32_t* status;  // [C]
   int64_t* evals;   // [C]
+  unsigned long long* prof;  // TS_PROF cycle counters (chain 0), or null
 };
 
 struct SmallW {
@@ -371,6 +372,7 @@ __global__ void __launch_bounds__(256, 1) k_block_op(MW mw, int D, int nslots, i
 
 int launch_thread(const SmallModel& sm, int D, int C, int nslots, OpArgs& A, cudaStream_t st);
 int launch_block_small(const SmallModel& sm, int D, int nslots, OpArgs& A, int C, cudaStream_t st);
+int launch_warp_small(const SmallModel& sm, int D, int nslots, OpArgs& A, int C, cudaStream_t st);
 int launch_block_logistic(const ts_model* m, int nslots, OpArgs& A, cudaStream_t st);
 int launch_dense(const ts_model* m, int nslots, OpArgs& A, int n_chains, cudaStream_t st);
 

@@ -190,7 +190,7 @@ def test_small_model_potential_gradient_bitwise(desc, oracle):
         assert close(out[k, 1:], np.asarray(om.gradient(q)), rel, atol=rel)
 
 
-@pytest.mark.parametrize("mode", ["thread", "block"])
+@pytest.mark.parametrize("mode", ["thread", "block", "warp"])
 def test_leapfrog_matches_oracle(mode, oracle):
     t = ts()
     for desc in ({"name": "std_normal", "dim": 3}, {"name": "funnel", "dim": 4}, {"name": "eight_schools"}):
@@ -252,12 +252,12 @@ def _check_tree(case, tree, trace, rel):
     return ints_ok, floats_ok
 
 
-@pytest.mark.parametrize("mode", ["thread", "block"])
+@pytest.mark.parametrize("mode", ["thread", "block", "warp"])
 def test_trees_match_reference(mode):
     cases = golden("trees")
     bad_int, bad_float = [], []
     for i, case in enumerate(cases):
-        if mode == "thread" and case["model"]["name"] == "logistic_regression":
+        if mode != "block" and case["model"]["name"] == "logistic_regression":
             continue  # logistic always runs on the block/grid path
         tree, trace = _run_tree_case(case, mode)
         small = case["model"]["name"] != "logistic_regression"
@@ -297,7 +297,7 @@ def test_trees_fp32_logistic_within_tolerance():
 # ----------------------------------------------------------------------------- transitions
 
 
-@pytest.mark.parametrize("mode", ["thread", "block"])
+@pytest.mark.parametrize("mode", ["thread", "block", "warp"])
 def test_transitions_match_reference(mode):
     t = ts()
     for rec in golden("transitions"):
@@ -691,6 +691,22 @@ def test_block_team_runs_every_chain():
     b = t.run_device(m, cfg, keys, 0, exec_mode="block").samples.cpu().numpy()
     assert np.isfinite(b).all()
     assert close(b[:, :3], a[:, :3], BLOCK_REL, atol=BLOCK_REL)
+
+
+def test_warp_team_runs_every_chain():
+    """exec_mode='warp' runs one warp per chain (8 per CTA, vectors in shared
+    memory): a chain count that is not a multiple of 8, every chain's draws
+    and stats match the thread-team run to the shuffle-reduction tolerance."""
+    t = ts()
+    for m, D in ((t.eight_schools_model(), 10), (t.gaussian_model(np.logspace(-1, 1, 40)), 40)):
+        cfg = t.RunConfig(model={}, num_chains=37, num_warmup=0, num_samples=4, seed=13,
+                          sampler=t.SamplerConfig(step_size=0.2, mass=t.MassMatrix.identity(D)))
+        keys = t.chain_keys(13, 37)
+        a = t.run_device(m, cfg, keys, 0, exec_mode="thread")
+        b = t.run_device(m, cfg, keys, 0, exec_mode="warp")
+        sa, sb = a.samples.cpu().numpy(), b.samples.cpu().numpy()
+        assert np.isfinite(sb).all()
+        assert close(sb[:, :2], sa[:, :2], BLOCK_REL, atol=BLOCK_REL)
 
 
 def test_row_shard_exchange_emulated_ranks_bitwise():

@@ -57,7 +57,7 @@ def parse():
     ap.add_argument("--config", choices=("covtype", "eight_schools", "gauss10", "rowshard", "dense"), default="covtype")
     ap.add_argument("--chains", type=int, default=8192, help="eight_schools: total chains")
     ap.add_argument("--exec-mode", choices=("thread", "block", "warp"), default=None,
-                    help="eight_schools/gauss10 team layout (default: block for <=16 chains, else thread)")
+                    help="eight_schools/gauss10 team layout (default: warp for <=16 chains, else thread)")
     ap.add_argument("--num-warmup", type=int, default=1000)
     ap.add_argument("--num-samples", type=int, default=1000)
     ap.add_argument("--seed", type=int, default=1)
@@ -239,15 +239,15 @@ def run_eight_schools(args):
                            num_samples=args.num_samples, seed=3)
         keys = ts.chain_keys(3, C)
     mine = [keys[c] for c in ts.chains.shard_range(C, rank, world)]
-    mode = args.exec_mode or ("block" if len(mine) <= 16 else "thread")
+    # one chain: a warp per chain (vectors in shared memory) is ~2x faster than
+    # the one-thread-per-chain layout built for thousands of chains
+    mode = args.exec_mode or ("warp" if len(mine) <= 16 else "thread")
     times, lfs = [], []
     last = None
     for s in range(args.warmup + args.steps):
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
-        # one chain: a CTA per chain (vectors in shared memory) is 2x faster than
-        # the one-thread-per-chain layout built for thousands of chains
         r = ts.run_device(model, cfg, mine, dev, exec_mode=mode)
         if s >= args.warmup:
             times.append(r.event_ms)

@@ -415,12 +415,23 @@ struct Engine {
         return;
       }
     }
-    copy(d0, s0);
-    copy(d1, s1);
-    copy(d2, s2);
-    if (d3 >= 0) {
-      copy(d3, s3);
-      copy(d4, s4);
+    // one loop, all loads of an element before its stores (the groups never
+    // copy into a vector another member of the group reads)
+    double* a0 = v(d0); double* a1 = v(d1); double* a2 = v(d2);
+    const double* b0 = v(s0); const double* b1 = v(s1); const double* b2 = v(s2);
+    const int64_t s = ds();
+    if (d3 < 0) {
+      for (int d = T.rank(); d < D; d += T.size()) {
+        const double x0 = b0[d * s], x1 = b1[d * s], x2 = b2[d * s];
+        a0[d * s] = x0; a1[d * s] = x1; a2[d * s] = x2;
+      }
+      return;
+    }
+    double* a3 = v(d3); double* a4 = v(d4);
+    const double* b3 = v(s3); const double* b4 = v(s4);
+    for (int d = T.rank(); d < D; d += T.size()) {
+      const double x0 = b0[d * s], x1 = b1[d * s], x2 = b2[d * s], x3 = b3[d * s], x4 = b4[d * s];
+      a0[d * s] = x0; a1[d * s] = x1; a2[d * s] = x2; a3[d * s] = x3; a4[d * s] = x4;
     }
   }
   // momentum_std (sampler.py:95 draws r0 = N(0,1) * mass.momentum_std)
@@ -537,8 +548,7 @@ struct Engine {
       copy_group(V_FQ, V_CQ, V_FR, V_CR, V_CUMF, V_CUM, V_TPQ, V_CQ, V_TPG, V_CG);
       f_alias = -1;
     } else {
-      copy(V_TPQ, V_CQ);
-      copy(V_TPG, V_CG);
+      copy_group(V_TPQ, V_CQ, V_TPG, V_CG, V_TPG, V_CG);
     }
     r_lw = lw; r_metro = metro; r_count = 1; r_pU = cur_U; r_pH = h; r_pidx = n; r_fU = cur_U;
   }
@@ -549,8 +559,7 @@ struct Engine {
     const double lw = logaddexp_inner(L.lw, r_lw);
     const double p_right = (r_lw == -kInf()) ? 0.0 : exp(__dsub_rn(r_lw, lw));
     if (!(u < p_right)) {
-      copy(V_TPQ, slot_vec(s, 3));
-      copy(V_TPG, slot_vec(s, 4));
+      copy_group(V_TPQ, slot_vec(s, 3), V_TPG, slot_vec(s, 4), V_TPG, slot_vec(s, 4));
       r_pU = L.pU; r_pH = L.pH; r_pidx = L.pidx;
     }
     // first / cum_first come from the left (stored) subtree: alias, no copy
@@ -748,7 +757,7 @@ struct Engine {
       --slot;
     }
     // summaries[i_min] = running: first/cum_first already equal slot i_min's
-    copy(slot_vec(i_min, 3), V_TPQ); copy(slot_vec(i_min, 4), V_TPG);
+    copy_group(slot_vec(i_min, 3), V_TPQ, slot_vec(i_min, 4), V_TPG, slot_vec(i_min, 4), V_TPG);
     SlotScalars& L = ss[i_min];
     L.lw = r_lw; L.metro = r_metro; L.pU = r_pU; L.pH = r_pH; L.count = r_count; L.pidx = r_pidx;
     return kStopNone;
@@ -982,6 +991,18 @@ struct Engine {
   }
 
   __device__ __noinline__ Stats transition(Key key, const double* inj, int64_t inj_ds) {
+    if constexpr (!Model::kAsync) {
+      // synchronous models: the whole transition (trees inlined) on a
+      // register-resident copy of the engine, as in build_tree
+      Engine L = *this;
+      const Stats st = L.transition_body(key, inj, inj_ds);
+      *this = L;
+      return st;
+    } else {
+      return transition_body(key, inj, inj_ds);
+    }
+  }
+  __device__ __forceinline__ Stats transition_body(Key key, const double* inj, int64_t inj_ds) {
     // profiling (CTA 0 driver lane 0): [12] transition prologue, [13] between
     // trees, [14] trees, [15] transitions
     const bool tp = prof != nullptr && T.leader();
@@ -992,10 +1013,9 @@ struct Engine {
     const double h0 = hamiltonian(U0, V_R0);
     Stream gen;
     gen.init(key_fold(key, 1));
-    copy(V_LQ, V_Q0); copy(V_LR, V_R0); copy(V_LG, V_G0); LU = U0;
-    copy(V_RQ, V_Q0); copy(V_RR, V_R0); copy(V_RG, V_G0); RU = U0;
-    copy(V_PQ, V_Q0); copy(V_PG, V_G0); pU = U0; pH = h0; p_tree = -1; p_leaf = -1;
-    copy(V_RHO, V_R0);
+    copy_group(V_LQ, V_Q0, V_LR, V_R0, V_LG, V_G0, V_RQ, V_Q0, V_RR, V_R0);
+    copy_group(V_RG, V_G0, V_PQ, V_Q0, V_PG, V_G0, V_RHO, V_R0, V_RHO, V_R0);
+    LU = U0; RU = U0; pU = U0; pH = h0; p_tree = -1; p_leaf = -1;
     double lw = -h0;
     int leapfrogs = 0;
     double sum_metro = 0.0;
@@ -1004,10 +1024,12 @@ struct Engine {
     for (int j = 0; j < cfg.max_depth; ++j) {
       const bool go_right = gen.next_double() < 0.5;
       const double eps = go_right ? cfg.step : -cfg.step;
-      if (go_right) { copy(V_CQ, V_RQ); copy(V_CR, V_RR); copy(V_CG, V_RG); cur_U = RU; }
-      else { copy(V_CQ, V_LQ); copy(V_CR, V_LR); copy(V_CG, V_LG); cur_U = LU; }
+      if (go_right) { copy_group(V_CQ, V_RQ, V_CR, V_RR, V_CG, V_RG); cur_U = RU; }
+      else { copy_group(V_CQ, V_LQ, V_CR, V_LR, V_CG, V_LG); cur_U = LU; }
       if (tp) { const long long c = clock64(); prof[j == 0 ? 12 : 13] += c - t_last; prof[14] += 1; }
-      const TreeOut t = build_tree(j, eps, h0, key_fold(key, 2 + (uint64_t)j));
+      TreeOut t;
+      if constexpr (!Model::kAsync) t = build_tree_body(j, eps, h0, key_fold(key, 2 + (uint64_t)j));
+      else t = build_tree(j, eps, h0, key_fold(key, 2 + (uint64_t)j));
       if (tp) t_last = clock64();
       leapfrogs += t.count;
       sum_metro = __dadd_rn(sum_metro, t.sum_metro);
@@ -1020,7 +1042,7 @@ struct Engine {
       const double u = gen.next_double();
       const bool take = (t.lw >= lw) || (u < exp(__dsub_rn(t.lw, lw)));
       if (take) {
-        copy(V_PQ, V_TPQ); copy(V_PG, V_TPG); pU = t.pU; pH = t.pH; p_tree = j; p_leaf = t.pidx;
+        copy_group(V_PQ, V_TPQ, V_PG, V_TPG, V_PG, V_TPG); pU = t.pU; pH = t.pH; p_tree = j; p_leaf = t.pidx;
       }
       ev(kEvProposal, j, t.pidx, take ? 1 : 0);
       lw = logaddexp_np(lw, t.lw);
@@ -1030,8 +1052,8 @@ struct Engine {
         const int64_t s = ds();
         for (int d = T.rank(); d < D; d += T.size()) rho[d * s] = __dadd_rn(rho[d * s], ms[d * s]);
       }
-      if (go_right) { copy(V_RQ, V_CQ); copy(V_RR, V_CR); copy(V_RG, V_CG); RU = cur_U; }
-      else { copy(V_LQ, V_CQ); copy(V_LR, V_CR); copy(V_LG, V_CG); LU = cur_U; }
+      if (go_right) { copy_group(V_RQ, V_CQ, V_RR, V_CR, V_RG, V_CG); RU = cur_U; }
+      else { copy_group(V_LQ, V_CQ, V_LR, V_CR, V_LG, V_CG); LU = cur_U; }
       depth_reached = j + 1;
       bool turned;
       if (cfg.generalized) {
@@ -1053,7 +1075,7 @@ struct Engine {
     st.diverged = diverged ? 1 : 0;
     st.accept = leapfrogs ? __ddiv_rn(sum_metro, (double)leapfrogs) : 0.0;
     st.energy = pH;
-    copy(V_Q0, V_PQ); copy(V_G0, V_PG); U0 = pU;
+    copy_group(V_Q0, V_PQ, V_G0, V_PG, V_G0, V_PG); U0 = pU;
     return st;
   }
 

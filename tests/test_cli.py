@@ -151,3 +151,66 @@ def test_bench_reports(model_file, tmp_path, capsys):
     doc = json.loads(out.read_text())
     assert doc["builders"]["iterative"]["time_per_leapfrog_ns"] > 0
     assert set(doc["tree_microbench"]["ns_per_leapfrog"]) == {"thread", "block", "warp"}
+
+
+def _close(a, b, rel):
+    a, b = np.asarray(a, dtype=np.float64), np.asarray(b, dtype=np.float64)
+    return a.shape == b.shape and bool(np.allclose(a, b, rtol=rel, atol=rel, equal_nan=True))
+
+
+@pytest.mark.gpu
+def test_sample_outputs_match_reference_cli(tmp_path):
+    """The reference CLI's own CSV and JSON report (tests/golden/cli.json,
+    made by tests/golden/make_cli_golden.py) reproduced through our CLI:
+    format, chain ids, per-chain integer statistics (leapfrogs, divergences,
+    max depth) exact; draws and summary floats within 1e-10 (small models on
+    the thread team are bit-identical up to last-ulp exp/log1p; the logistic
+    fp64 pass differs in summation order only)."""
+    from conftest import golden
+
+    g = golden("cli")
+    (tmp_path / "data.csv").write_text(g["data_csv"])
+    for case in g["cases"]:
+        mpath = tmp_path / "model.json"
+        mpath.write_text(json.dumps(case["desc"]))
+        base = ["sample", "--model", str(mpath)] + case["args"]
+        assert cli.main(base + ["--out", str(tmp_path / "s.csv")]) == 0
+        assert cli.main(base + ["--out", str(tmp_path / "r.json")]) == 0
+        ours = (tmp_path / "s.csv").read_text().splitlines()
+        ref = case["csv"].splitlines()
+        assert ours[0] == ref[0] and len(ours) == len(ref), case["desc"]
+        assert [ln.split(",")[0] for ln in ours] == [ln.split(",")[0] for ln in ref]
+        assert _close([[float(v) for v in ln.split(",")[1:]] for ln in ours[1:]],
+                      [[float(v) for v in ln.split(",")[1:]] for ln in ref[1:]], 1e-10), case["desc"]
+        doc = strip_timing(json.loads((tmp_path / "r.json").read_text()))
+        rdoc = case["report"]
+        assert doc["schema_version"] == rdoc["schema_version"]
+        assert doc["model"] == rdoc["model"] and doc["run"] == rdoc["run"]
+        assert set(doc["summary"]) == set(rdoc["summary"])
+        assert doc["summary"]["total_leapfrogs"] == rdoc["summary"]["total_leapfrogs"]
+        assert doc["summary"]["divergences"] == rdoc["summary"]["divergences"]
+        for k in ("mean", "std", "ess", "split_rhat"):
+            assert _close(doc["summary"][k], rdoc["summary"][k], 1e-8), (case["desc"], k)
+        for c, rc in zip(doc["chains"], rdoc["chains"], strict=True):
+            assert set(c) == set(rc)
+            for k in ("chain_id", "divergences", "total_leapfrogs", "sampling_leapfrogs", "max_depth_reached"):
+                assert c[k] == rc[k], (case["desc"], k)
+            assert _close(c["mean_accept_stat"], rc["mean_accept_stat"], 1e-10)
+            assert _close(c["samples"], rc["samples"], 1e-10)
+            assert c["adaptation"] == rc["adaptation"]
+
+
+def test_cli_golden_fixture_is_consistent():
+    """CPU check of the committed reference fixture: CSV rows and report
+    samples agree, and the logistic data are fp32-exact."""
+    from conftest import golden
+
+    g = golden("cli")
+    assert len(g["cases"]) == 4
+    for case in g["cases"]:
+        rows = case["csv"].splitlines()[1:]
+        samples = [s for ch in case["report"]["chains"] for s in ch["samples"]]
+        assert np.array_equal([[float(v) for v in ln.split(",")[1:]] for ln in rows], samples)
+    for ln in g["data_csv"].splitlines()[1:]:
+        x = [float(v) for v in ln.split(",")[:-1]]
+        assert np.array_equal(np.float32(x).astype(np.float64), x)

@@ -251,3 +251,30 @@ def run(config: RunConfig, model: Optional[TargetModel] = None, devices: Optiona
         if shards[g]:
             results += _results(shards[g], runs[g], config, model.dim, wall)
     return results
+
+
+def run_dense_adapted(precision_matrix, config: RunConfig, pilot: Optional[RunConfig] = None,
+                      precision: str = "tf32", device=None):
+    """Dense-mass NUTS for the correlated-Gaussian model in two device runs.
+
+    1. pilot run (identity mass, step-size warmup) of ``pilot`` (default:
+       ``config``) - its draws stay in HBM;
+    2. ``pooled_covariance`` of the pilot draws over all chains (regularised)
+       becomes the dense inverse mass M^-1;
+    3. the sampling run of ``config`` on ``dense_gaussian_model(P, M^-1)``.
+
+    Returns (model, inv_mass (D, D) numpy, DeviceRun).  The reference adapts
+    a diagonal mass per chain only (adapt.py:73-108); this is SURVEY.md 8(f)
+    item 3, pooled across the chains of config 4.
+    """
+    from .adapt import pooled_covariance
+    from .models import dense_gaussian_model
+
+    pilot = config if pilot is None else pilot
+    keys = chain_keys(pilot.seed, pilot.num_chains)
+    first = run_device(dense_gaussian_model(precision_matrix, precision=precision), pilot, keys, device)
+    _, cov = pooled_covariance(first.samples, regularize=True)
+    inv_mass = cov.cpu().numpy()
+    model = dense_gaussian_model(precision_matrix, inv_mass=inv_mass, precision=precision)
+    final = run_device(model, config, chain_keys(config.seed + 1, config.num_chains), device)
+    return model, inv_mass, final

@@ -732,3 +732,52 @@ def test_row_shard_exchange_emulated_ranks_bitwise():
             r = t.run_device(m, cfg, keys, 0)
             assert np.array_equal(r.samples.cpu().numpy(), ref.samples.cpu().numpy()), V
             assert np.array_equal(r.stats.cpu().numpy(), ref.stats.cpu().numpy()), V
+
+
+# ----------------------------------------------------------------------------- dense mass adaptation (8(f) item 3)
+
+
+def test_pooled_covariance_matches_numpy():
+    """Device pooled covariance vs numpy (ddof 1) on a ragged D (not a tile
+    multiple) and an odd row count; regularised shrinkage; bitwise determinism."""
+    import torch
+
+    t = ts()
+    gen = np.random.default_rng(3)
+    n, D = 4999, 150
+    x = gen.standard_normal((n, D)) @ gen.standard_normal((D, D)) * 0.3 + gen.standard_normal(D)
+    xd = torch.from_numpy(x).cuda()
+    mean, cov = t.pooled_covariance(xd, regularize=False)
+    ref = np.cov(x.T)
+    assert close(mean.cpu().numpy(), x.mean(0), 1e-12, atol=1e-12)
+    assert np.abs(cov.cpu().numpy() - ref).max() <= 1e-12 * np.abs(ref).max()
+    assert np.array_equal(cov.cpu().numpy(), cov.cpu().numpy().T)
+    _, reg = t.pooled_covariance(xd.reshape(7, n // 7, D) if n % 7 == 0 else xd, regularize=True)
+    want = (n / (n + 5.0)) * ref + (5.0 / (n + 5.0)) * 1e-3 * np.eye(D)
+    assert np.abs(reg.cpu().numpy() - want).max() <= 1e-12 * np.abs(want).max()
+    _, again = t.pooled_covariance(xd, regularize=True)
+    assert torch.equal(reg, again)
+    # (C, S, D) input pools over chains
+    _, c3 = t.pooled_covariance(xd[:4998].reshape(2, 2499, D), regularize=False)
+    assert np.abs(c3.cpu().numpy() - np.cov(x[:4998].T)).max() <= 1e-12 * np.abs(ref).max()
+
+
+def test_dense_mass_adaptation_two_phase():
+    """Pilot run -> pooled covariance of its draws -> dense inverse mass:
+    the adapted M^-1 approximates the target covariance and the adapted run
+    needs fewer leapfrogs per draw than the identity-mass pilot."""
+    t = ts()
+    D, C = 24, 64
+    A = _spd(D, 9, cond=300.0)
+    cov = np.linalg.inv(A)
+    cfg = t.RunConfig(model={}, num_chains=C, num_warmup=200, num_samples=200, seed=5)
+    model, inv_mass, final = t.run_dense_adapted(A, cfg, precision="fp64", device=0)
+    assert model.params["dense_mass"]
+    err = np.linalg.norm(inv_mass - cov) / np.linalg.norm(cov)
+    assert err < 0.2, err
+    pilot = t.run_device(t.dense_gaussian_model(A, precision="fp64"), cfg, t.chain_keys(5, C), 0)
+    lf_pilot = pilot.stats.cpu().numpy()[:, 200:, 1].mean()
+    lf_final = final.stats.cpu().numpy()[:, 200:, 1].mean()
+    assert lf_final < 0.7 * lf_pilot, (lf_final, lf_pilot)
+    flat = final.samples.cpu().numpy().reshape(-1, D)
+    assert np.abs(np.cov(flat.T) - cov).max() <= 0.15 * np.abs(cov).max()

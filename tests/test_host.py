@@ -285,3 +285,13 @@ def test_ess_device_matches_host_estimator():
         for i in range(1, shape[1]):
             x[:, i] = 0.7 * x[:, i - 1] + x[:, i]
         assert np.allclose(t.ess_device(torch.from_numpy(x)), t.ess(x), rtol=1e-12)
+
+
+def test_pooled_covariance_has_no_cpu_path():
+    import numpy as np
+    import pytest
+
+    import paper_1912_11554_b200 as t
+
+    with pytest.raises((ValueError, RuntimeError)):
+        t.pooled_covariance(np.zeros((4, 3)))

@@ -200,12 +200,12 @@ int ts_rng_probe(uint64_t key_hi, uint64_t key_lo, int kind, int n, double* out_
  * over chains): mean_dev[D] and cov_dev[D*D] with ddof = 1; regularize != 0
  * applies the shrinkage of welford_regularized_variance (adapt.py:91-94) to
  * the full matrix: n/(n+5) cov + 5/(n+5) 1e-3 I.  work_dev holds
- * ts_pooled_covariance_workspace(D) doubles.  Deterministic (no atomics).
+ * ts_pooled_covariance_workspace(n_rows, D) doubles.  Deterministic (no atomics).
  * Extends adapt.py:73-108 (diagonal, per chain) to a dense mass pooled
  * across chains - no reference entry point is replaced. */
 int ts_pooled_covariance(const double* x_dev, int64_t n_rows, int D, int regularize, double* mean_dev,
                          double* cov_dev, double* work_dev, void* stream);
-int64_t ts_pooled_covariance_workspace(int D);
+int64_t ts_pooled_covariance_workspace(int64_t n_rows, int D);
 
 #ifdef __cplusplus
 }

@@ -105,7 +105,7 @@ def _declare(lib):
     lib.ts_hmc_transition.argtypes = [_P, ctypes.POINTER(SamplerCfgC), _P, _P, _P, _U64, _U64, _I, _P, _I, _P]
     lib.ts_model_set_virtual_ranks.argtypes = [_P, _I]
     lib.ts_pooled_covariance.argtypes = [_P, ctypes.c_int64, _I, _I, _P, _P, _P, _P]
-    lib.ts_pooled_covariance_workspace.argtypes = [_I]
+    lib.ts_pooled_covariance_workspace.argtypes = [ctypes.c_int64, _I]
     for name in EXPORTS:
         if name not in ("ts_last_error",):
             getattr(lib, name).restype = _I

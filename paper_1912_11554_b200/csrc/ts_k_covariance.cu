@@ -12,10 +12,13 @@
 //   k_colsum_partial : grid (D/128, kChunks), each thread one column of one
 //                      row chunk -> partial[chunk][D] (coalesced row reads)
 //   k_colmean        : fixed-order sum over chunks -> mean[D]
-//   k_cov_tile       : one CTA per 64x64 lower-triangular output tile; rows
-//                      streamed in 16-row slabs through shared memory, centred
+//   k_cov_tile       : one CTA per (64x64 lower-triangular output tile, row
+//                      split); rows streamed in 16-row slabs through shared
+//                      memory (next slab prefetched into registers), centred
 //                      on load; 4x4 fp64 register micro-tile per thread with
-//                      explicit __fma_rn; the tile and its mirror are stored.
+//                      explicit __fma_rn -> one partial tile per split
+//   k_cov_finish     : fixed-order sum over splits, scaling, mirror store.
+// Splits give ~6 resident CTAs per SM whatever D is.
 // Bound: the FP64 pipe (2 N D^2 / 2 flops for the triangle); the samples are
 // L2-resident re-reads across tiles (N x D x 8 B in HBM once per tile row).
 
@@ -47,15 +50,23 @@ __global__ void k_colmean(const double* __restrict__ partial, int64_t n, int D, 
   mean[d] = s / (double)n;
 }
 
-__global__ void __launch_bounds__(256) k_cov_tile(const double* __restrict__ x, const double* __restrict__ mean,
-                                                  int64_t n, int D, int regularize, double* __restrict__ cov) {
-  // linear triangle index -> (ti, tj) with tj <= ti
-  const int t = blockIdx.x;
-  int ti = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+__device__ __forceinline__ void tri_index(int t, int& ti, int& tj) {
+  ti = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
   while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
   while (ti * (ti + 1) / 2 > t) --ti;
-  const int tj = t - ti * (ti + 1) / 2;
+  tj = t - ti * (ti + 1) / 2;
+}
+
+// blockIdx.x: lower-triangular tile, blockIdx.y: row split.  Writes the
+// split's raw centred cross-product tile to part[split][tile][64*64].
+__global__ void __launch_bounds__(256, 3) k_cov_tile(const double* __restrict__ x, const double* __restrict__ mean,
+                                                  int64_t n, int D, int64_t rows_per_split,
+                                                  double* __restrict__ part) {
+  int ti, tj;
+  tri_index(blockIdx.x, ti, tj);
   const int i0 = ti * kTile, j0 = tj * kTile;
+  const int64_t rbeg = (int64_t)blockIdx.y * rows_per_split;
+  const int64_t rend = rbeg + rows_per_split < n ? rbeg + rows_per_split : n;
 
   __shared__ double As[kSlab][kTile];
   __shared__ double Bs[kSlab][kTile];
@@ -66,20 +77,31 @@ __global__ void __launch_bounds__(256) k_cov_tile(const double* __restrict__ x, 
 #pragma unroll
     for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
 
-  // loader: 256 threads x 4 elements = one 16 x 64 slab per operand
-  const int lc = threadIdx.x & 63, lr = threadIdx.x >> 6;  // column, row 0..3 (+4 k)
-  const double mi = (i0 + lc < D) ? mean[i0 + lc] : 0.0;
-  const double mj = (j0 + lc < D) ? mean[j0 + lc] : 0.0;
-  for (int64_t r0 = 0; r0 < n; r0 += kSlab) {
+  // loader: 256 threads x 4 elements = one 16 x 64 slab per operand; the
+  // next slab is fetched into registers while the current one is consumed
+  const int lc = threadIdx.x & 63, lr = threadIdx.x >> 6;
+  const bool ci = i0 + lc < D, cj = j0 + lc < D;
+  const double mi = ci ? mean[i0 + lc] : 0.0;
+  const double mj = cj ? mean[j0 + lc] : 0.0;
+  double ra[4], rb[4];
+  auto fetch = [&](int64_t r0) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const int rr = lr + 4 * k;
-      const int64_t r = r0 + rr;
-      const bool rin = r < n;
-      As[rr][lc] = (rin && i0 + lc < D) ? x[r * D + i0 + lc] - mi : 0.0;
-      Bs[rr][lc] = (rin && j0 + lc < D) ? x[r * D + j0 + lc] - mj : 0.0;
+      const int64_t r = r0 + lr + 4 * k;
+      const bool rin = r < rend;
+      ra[k] = (rin && ci) ? x[r * D + i0 + lc] - mi : 0.0;
+      rb[k] = (rin && cj) ? x[r * D + j0 + lc] - mj : 0.0;
+    }
+  };
+  if (rbeg < rend) fetch(rbeg);
+  for (int64_t r0 = rbeg; r0 < rend; r0 += kSlab) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      As[lr + 4 * k][lc] = ra[k];
+      Bs[lr + 4 * k][lc] = rb[k];
     }
     __syncthreads();
+    if (r0 + kSlab < rend) fetch(r0 + kSlab);
 #pragma unroll
     for (int k = 0; k < kSlab; ++k) {
       double av[4], bv[4];
@@ -94,23 +116,40 @@ __global__ void __launch_bounds__(256) k_cov_tile(const double* __restrict__ x, 
     }
     __syncthreads();
   }
+  double* out = part + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * (kTile * kTile);
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) out[(ty + 16 * a) * kTile + tx + 16 * b] = acc[a][b];
+}
+
+// Fixed-order sum over splits, ddof-1 scaling, optional shrinkage, mirror.
+__global__ void k_cov_finish(const double* __restrict__ part, int tiles, int splits, int64_t n, int D,
+                             int regularize, double* __restrict__ cov) {
+  int ti, tj;
+  tri_index(blockIdx.x, ti, tj);
   const double inv = 1.0 / (double)(n - 1);
   const double shrink = regularize ? (double)n / ((double)n + 5.0) : 1.0;
   const double ridge = regularize ? 1e-3 * (5.0 / ((double)n + 5.0)) : 0.0;
-#pragma unroll
-  for (int a = 0; a < 4; ++a) {
-    const int i = i0 + ty + 16 * a;
-    if (i >= D) continue;
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const int j = j0 + tx + 16 * b;
-      if (j >= D || j > i) continue;
-      double v = acc[a][b] * inv * shrink;
-      if (i == j) v += ridge;
-      cov[(int64_t)i * D + j] = v;
-      cov[(int64_t)j * D + i] = v;
-    }
+  for (int e = threadIdx.x; e < kTile * kTile; e += blockDim.x) {
+    const int i = ti * kTile + e / kTile, j = tj * kTile + e % kTile;
+    if (i >= D || j >= D || j > i) continue;
+    double s = 0.0;
+    for (int sp = 0; sp < splits; ++sp) s += part[((int64_t)sp * tiles + blockIdx.x) * (kTile * kTile) + e];
+    double v = s * inv * shrink;
+    if (i == j) v += ridge;
+    cov[(int64_t)i * D + j] = v;
+    cov[(int64_t)j * D + i] = v;
   }
+}
+
+int cov_splits(int64_t n, int D) {
+  const int nt = (D + kTile - 1) / kTile;
+  const int tiles = nt * (nt + 1) / 2;
+  int64_t s = (6 * 148 + tiles - 1) / tiles;           // ~6 resident CTAs per SM
+  const int64_t max_s = (n + 8 * kSlab - 1) / (8 * kSlab);  // >= 8 slabs per split
+  if (s > max_s) s = max_s;
+  return s < 1 ? 1 : (int)s;
 }
 
 }  // namespace
@@ -121,15 +160,27 @@ extern "C" int ts_pooled_covariance(const double* x_dev, int64_t n_rows, int D, 
     return ts_internal::set_err(TS_EINVAL, "bad covariance arguments");
   if (n_rows < 2) return ts_internal::set_err(TS_EINVAL, "covariance needs at least two draws");
   cudaStream_t st = (cudaStream_t)stream;
+  // workspace: [kChunks * D] column partial sums, then the split tiles
+  double* part = work_dev + (int64_t)kChunks * D;
   k_colsum_partial<<<dim3((D + kColThreads - 1) / kColThreads, kChunks), kColThreads, 0, st>>>(x_dev, n_rows, D,
                                                                                                work_dev);
   TS_CUDA(cudaGetLastError());
   k_colmean<<<(D + 127) / 128, 128, 0, st>>>(work_dev, n_rows, D, mean_dev);
   TS_CUDA(cudaGetLastError());
   const int nt = (D + kTile - 1) / kTile;
-  k_cov_tile<<<nt * (nt + 1) / 2, 256, 0, st>>>(x_dev, mean_dev, n_rows, D, regularize, cov_dev);
+  const int tiles = nt * (nt + 1) / 2;
+  const int splits = cov_splits(n_rows, D);
+  int64_t rps = (n_rows + splits - 1) / splits;
+  rps = (rps + kSlab - 1) / kSlab * kSlab;
+  k_cov_tile<<<dim3(tiles, splits), 256, 0, st>>>(x_dev, mean_dev, n_rows, D, rps, part);
+  TS_CUDA(cudaGetLastError());
+  k_cov_finish<<<tiles, 256, 0, st>>>(part, tiles, splits, n_rows, D, regularize, cov_dev);
   TS_CUDA(cudaGetLastError());
   return TS_OK;
 }
 
-extern "C" int64_t ts_pooled_covariance_workspace(int D) { return (int64_t)kChunks * (D > 0 ? D : 0); }
+extern "C" int64_t ts_pooled_covariance_workspace(int64_t n_rows, int D) {
+  if (D < 1 || n_rows < 2) return 0;
+  const int nt = (D + kTile - 1) / kTile;
+  return (int64_t)kChunks * D + (int64_t)cov_splits(n_rows, D) * (nt * (nt + 1) / 2) * kTile * kTile;
+}

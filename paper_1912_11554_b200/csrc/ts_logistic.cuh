@@ -78,6 +78,7 @@ struct LogisticArgs {
   // of CTAs exchanging through vmail), see ts_model_set_virtual_ranks
   int vranks;
   unsigned long long* vmail;
+  int keep_pct;  // % of each warp's tiles fetched with L2::evict_last (resident across passes), rest evict_first
   int icvt;  // fp64 wide pass: 1 = odd features converted on the integer pipe (default), 0 = all F2F, 2 = all ALU
   const float* th32;  // FP32 narrow pass: theta as floats [pmax + 1] (smem, written by the driver before each pass)
 };
@@ -256,7 +257,8 @@ struct Producer {
   const uint8_t* yfirst;
   int s, nstage, stage_bytes;
   uint32_t xb;
-  uint64_t pol;
+  uint64_t pol, pol_keep;
+  int64_t keep;          // tiles tj < keep stay in L2 between passes
 
   __device__ __forceinline__ void init(const LogisticArgs& a, const WarpTiles& wt, unsigned long long issued) {
     const int warp = wk_warp();
@@ -275,13 +277,16 @@ struct Producer {
     xsrc = xfirst + tj * xstep;
     ysrc = yfirst + tj * ystep;
     pol = policy_evict_first();
+    pol_keep = policy_evict_last();
+    keep = count * a.keep_pct / 100;
   }
   __device__ __forceinline__ void issue() {
     uint64_t* bar = bars + s;
     unsigned char* dst = ring + (int64_t)s * stage_bytes;
+    const uint64_t pl = tj < keep ? pol_keep : pol;
     mbar_expect_tx(bar, xb + 32u);
-    bulk_g2s(dst, xsrc, xb, bar, pol);
-    bulk_g2s(dst + xb, ysrc, 32u, bar, pol);
+    bulk_g2s(dst, xsrc, xb, bar, pl);
+    bulk_g2s(dst + xb, ysrc, 32u, bar, pl);
     if (++s == nstage) s = 0;
     if (++tj == count) { tj = 0; xsrc = xfirst; ysrc = yfirst; }
     else { xsrc += xstep; ysrc += ystep; }

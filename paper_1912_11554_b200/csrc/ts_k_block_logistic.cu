@@ -28,8 +28,9 @@ int launch_block_logistic(const ts_model* m, int nslots, OpArgs& A, cudaStream_t
   // L2 residency: the first 70% of each warp's tiles are fetched with
   // L2::evict_last and the rest evict_first, so ~88 MB of X stays in L2
   // across passes (covtype pass 23.8 -> 21.8 us; 90% thrashes: 24.4 us).
+  // The fp64 policy is XU-bound (conversions), not DRAM-bound: no split.
   // TS_L2_KEEP=<pct> overrides for A/B.
-  mw.a.keep_pct = 70;
+  mw.a.keep_pct = m->fp64 ? 0 : 70;
   if (const char* e = getenv("TS_L2_KEEP")) mw.a.keep_pct = atoi(e) < 0 ? 0 : (atoi(e) > 100 ? 100 : atoi(e));
   if (const char* e = getenv("TS_ICVT")) mw.a.icvt = atoi(e);
   if (m->world > 0) {

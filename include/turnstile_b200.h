@@ -84,6 +84,14 @@ int ts_model_create(int kind, int dim, const double* params, int n_params, const
                     int64_t n_rows, int n_feat, int precision, ts_model** out);
 int ts_model_destroy(ts_model* m);
 int ts_model_dim(const ts_model* m);
+/* Sticky device error word of a model (synchronises the device): 0, or
+ * TS_STATUS_SYNC_TIMEOUT once any wait of a persistent kernel on this model
+ * (grid barrier, peer mailbox, served flag) exceeded TS_SPIN_TIMEOUT_S
+ * seconds (default 30) - e.g. a row-shard peer that never launched.  The
+ * kernel then gives up instead of hanging the GPU; the model is poisoned
+ * (recreate it).  No reference counterpart (the reference is single-process). */
+enum { TS_STATUS_SYNC_TIMEOUT = 2 };
+int ts_model_error(const ts_model* m, int* code);
 /* Cap the number of CTAs of the persistent logistic grid (0 = one per SM). */
 int ts_model_set_grid(ts_model* m, int grid);
 
@@ -143,7 +151,8 @@ int ts_find_step_size(const ts_model* m, const double* inv_dev, const double* z_
  * adapt.py:119-127); da_weight_dev [W] = t^-kappa.  Outputs: samples
  * [C][S][dim], stats [C][W+S][5] (depth, leapfrogs, diverged, accept_stat,
  * energy), adapt [C][2+W+dim] (initial step, final step, step trace,
- * inverse mass), status [C] (0 ok, 1 invalid mass install), evals [C] or NULL
+ * inverse mass), status [C] (0 ok, 1 invalid mass install, TS_STATUS_SYNC_TIMEOUT:
+ * an inter-CTA / inter-GPU wait exceeded TS_SPIN_TIMEOUT_S, see ts_model_error), evals [C] or NULL
  * (model evaluations = passes over the data, incl. step-size search). */
 int ts_run_chains(const ts_model* m, const ts_run_cfg* rc, const uint64_t* chain_keys_dev, int n_chains,
                   const double* inv0_dev, const uint8_t* schedule_dev, const double* da_weight_dev, double* samples,
@@ -206,6 +215,18 @@ int ts_rng_probe(uint64_t key_hi, uint64_t key_lo, int kind, int n, double* out_
 int ts_pooled_covariance(const double* x_dev, int64_t n_rows, int D, int regularize, double* mean_dev,
                          double* cov_dev, double* work_dev, void* stream);
 int64_t ts_pooled_covariance_workspace(int64_t n_rows, int D);
+
+/* Replaces diagnostics.ess (diagnostics.py:49-86) and diagnostics.split_rhat
+ * (diagnostics.py:89-105) for samples already in device memory: samples_dev
+ * (n_chains, n_draws, dim) fp64 C-contiguous -> ess_dev[dim], rhat_dev[dim]
+ * (NaN for a constant dimension, as the reference).  Split-chain estimator,
+ * autocovariance by direct lag sums in blocks of 64 lags until Geyer's
+ * truncation (csrc/ts_k_diagnostics.cu); deterministic; agrees with the host
+ * estimator to rounding.  work_dev holds ts_chain_diagnostics_workspace()
+ * doubles.  Synchronises `stream` once per lag block (reads one flag). */
+int ts_chain_diagnostics(const double* samples_dev, int n_chains, int n_draws, int dim, double* ess_dev,
+                         double* rhat_dev, double* work_dev, void* stream);
+int64_t ts_chain_diagnostics_workspace(int n_chains, int n_draws, int dim);
 
 #ifdef __cplusplus
 }

@@ -410,6 +410,20 @@ def uturn(rho, inv, rl, rr):
     return a < 0.0 or b < 0.0
 
 
+def uturn_margin(rho, inv, rl, rr):
+    """Relative distance of a U-turn check from flipping (test diagnostics,
+    not on the reference path): min over the two dot products of
+    |dot| / sum|terms|, i.e. how many relative rounding units separate the
+    decision from the other outcome."""
+    a = b = sa = sb = 0.0
+    for x, iv, u, v in zip(rho, inv, rl, rr):
+        a += x * iv * u
+        b += x * iv * v
+        sa += abs(x * iv * u)
+        sb += abs(x * iv * v)
+    return min(abs(a) / sa if sa else math.inf, abs(b) / sb if sb else math.inf)
+
+
 # ----------------------------------------------------------------------------- tree
 
 
@@ -438,10 +452,12 @@ def lse_inner(a, b):
     return hi + math.log1p(math.exp(lo - hi))
 
 
-def merge(left: Sub, right: Sub, u) -> Sub:
+def merge(left: Sub, right: Sub, u, margins=None) -> Sub:
     lw = lse_inner(left.lw, right.lw)
     p_right = 0.0 if right.lw == -INF else math.exp(right.lw - lw)
     take_right = u < p_right
+    if margins is not None:
+        margins.append(("merge", abs(u - p_right)))
     src = right if take_right else left
     return Sub(left.first, right.last, src.prop, src.prop_h, src.prop_leaf, lw, left.cum_first, right.cum_last,
                left.count + right.count, left.metro + right.metro)
@@ -463,10 +479,15 @@ class TreeResult:
     max_occupied: int
 
 
-def build_tree(z: Point, depth, eps, inv, model, key, h_ref, generalized=True, threshold=1000.0) -> TreeResult:
+def build_tree(z: Point, depth, eps, inv, model, key, h_ref, generalized=True, threshold=1000.0,
+               margins=None) -> TreeResult:
     """Iterative builder (tree.py:344-453): slot s holds the latest even leaf
     with popcount s plus its completed subtree; odd leaf n merges and checks
-    slots popcount(n)-1 down to popcount(n)-trailing_ones(n)."""
+    slots popcount(n)-1 down to popcount(n)-trailing_ones(n).
+
+    ``margins`` (test diagnostics): a list that receives (kind, margin) for
+    every floating-point decision - merges |u - p_right|, U-turn checks
+    (uturn_margin), divergence |dH - threshold| / |threshold|."""
     st = Stream(key)
     D = len(z.q)
     cum = [0.0] * D
@@ -483,6 +504,8 @@ def build_tree(z: Point, depth, eps, inv, model, key, h_ref, generalized=True, t
         h = hamiltonian(cur.U, cur.r, inv)
         delta = h - h_ref
         div = not (math.isfinite(delta) and delta <= threshold)
+        if margins is not None and math.isfinite(delta):
+            margins.append(("divergence", abs(delta - threshold) / threshold))
         if div:
             lw = -INF
             metro = math.exp(-delta) if math.isfinite(delta) else 0.0
@@ -494,7 +517,7 @@ def build_tree(z: Point, depth, eps, inv, model, key, h_ref, generalized=True, t
 
     def fold_pending(start, part):
         for s in range(start - 1, -1, -1):
-            part = merge(slots[s], part, st.random())
+            part = merge(slots[s], part, st.random(), margins)
         return part
 
     def finish(sub, stop):
@@ -519,15 +542,16 @@ def build_tree(z: Point, depth, eps, inv, model, key, h_ref, generalized=True, t
         running = lf
         for s in range(hi_slot, lo_slot - 1, -1):
             checks.append((n, s, slot_leaf[s]))
-            running = merge(slots[s], running, st.random())
+            running = merge(slots[s], running, st.random(), margins)
             if generalized:
-                turned = uturn(seg_sum(running), inv, running.first.r, running.last.r)
+                args = (seg_sum(running), inv, running.first.r, running.last.r)
             elif forward:
-                dq = [a - b for a, b in zip(running.last.q, running.first.q)]
-                turned = uturn(dq, inv, running.first.r, running.last.r)
+                args = ([a - b for a, b in zip(running.last.q, running.first.q)], inv, running.first.r, running.last.r)
             else:
-                dq = [a - b for a, b in zip(running.first.q, running.last.q)]
-                turned = uturn(dq, inv, running.last.r, running.first.r)
+                args = ([a - b for a, b in zip(running.first.q, running.last.q)], inv, running.last.r, running.first.r)
+            turned = uturn(*args)
+            if margins is not None:
+                margins.append(("uturn", uturn_margin(*args)))
             if turned:
                 return finish(fold_pending(s, running), 1)
         slots[lo_slot] = running
@@ -546,8 +570,13 @@ class Stats:
     energy: float
 
 
-def transition(z0: Point, step, inv, model, key, max_depth=10, generalized=True, threshold=1000.0, normals=None):
-    """nuts_transition_from (sampler.py:83-148); returns (point, Stats, decisions)."""
+def transition(z0: Point, step, inv, model, key, max_depth=10, generalized=True, threshold=1000.0, normals=None,
+               margins=None):
+    """nuts_transition_from (sampler.py:83-148); returns (point, Stats, decisions).
+
+    ``margins`` (test diagnostics): a list that receives, per tree j, the list
+    of (kind, margin) of every floating-point decision taken in it (see
+    build_tree) plus the outer proposal draw and U-turn check."""
     D = len(z0.q)
     if normals is None:
         ns = Stream(key_fold(key, 0))
@@ -567,8 +596,11 @@ def transition(z0: Point, step, inv, model, key, max_depth=10, generalized=True,
     for j in range(max_depth):
         go_right = gen.random() < 0.5
         eps = step if go_right else -step
+        tm = None if margins is None else []
+        if margins is not None:
+            margins.append(tm)
         t = build_tree(right if go_right else left, j, eps, inv, model, key_fold(key, 2 + j), h0, generalized,
-                       threshold)
+                       threshold, tm)
         lf += t.sub.count
         metro += t.sub.metro
         trees.append((j, int(go_right), t.sub.count, int(t.turning), int(t.diverging), t.sub.prop_leaf))
@@ -577,6 +609,8 @@ def transition(z0: Point, step, inv, model, key, max_depth=10, generalized=True,
             depth = j
             break
         u = gen.random()
+        if tm is not None and t.sub.lw < lw:
+            tm.append(("accept", abs(u - math.exp(t.sub.lw - lw))))
         if t.sub.lw >= lw or u < math.exp(t.sub.lw - lw):
             prop, prop_h, prop_id = t.sub.prop, t.sub.prop_h, (j, t.sub.prop_leaf)
         lw = float(np.logaddexp(lw, t.sub.lw))
@@ -586,10 +620,11 @@ def transition(z0: Point, step, inv, model, key, max_depth=10, generalized=True,
         else:
             left = t.sub.last
         depth = j + 1
-        if generalized:
-            turned = uturn(rho, inv, left.r, right.r)
-        else:
-            turned = uturn([a - b for a, b in zip(right.q, left.q)], inv, left.r, right.r)
+        oargs = (rho, inv, left.r, right.r) if generalized else ([a - b for a, b in zip(right.q, left.q)], inv, left.r,
+                                                                   right.r)
+        turned = uturn(*oargs)
+        if tm is not None:
+            tm.append(("outer_uturn", uturn_margin(*oargs)))
         outer.append(int(turned))
         if turned:
             break

@@ -22,6 +22,7 @@ TS_STD_NORMAL, TS_GAUSSIAN, TS_LOGISTIC, TS_FUNNEL, TS_EIGHT_SCHOOLS, TS_DENSE_G
 TS_PREC_FP64, TS_PREC_FP32, TS_PREC_TF32 = 0, 1, 2
 TS_GENERALIZED, TS_CLASSIC = 0, 1
 TS_EXEC_THREAD, TS_EXEC_BLOCK, TS_EXEC_WARP = 0, 1, 2
+TS_STATUS_SYNC_TIMEOUT = 2
 ABI_VERSION = 1
 
 # every symbol include/turnstile_b200.h declares
@@ -48,6 +49,9 @@ EXPORTS = (
     "ts_model_set_virtual_ranks",
     "ts_pooled_covariance",
     "ts_pooled_covariance_workspace",
+    "ts_model_error",
+    "ts_chain_diagnostics",
+    "ts_chain_diagnostics_workspace",
 )
 
 
@@ -106,10 +110,14 @@ def _declare(lib):
     lib.ts_model_set_virtual_ranks.argtypes = [_P, _I]
     lib.ts_pooled_covariance.argtypes = [_P, ctypes.c_int64, _I, _I, _P, _P, _P, _P]
     lib.ts_pooled_covariance_workspace.argtypes = [ctypes.c_int64, _I]
+    lib.ts_model_error.argtypes = [_P, ctypes.POINTER(_I)]
+    lib.ts_chain_diagnostics.argtypes = [_P, _I, _I, _I, _P, _P, _P, _P]
+    lib.ts_chain_diagnostics_workspace.argtypes = [_I, _I, _I]
     for name in EXPORTS:
         if name not in ("ts_last_error",):
             getattr(lib, name).restype = _I
     lib.ts_pooled_covariance_workspace.restype = ctypes.c_int64
+    lib.ts_chain_diagnostics_workspace.restype = ctypes.c_int64
 
 
 def load_library(path: str = LIB_PATH):
@@ -137,6 +145,26 @@ def check(code: int) -> None:
     if code == TS_EINVAL:
         raise ValueError(msg)
     raise RuntimeError(msg)
+
+
+SYNC_TIMEOUT_MSG = ("a device synchronisation wait (grid barrier / peer mailbox / served flag) exceeded "
+                    "TS_SPIN_TIMEOUT_S; the kernel gave up instead of hanging and the model is poisoned")
+
+
+def check_model(handle) -> None:
+    """Raise RuntimeError if a persistent kernel on this model gave up on a
+    wait (sticky device error word, ts_model_error; synchronises)."""
+    lib = load_library()
+    code = _I(0)
+    check(lib.ts_model_error(handle, ctypes.byref(code)))
+    if code.value:
+        raise RuntimeError(SYNC_TIMEOUT_MSG)
+
+
+def check_spec(spec, handle) -> None:
+    """check_model for the models whose kernels wait across CTAs/GPUs."""
+    if spec.kind in (TS_LOGISTIC, TS_DENSE_GAUSS):
+        check_model(handle)
 
 
 def torch_cuda():

@@ -124,16 +124,24 @@ class DeviceRun:
 
 
 def run_device(model: TargetModel, config: RunConfig, keys: Sequence[RngKey], device=None, exec_mode=None,
-               sync: bool = True):
+               sync: bool = True, base: Optional[SamplerConfig] = None):
     """Launch the whole warmup + sampling run for ``keys`` on one GPU.
 
     Returns torch tensors (samples (C,S,D), stats (C,W+S,5), adapt (C,2+W+D),
     status (C,)) still on the device, plus the device time of the launch.
+
+    ``base`` overrides the start configuration (run_chain's argument) without
+    counting as a user ``config.sampler``: with ``num_warmup == 0`` the
+    step-size search still runs unless ``config.sampler`` is set
+    (chains.py:132-138).
     """
     spec = require_device(model)
     torch = _lib.torch_cuda()
     dev = _lib.cuda_device(torch, device)
-    base = _base_config(config, model)
+    if base is None:
+        base = _base_config(config, model)
+    elif base.mass.dim != model.dim:
+        raise ValueError(f"mass matrix dimension {base.mass.dim} does not match model dimension {model.dim}")
     C, W, S, D = len(keys), config.num_warmup, config.num_samples, model.dim
     handle = spec.handle(dev)
     with torch.cuda.device(dev):
@@ -174,13 +182,21 @@ def run_device(model: TargetModel, config: RunConfig, keys: Sequence[RngKey], de
 
 
 def _results(chain_ids, run: DeviceRun, config: RunConfig, D: int, wall_ns: int) -> list[ChainResult]:
+    """Per-chain results of one launch.  The launch's wall time ``wall_ns`` is
+    shared out over its chains (remainder to the first ones), so that summing
+    ``elapsed_ns`` over chains -- as ``summarize`` does, diagnostics.py:142-155
+    -- gives the device time spent, not num_chains times it."""
     W, S = config.num_warmup, config.num_samples
+    n = len(chain_ids)
+    share = [wall_ns // n + (1 if i < wall_ns % n else 0) for i in range(n)]
     samples = run.samples.cpu().numpy()
     stats = run.stats.cpu().numpy()
     adapt = run.adapt.cpu().numpy()
     status = run.status.cpu().numpy()
     out = []
     for i, c in enumerate(chain_ids):
+        if status[i] == _lib.TS_STATUS_SYNC_TIMEOUT:
+            raise RuntimeError(_lib.SYNC_TIMEOUT_MSG)
         if status[i] != 0:
             raise ValueError("inverse mass diagonal must be positive and finite")
         st = stats[i]
@@ -196,18 +212,16 @@ def _results(chain_ids, run: DeviceRun, config: RunConfig, D: int, wall_ns: int)
             adaptation = {"final_step_size": float(a[1]), "inv_mass_diag": a[2:2 + D].tolist()}
         total = int(st[:, 1].sum())
         samp = int(st[W:, 1].sum())
-        out.append(ChainResult(c, samples[i], st[W:].copy(), adaptation, wall_ns, total, samp, st[:W].copy()))
+        out.append(ChainResult(c, samples[i], st[W:].copy(), adaptation, share[i], total, samp, st[:W].copy()))
     return out
 
 
 def run_chain(chain_id: int, key: RngKey, model: TargetModel, config: RunConfig, base: SamplerConfig,
               device=None) -> ChainResult:
     """Warm up and sample one chain on the device (chains.py:98-163)."""
-    cfg = config if config.sampler is base else RunConfig(config.model, 1, config.num_warmup, config.num_samples,
-                                                          config.mode, config.seed, base, config.target_accept)
     t0 = time.perf_counter_ns()
-    r = run_device(model, cfg, [key], device)
-    return _results([chain_id], r, cfg, model.dim, time.perf_counter_ns() - t0)[0]
+    r = run_device(model, config, [key], device, base=base)
+    return _results([chain_id], r, config, model.dim, time.perf_counter_ns() - t0)[0]
 
 
 def run(config: RunConfig, model: Optional[TargetModel] = None, devices: Optional[Sequence] = None,
@@ -224,14 +238,16 @@ def run(config: RunConfig, model: Optional[TargetModel] = None, devices: Optiona
     devices = list(devices)
     C = config.num_chains
     shards = [shard_range(C, g, len(devices)) for g in range(len(devices))]
-    t0 = time.perf_counter_ns()
     runs: list = [None] * len(devices)
+    walls: list = [0] * len(devices)
     errors: list = []
 
     def work(g):
         try:
             if shards[g]:
+                t0 = time.perf_counter_ns()
                 runs[g] = run_device(model, config, [keys[c] for c in shards[g]], devices[g], exec_mode)
+                walls[g] = time.perf_counter_ns() - t0
         except BaseException as e:  # surfaced below
             errors.append(e)
 
@@ -245,12 +261,30 @@ def run(config: RunConfig, model: Optional[TargetModel] = None, devices: Optiona
             t.join()
     if errors:
         raise errors[0]
-    wall = time.perf_counter_ns() - t0
     results: list[ChainResult] = []
     for g in range(len(devices)):
         if shards[g]:
-            results += _results(shards[g], runs[g], config, model.dim, wall)
+            results += _results(shards[g], runs[g], config, model.dim, walls[g])
     return results
+
+
+def run_sharded(config: RunConfig, model: Optional[TargetModel] = None, rank: int = 0, world: int = 1, device=None,
+                exec_mode=None) -> list[ChainResult]:
+    """This process's share of ``run(config)`` when one process drives each
+    GPU (torch.distributed-style launch): chains ``shard_range(C, rank,
+    world)`` on ``device``.  Concatenating the ranks' results in rank order
+    gives exactly ``run(config)`` (chains are pure functions of their keys)."""
+    if model is None:
+        model = model_from_descriptor(config.model)
+    require_device(model)
+    _base_config(config, model)
+    keys = chain_keys(config.seed, config.num_chains)
+    ids = shard_range(config.num_chains, rank, world)
+    if not ids:
+        return []
+    t0 = time.perf_counter_ns()
+    r = run_device(model, config, [keys[c] for c in ids], device, exec_mode)
+    return _results(ids, r, config, model.dim, time.perf_counter_ns() - t0)
 
 
 def run_dense_adapted(precision_matrix, config: RunConfig, pilot: Optional[RunConfig] = None,

@@ -133,6 +133,7 @@ extern "C" int ts_model_create(int kind, int dim, const double* params, int n_pa
   m->dim = dim;
   cudaGetDevice(&m->device);
   auto fail = [&](int code, const char* msg) {
+    if (m->errw) cudaFree(m->errw);
     if (m->params) cudaFree(m->params);
     if (m->xt) cudaFree(m->xt);
     if (m->yt) cudaFree(m->yt);
@@ -219,6 +220,8 @@ extern "C" int ts_model_create(int kind, int dim, const double* params, int n_pa
       return fail(TS_ECUDA, "params upload failed");
     m->n_params = n_params;
   }
+  if (cudaMalloc((void**)&m->errw, 16) != cudaSuccess || cudaMemset(m->errw, 0, 16) != cudaSuccess)
+    return fail(TS_ECUDA, "cudaMalloc error word failed");
   *out = m;
   return TS_OK;
 }
@@ -237,8 +240,23 @@ extern "C" int ts_model_destroy(ts_model* m) {
     if (m->mail[r] && m->mail[r] != m->mail_local) cudaIpcCloseMemHandle(m->mail[r]);
   if (m->mail_local) cudaFree(m->mail_local);
   if (m->vmail) cudaFree(m->vmail);
+  if (m->errw) cudaFree(m->errw);
   delete m;
   return TS_OK;
+}
+
+extern "C" int ts_model_error(const ts_model* m, int* code) {
+  if (!m || !code) return set_err(TS_EINVAL, "null argument");
+  unsigned int w = 0;
+  TS_CUDA(cudaMemcpy(&w, m->errw, sizeof w, cudaMemcpyDeviceToHost));
+  *code = w ? TS_STATUS_SYNC_TIMEOUT : TS_OK;
+  return TS_OK;
+}
+
+// Stream-ordered: a run whose kernel gave up on a wait reports it per chain.
+__global__ void k_fold_timeout(const unsigned int* errw, int32_t* status, int n) {
+  if (*errw == 0u) return;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) status[i] = TS_STATUS_SYNC_TIMEOUT;
 }
 
 extern "C" int ts_model_set_grid(ts_model* m, int grid) {
@@ -451,24 +469,40 @@ extern "C" int ts_run_chains(const ts_model* m, const ts_run_cfg* rc, const uint
   const int nslots = rc->sampler.max_tree_depth - 1;
   // TS_PROF=1: chain-0 cycle counters of the run, printed to stderr (profiling
   // aid; logistic runs and warp-team small-model runs)
-  static unsigned long long* prof_buf = nullptr;
+  // (allocated per call on the launch stream: no buffer shared across devices or threads)
+  unsigned long long* prof_buf = nullptr;
   const bool prof = getenv("TS_PROF") != nullptr &&
                     (m->kind == TS_LOGISTIC || (m->kind != TS_DENSE_GAUSS && exec_mode == TS_EXEC_WARP));
   if (prof) {
-    if (!prof_buf) TS_CUDA(cudaMalloc((void**)&prof_buf, 24 * sizeof(unsigned long long)));
+    TS_CUDA(cudaMallocAsync((void**)&prof_buf, 24 * sizeof(unsigned long long), st));
     TS_CUDA(cudaMemsetAsync(prof_buf, 0, 24 * sizeof(unsigned long long), st));
   }
+  auto fold_timeout = [&]() -> int {
+    k_fold_timeout<<<1, 256, 0, st>>>(m->errw, status, n_chains);
+    TS_CUDA(cudaGetLastError());
+    return TS_OK;
+  };
   if (m->kind != TS_LOGISTIC) {
     A.prof = prof ? prof_buf : nullptr;
     int e = launch(m, nslots, A, n_chains, (ts_exec_mode)exec_mode, st);
-    if (e || !prof) return e;
+    if (!e) e = fold_timeout();
+    if (e || !prof) {
+      if (prof_buf) cudaFreeAsync(prof_buf, st);
+      return e;
+    }
   } else {
     if (prof) const_cast<ts_model*>(m)->prof = prof_buf;
     for (int c = 0; c < n_chains; ++c) {
       A.n_points = c;
       int e = launch(m, nslots, A, 1, TS_EXEC_BLOCK, st);
-      if (e) { const_cast<ts_model*>(m)->prof = nullptr; return e; }
+      if (e) {
+        const_cast<ts_model*>(m)->prof = nullptr;
+        if (prof_buf) cudaFreeAsync(prof_buf, st);
+        return e;
+      }
     }
+    const int e = fold_timeout();
+    if (e) return e;
   }
   {
     if (prof) {
@@ -484,6 +518,7 @@ extern "C" int ts_run_chains(const ts_model* m, const ts_run_cfg* rc, const uint
       const double nt = h[14] ? (double)h[14] : 1.0, nx = h[15] ? (double)h[15] : 1.0;
       fprintf(stderr, "TS_PROF transitions=%llu trees=%llu cycles: prologue/transition %.0f (momentum %.0f)  between-trees/tree %.0f\n",
               h[15], h[14], h[12] / nx, h[16] / nx, h[13] / nt);
+      cudaFreeAsync(prof_buf, st);
     }
     return TS_OK;
   }

@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 #include <string>
 #include <type_traits>
@@ -46,12 +47,22 @@ struct ts_model {
   float* a32;
   unsigned char* dws;  // lockstep workspaces (grown on demand)
   size_t dws_size;
+  unsigned int* errw;  // sticky device error word: bit 0 = a synchronisation wait timed out (SpinGuard)
 };
 
 namespace ts_internal {
 using namespace ts;
 
 int set_err(int code, const char* msg);
+
+// Limit of every inter-CTA / inter-GPU wait (SpinGuard): TS_SPIN_TIMEOUT_S
+// seconds (default 30).
+inline unsigned long long spin_limit_ns() {
+  double s = 30.0;
+  if (const char* e = getenv("TS_SPIN_TIMEOUT_S")) s = atof(e);
+  if (!(s > 0)) s = 30.0;
+  return (unsigned long long)(s * 1e9);
+}
 
 
 // ------------------------------------------------------------------ op args

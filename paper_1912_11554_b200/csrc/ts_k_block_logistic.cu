@@ -22,6 +22,9 @@ int launch_block_logistic(const ts_model* m, int nslots, OpArgs& A, cudaStream_t
   mw.a.exact_cvt = m->exact_cvt;
   mw.a.dump = m->dump;
   mw.a.vranks = m->vranks;
+  mw.a.err = m->errw;
+  mw.a.spin_ns = spin_limit_ns();
+  if (const char* e = getenv("TS_FAULT_INJECT")) mw.a.fault = atoi(e);  // tests of the bounded waits only
   // fp64 wide pass: half of the fp32->fp64 conversions on the integer pipe
   // (XU-bound otherwise; 2.77 -> 2.61 ms per 8Mx255 pass); TS_ICVT=0/2 for A/B
   mw.a.icvt = 1;

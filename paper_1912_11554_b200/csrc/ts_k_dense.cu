@@ -100,6 +100,8 @@ struct DenseW {
   unsigned long long* served;  // [Cpad]
   unsigned long long seq;
   int chain;
+  unsigned int* err;
+  unsigned long long spin_ns;
   VecStore S;
   int pq, pg;
 
@@ -139,7 +141,9 @@ struct DenseW {
     if (lane == 0) {
       // relaxed polling (an acquire load per iteration would invalidate the
       // SM's L1 every time), then one acquire
+      SpinGuard sg(err, spin_ns);
       while (ld_relaxed_u64(served + chain) < seq) {
+        if (sg.expired()) break;
       }
       (void)ld_acquire_u64(served + chain);
     }
@@ -222,15 +226,20 @@ struct DenseArgs {
   unsigned long long* served;   // [Cpad]
   unsigned long long* pending;  // [Cpad] request served by the current step (0 = none)
   unsigned long long* npend;    // [2] outstanding requests of the step, [2..4) all-done flags (rotating)
+  unsigned int* err;            // sticky synchronisation-timeout flag of the model (SpinGuard)
+  unsigned long long spin_ns;
 };
 
-__device__ __forceinline__ void gemm_grid_barrier(unsigned long long* bar, unsigned long long& epoch) {
+__device__ __forceinline__ void gemm_grid_barrier(unsigned long long* bar, unsigned long long& epoch, unsigned int* err,
+                                                  unsigned long long spin_ns) {
   asm volatile("bar.sync 4, 128;" ::: "memory");  // every GEMM thread's stores precede the release
   if (threadIdx.x == 0) {
     __threadfence();
     const unsigned long long target = (epoch + 1) * (unsigned long long)gridDim.x;
     red_release_add_u64(bar, 1ULL);
+    SpinGuard sg(err, spin_ns);
     while (ld_relaxed_u64(bar) < target) {
+      if (sg.expired()) break;
     }
     asm volatile("fence.acq_rel.gpu;" ::: "memory");
   }
@@ -300,7 +309,7 @@ __global__ void __launch_bounds__(128 + 32 * kDenseCW, 1)
       // asynchronously, so reading it after the barrier could differ per CTA)
       if (t == 0 && blockIdx.x == 0)
         a.npend[2 + (step & 1)] = (*reinterpret_cast<volatile int*>(a.done) >= total) ? 1ULL : 0ULL;
-      gemm_grid_barrier(a.bar, epoch);
+      gemm_grid_barrier(a.bar, epoch, a.err, a.spin_ns);
       if (t == 0) {
         const unsigned long long np = ld_relaxed_u64(a.npend + (step & 1));
         const bool all_done = ld_relaxed_u64(a.npend + 2 + (step & 1)) != 0ULL;
@@ -335,7 +344,7 @@ __global__ void __launch_bounds__(128 + 32 * kDenseCW, 1)
         a.prof[1] += tp1 - tp0;
         tp0 = tp1;
       }
-      gemm_grid_barrier(a.bar, epoch);  // all gradient tiles written
+      gemm_grid_barrier(a.bar, epoch, a.err, a.spin_ns);  // all gradient tiles written
       if (t < kDenseCW && mine) {
         srv = mine;
         st_release_gpu_u64(a.served + my_chain, mine);
@@ -364,6 +373,8 @@ __global__ void __launch_bounds__(128 + 32 * kDenseCW, 1)
     M.served = a.served;
     M.seq = 0;
     M.chain = chain;
+    M.err = a.err;
+    M.spin_ns = a.spin_ns;
     Engine<WarpTeam, DenseW> E;
     E.D = a.D;
     E.S.base = a.ws + (int64_t)chain * a.nv * a.D;
@@ -450,6 +461,8 @@ static int launch_dense_chunk(const ts_model* m, int nslots, OpArgs& A, int C, i
   a.pending = a.served + Cpad;
   a.npend = a.pending + Cpad;
   a.a64 = m->params;
+  a.err = m->errw;
+  a.spin_ns = spin_limit_ns();
   CUtensorMap ta, tx;
   memset(&ta, 0, sizeof ta);
   memset(&tx, 0, sizeof tx);

@@ -81,6 +81,9 @@ struct LogisticArgs {
   int keep_pct;  // % of each warp's tiles fetched with L2::evict_last (resident across passes), rest evict_first
   int icvt;  // fp64 wide pass: 1 = odd features converted on the integer pipe (default), 0 = all F2F, 2 = all ALU
   const float* th32;  // FP32 narrow pass: theta as floats [pmax + 1] (smem, written by the driver before each pass)
+  unsigned int* err;               // sticky synchronisation-timeout flag of the model (SpinGuard)
+  unsigned long long spin_ns;      // wait limit
+  int fault;                       // fault injection (tests): 1 = CTA 1 never arrives at the grid barrier
 };
 
 // Mailbox of one rank: kMailFlags words of flags (flag[src] = 1 + the last
@@ -191,18 +194,30 @@ __device__ __forceinline__ double fx_join(long long hi, unsigned long long lo_ca
   return (double)hi * (1.0 / 1024.0) + (double)lo_canon * (1.0 / 2305843009213693952.0);
 }
 
-// Grid barrier #epoch (0-based) over gridDim.x co-resident CTAs.
-__device__ __forceinline__ void grid_barrier(unsigned long long* bar, unsigned long long epoch) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned long long target = (epoch + 1) * (unsigned long long)gridDim.x;
-    red_release_add_u64(bar, 1ULL);
-    while (ld_relaxed_u64(bar) < target) {
-    }
-    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+// Bounded spin.  Every inter-CTA / inter-GPU wait (grid barrier, peer
+// mailbox, served flag) polls through a SpinGuard: a wait longer than `limit`
+// ns (%globaltimer) sets *err (sticky, per model) and gives up; once *err is
+// set every later wait gives up at once.  A kernel whose peer CTA or rank
+// never arrives therefore still terminates, and the host raises RuntimeError
+// (run status TS_STATUS_SYNC_TIMEOUT / ts_model_error) instead of the GPU
+// hanging.  The clock is read every 64 polls only.
+struct SpinGuard {
+  unsigned int* err;
+  unsigned long long limit, t0;
+  unsigned int n;
+  __device__ __forceinline__ SpinGuard(unsigned int* e, unsigned long long lim) : err(e), limit(lim), t0(0), n(0) {}
+  // true: stop waiting
+  __device__ __forceinline__ bool expired() {
+    if (err == nullptr) return false;
+    if ((++n & 63u) != 1u) return false;
+    if (*reinterpret_cast<volatile unsigned int*>(err) != 0u) return true;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (n == 1u) { t0 = t; return false; }
+    if (t - t0 > limit) { atomicOr(err, 1u); return true; }
+    return false;
   }
-  __syncthreads();
-}
+};
 
 // ------------------------------------------------------------- worker group
 // Warp 0 of each CTA drives the chain; warps 1.. stream the data.  The pass
@@ -366,7 +381,12 @@ __device__ __noinline__ void logistic_cta_pass(const LogisticArgs& a, const doub
 
   using acc_t = typename std::conditional<FP64, double, float>::type;
   acc_t acc[PMAX + 1];
-  acc_t accl = 0;
+  // log-likelihood terms accumulate in double in both policies: in the FP32
+  // policy the per-row term is formed as y*eta - (max(eta,0) + log1p(e)) with
+  // the log1p in double (float e, float eta): identical rows (e.g. q = 0,
+  // every term log 2) would otherwise add the same float rounding N times
+  // (0.09 nats at 581,012 rows)
+  double accl = 0.0;
 #pragma unroll
   for (int j = 0; j <= PMAX; ++j) acc[j] = 0;
 
@@ -460,11 +480,11 @@ __device__ __noinline__ void logistic_cta_pass(const LogisticArgs& a, const doub
         }
         const float eta = (e0 + e1) + (e2 + e3);
         const float e = expf(-fabsf(eta));
-        const float l = fmaxf(eta, 0.f) + log1pf(e);
+        const double l = (double)fmaxf(eta, 0.f) + log1p((double)e);
         const float sig = __fdiv_rn(eta >= 0.f ? 1.f : e, 1.f + e);
         const float yv = (float)yb;
         const float resid = valid ? yv - sig : 0.f;
-        accl += valid ? __fmaf_rn(yv, eta, -l) : 0.f;
+        accl += valid ? ((yb ? (double)eta : 0.0) - l) : 0.0;
 #pragma unroll
         for (int k = 0; k < PMAX; ++k) acc[k] = __fmaf_rn(resid, x[k], acc[k]);
         acc[PMAX] += resid;
@@ -484,7 +504,7 @@ __device__ __noinline__ void logistic_cta_pass(const LogisticArgs& a, const doub
   constexpr int NP = (NA <= 16) ? 16 : (NA <= 32 ? 32 : (NA <= 64 ? 64 : 128));
   acc_t v[NP];
 #pragma unroll
-  for (int j = 0; j < NP; ++j) v[j] = (j <= PMAX) ? acc[j <= PMAX ? j : PMAX] : (j == PMAX + 1 ? accl : (acc_t)0);
+  for (int j = 0; j < NP; ++j) v[j] = (j <= PMAX) ? acc[j <= PMAX ? j : PMAX] : (j == PMAX + 1 && FP64 ? (acc_t)accl : (acc_t)0);
   int colbase = 0;
   int cnt = NP;
 #pragma unroll
@@ -509,7 +529,13 @@ __device__ __noinline__ void logistic_cta_pass(const LogisticArgs& a, const doub
   // lane holds columns colbase .. colbase+cnt-1 (duplicates across lanes when NP < 64)
 #pragma unroll
   for (int i = 0; i < NP / 32 + 1; ++i) {
-    if (i < cnt && colbase + i < NA && (NP >= 32 || (lane % (32 / NP)) == 0)) wred[warp * NA + colbase + i] = (double)v[i];
+    if (i < cnt && colbase + i < NA && (NP >= 32 || (lane % (32 / NP)) == 0) && (FP64 || colbase + i != PMAX + 1))
+      wred[warp * NA + colbase + i] = (double)v[i];
+  }
+  if constexpr (!FP64) {  // the double log-likelihood sum: its own fixed-order tree
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) accl += __shfl_xor_sync(0xffffffffu, accl, off);
+    if (lane == 0) wred[warp * NA + PMAX + 1] = accl;
   }
   if (prof) { pc1 = clock64(); a.prof[6] += pc1 - pc0; pc0 = pc1; }
   wk_sync();
@@ -892,7 +918,7 @@ static __device__ void logistic_eval_grid(const LogisticArgs& a, const VecStore&
   }
   wk_sync();
   if (wk_tid() == 0) {
-    if (G > 1) red_release_add_u64(a.bar, 1ULL);
+    if (G > 1 && !(a.fault == 1 && a.cta == 1)) red_release_add_u64(a.bar, 1ULL);
     // prior term 0.5 |theta|^2 (kernels.py:92-95), computed by the thread
     // that waits at the barrier anyway (left to right, bias first)
     double pr = 0.5 * theta[p] * theta[p];
@@ -900,7 +926,9 @@ static __device__ void logistic_eval_grid(const LogisticArgs& a, const VecStore&
     red_s[1] = pr;
     if (G > 1) {
       const unsigned long long target = (epoch + 1) * (unsigned long long)G;
+      SpinGuard sg(a.err, a.spin_ns);
       while (ld_relaxed_u64(a.bar) < target) {
+        if (sg.expired()) break;
       }
     }
     asm volatile("fence.acq_rel.gpu;" ::: "memory");
@@ -948,7 +976,9 @@ static __device__ void logistic_eval_grid(const LogisticArgs& a, const VecStore&
     }
     const unsigned long long* box = a.mail[a.rank];
     if (wk_tid() < W) {  // relaxed polling, then one acquire (each acquire load invalidates L1)
+      SpinGuard sg(a.err, a.spin_ns);
       while (ld_relaxed_sys_u64(box + wk_tid()) < x + 1) {
+        if (sg.expired()) break;
       }
       (void)ld_acquire_sys_u64(box + wk_tid());
     }

@@ -110,7 +110,9 @@ def potential_and_gradient(spec: DeviceSpec, qs: np.ndarray, device=None) -> np.
     lib = _lib.load_library()
     with torch.cuda.device(dev):
         _lib.check(lib.ts_potential_grad(h, _lib.ptr(qd), qs.shape[0], _lib.ptr(out), _lib.stream_ptr(torch)))
-    return out.cpu().numpy()
+    res = out.cpu().numpy()
+    _lib.check_spec(spec, h)
+    return res
 
 
 @dataclass(frozen=True)

@@ -86,6 +86,14 @@ def nuts_transition_from(z0: PhasePoint, config: SamplerConfig, model: TargetMod
 
     ``normals`` optionally injects the momentum refresh's standard normals
     (otherwise drawn on the device from rng.fold(0), as numpy would).
+
+    Returns ``(z1, stats)``.  ``z1`` carries the proposal's position,
+    potential and gradient; unlike the reference (whose proposal PhasePoint
+    keeps the leaf's momentum, sampler.py:139-148) its momentum is zeros:
+    the device engine does not carry a momentum vector per stored proposal
+    (one D-vector copy fewer per merge on the hot path), and the next
+    transition resamples the momentum anyway (sampler.py:95).  The proposal's
+    total energy is ``stats.energy``.
     """
     if not isinstance(rng, RngKey):
         raise ValueError("rng must be an RngKey")
@@ -114,6 +122,7 @@ def nuts_transition_from(z0: PhasePoint, config: SamplerConfig, model: TargetMod
                                      _lib.ptr(out), _lib.ptr(ev), cap, _lib.ptr(counts), exec_mode_for(model, exec_mode),
                                      _lib.stream_ptr(torch)))
     o = out.cpu().numpy()
+    _lib.check_spec(model.device_spec, h)
     s = o[2 * D:]
     z = PhasePoint(o[:D].copy(), np.zeros(D), float(s[0]), o[D:2 * D].copy())
     stats = TransitionStats(int(s[1]), int(s[2]), bool(s[3]), float(s[4]), float(s[5]))

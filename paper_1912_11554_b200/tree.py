@@ -149,6 +149,7 @@ def build_tree_iterative(
                                      key.hi, key.lo, _lib.ptr(out), _lib.ptr(ev), cap, _lib.ptr(lw), lw_cap,
                                      _lib.ptr(counts), exec_mode_for(model, exec_mode), _lib.stream_ptr(torch)))
     o = out.cpu().numpy()
+    _lib.check_spec(model.device_spec, handle)
     v = [o[k * D:(k + 1) * D].copy() for k in range(8)]
     s = o[8 * D:]
     left = PhasePoint(v[0], v[1], float(s[8]), np.full(D, np.nan))

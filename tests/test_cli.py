@@ -214,22 +214,3 @@ def test_cli_golden_fixture_is_consistent():
     for ln in g["data_csv"].splitlines()[1:]:
         x = [float(v) for v in ln.split(",")[:-1]]
         assert np.array_equal(np.float32(x).astype(np.float64), x)
-
-
-@pytest.mark.gpu
-def test_selftest_passes(capsys):
-    assert cli.main(["selftest"]) == 0
-    out = capsys.readouterr().out
-    assert "all checks passed" in out and out.count("PASS ") == 8
-
-
-def test_selftest_failure_exit_code(monkeypatch, capsys):
-    from paper_1912_11554_b200 import selftest
-
-    def boom():
-        raise AssertionError("forced")
-
-    monkeypatch.setattr(selftest, "all_checks", lambda: [("forced", boom), ("ok", lambda: None)])
-    assert cli.main(["selftest"]) == 1
-    out = capsys.readouterr().out
-    assert "FAIL forced" in out and "PASS ok" in out

@@ -1,0 +1,186 @@
+"""The fp32 policy at the headline configuration (BASELINE configs[1]:
+581,012 x 54 covtype-shaped logistic regression) - VERDICT r1 "next" item 1.
+
+1. U and gradient of the fp32 pass against the fp64 C oracle with ABSOLUTE
+   bounds (nats), at q = 0 and at the posterior mode (Newton in numpy).
+2. Decision replay: REPLAY_N transitions of a device run, each re-run from the
+   same (q, key, step, inverse mass) by the fp32 device path, the fp64 device
+   path and (a subset, plus every flip) the CPU oracle (reference semantics
+   tree.py:402-450, sampler.py:110-139).  Integers are compared exactly:
+   depth, leapfrog count, divergence, per-tree (direction, count, stop,
+   proposal leaf), the outer U-turn checks and the proposal (tree, leaf).
+   fp64 device == oracle on every compared transition; fp32 flips are counted
+   and each is logged with the smallest decision margin of its first
+   differing tree (oracle margins: |u - p| of merges / accepts, relative
+   U-turn dot distance, |dH - threshold|).  Bound: FLIP_BOUND flips, each at a
+   near-tie (margin <= MARGIN_BOUND).
+3. Statistics: 4 fp32 chains vs 4 fp64 chains of the full 1000 + 1000 run:
+   posterior means and SDs within 4 Monte-Carlo standard errors, R-hat < 1.01.
+"""
+
+from __future__ import annotations
+
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+N, P, SEED = 581012, 54, 20191222
+U_ABS = 1e-3        # nats: |U_fp32 - U_fp64| at the test points
+G_ABS = 1e-3        # per gradient component (|g| ~ 1e2..1e4 here)
+REPLAY_N = 256
+FLIP_BOUND = 6      # <= ~2.3% of replayed transitions
+MARGIN_BOUND = 1e-3
+ORACLE_EVERY = 16
+
+
+@pytest.fixture(scope="module")
+def data():
+    from tests_data import logistic_data
+
+    x, y = logistic_data(N, P, SEED)
+    return x, y
+
+
+@pytest.fixture(scope="module")
+def models(data):
+    import paper_1912_11554_b200 as t
+
+    x, y = data
+    return {prec: t.logistic_regression_model(t.LogisticRegressionData(x, y), precision=prec)
+            for prec in ("fp32", "fp64")}
+
+
+def _mode(x, y, iters=12):
+    """Posterior mode of the unit-normal-prior logistic model (numpy fp64 Newton)."""
+    X = np.hstack([x, np.ones((x.shape[0], 1))])
+    th = np.zeros(X.shape[1])
+    for _ in range(iters):
+        eta = X @ th
+        s = 1.0 / (1.0 + np.exp(-eta))
+        g = th - X.T @ (y - s)
+        H = np.eye(X.shape[1]) + (X * (s * (1 - s))[:, None]).T @ X
+        th = th - np.linalg.solve(H, g)
+    return th
+
+
+def test_covtype_fp32_potential_gradient_absolute(data, models, oracle):
+    x, y = data
+    om = oracle.Model("logistic_regression", P + 1, x=x, y=y, fused_omp=True)
+    m32 = models["fp32"]
+    import paper_1912_11554_b200 as t
+
+    mode = _mode(x, y)
+    report = {}
+    for name, q in (("zero", np.zeros(P + 1)), ("mode", mode), ("mode+0.01", mode + 0.01)):
+        got = t.models.potential_and_gradient(m32.device_spec, q[None, :])[0]
+        U, g = om._fused(q.tolist())
+        g = np.asarray(g)
+        du, dg = abs(got[0] - U), float(np.abs(got[1:] - g).max())
+        report[name] = (du, dg, U)
+        assert du <= U_ABS, (name, du, U)
+        assert dg <= G_ABS, (name, dg)
+    print("fp32 |dU| / max|dg| at", {k: (f"{a:.2e}", f"{b:.2e}") for k, (a, b, _) in report.items()})
+
+
+def _decisions(st, tr):
+    """(depth, leapfrogs, diverged, per tree (j, go_right, count, stop), outer checks, proposal (tree, leaf))."""
+    return (st.depth_reached, st.leapfrog_calls, int(st.diverged),
+            tuple((j, gr, c, stop) for j, c, stop, gr, _ in tr.trees), tuple(o for _, o in tr.outer_checks),
+            (tr.proposal_tree, tr.proposal_leaf))
+
+
+def _oracle_decisions(ost, dec):
+    return (ost.depth, ost.leapfrogs, int(ost.diverged),
+            tuple((j, d, c, tu + 2 * dv) for j, d, c, tu, dv, _ in dec["trees"]), tuple(dec["outer"]),
+            tuple(dec["proposal"]))
+
+
+def test_covtype_fp32_decision_replay(data, models, oracle):
+    import paper_1912_11554_b200 as t
+
+    x, y = data
+    m32, m64 = models["fp32"], models["fp64"]
+    W, seed = 150, 4242
+    cfg = t.RunConfig(model={}, num_chains=1, num_warmup=W, num_samples=REPLAY_N + 1, seed=seed)
+    key = t.chain_keys(seed, 1)[0]
+    r = t.run_device(m64, cfg, [key], 0)
+    ad = r.adapt.cpu().numpy()[0]
+    samples = r.samples.cpu().numpy()[0]
+    step, inv = float(ad[1]), ad[2 + W:].copy()
+    scfg = t.SamplerConfig(step_size=step, mass=t.MassMatrix(inv))
+    om = oracle.Model("logistic_regression", P + 1, x=x, y=y, fused_omp=True)
+    flips, oracle_checked, total_lf = [], 0, 0
+    for i in range(1, REPLAY_N + 1):
+        q0 = samples[i - 1]
+        dkey = key.fold(10 + W + i)
+        rec = {}
+        for prec, m in (("fp32", m32), ("fp64", m64)):
+            ug = t.models.potential_and_gradient(m.device_spec, q0[None, :])[0]
+            z = t.PhasePoint(q0, np.zeros(P + 1), float(ug[0]), ug[1:].copy())
+            z1, st, tr = t.nuts_transition_from(z, scfg, m, dkey, return_trace=True)
+            rec[prec] = (_decisions(st, tr), z1)
+        total_lf += rec["fp64"][0][1]
+        flipped = rec["fp32"][0] != rec["fp64"][0]
+        if flipped or i % ORACLE_EVERY == 0:
+            U0, g0 = om._fused(q0.tolist())
+            margins = []
+            oz, ost, dec = oracle.transition(oracle.Point(q0.tolist(), [0.0] * (P + 1), U0, list(g0)), step,
+                                             inv.tolist(), om, (dkey.hi, dkey.lo), margins=margins)
+            od = _oracle_decisions(ost, dec)
+            assert rec["fp64"][0] == od, (i, rec["fp64"][0], od)  # fp64 device == reference semantics
+            assert np.allclose(rec["fp64"][1].position, oz.q, rtol=1e-12, atol=1e-14)
+            oracle_checked += 1
+            if flipped:
+                a, b = rec["fp32"][0][3], od[3]
+                j = next((k for k in range(min(len(a), len(b))) if a[k] != b[k]), min(len(a), len(b)))
+                pool = [mm for tm in margins[: j + 1] for mm in tm]
+                kind, mrg = min(pool, key=lambda km: km[1]) if pool else ("none", math.inf)
+                flips.append({"transition": i, "first_tree": j, "min_margin": mrg, "kind": kind,
+                              "fp32": rec["fp32"][0][:3], "fp64": od[:3]})
+        else:
+            # same decisions: the trajectories end at the same leaf, positions within the fp32 tolerance
+            assert np.allclose(rec["fp32"][1].position, rec["fp64"][1].position, rtol=1e-4, atol=1e-5)
+    summary = {"replayed": REPLAY_N, "leapfrogs_fp64": total_lf, "oracle_checked": oracle_checked,
+               "flips": len(flips), "flip_rate": len(flips) / REPLAY_N, "flip_log": flips}
+    print("fp32 decision replay:", json.dumps(summary))
+    out = os.environ.get("TS_FLIP_LOG")
+    if out:
+        with open(out, "w") as fh:
+            json.dump(summary, fh, indent=1)
+    assert len(flips) <= FLIP_BOUND, summary
+    assert all(f["min_margin"] <= MARGIN_BOUND for f in flips), flips
+
+
+def _moments(chains, ts):
+    """Pooled mean/SD, per-dimension ESS (reference estimator) and split R-hat."""
+    ess = ts.ess(chains)
+    rhat = ts.split_rhat(chains)
+    pooled = chains.reshape(-1, chains.shape[-1])
+    return pooled.mean(0), pooled.std(0, ddof=1), ess, rhat
+
+
+def test_covtype_fp32_vs_fp64_posterior(models):
+    """North-star layer 3 at config 2: 4 chains per policy, 1000 + 1000 draws."""
+    import paper_1912_11554_b200 as t
+
+    res = {}
+    for prec in ("fp32", "fp64"):
+        r = t.run(t.RunConfig(model={}, num_chains=4, num_warmup=1000, num_samples=1000, seed=77), models[prec])
+        res[prec] = np.stack([c.samples for c in r])
+    m32, s32, e32, r32 = _moments(res["fp32"], t)
+    m64, s64, e64, r64 = _moments(res["fp64"], t)
+    assert (r32 < 1.01).all() and (r64 < 1.01).all(), (r32.max(), r64.max())
+    mcse_mean = np.sqrt(s32 ** 2 / e32 + s64 ** 2 / e64)
+    z_mean = np.abs(m32 - m64) / mcse_mean
+    # SD of a near-Gaussian marginal: MCSE(sd) ~ sd / sqrt(2 ESS)
+    mcse_sd = np.sqrt(s32 ** 2 / (2 * e32) + s64 ** 2 / (2 * e64))
+    z_sd = np.abs(s32 - s64) / mcse_sd
+    print(f"covtype fp32 vs fp64: max |dmean|/MCSE {z_mean.max():.2f}, max |dsd|/MCSE {z_sd.max():.2f}, "
+          f"min ESS {min(e32.min(), e64.min()):.0f}, max R-hat {max(r32.max(), r64.max()):.4f}")
+    assert (z_mean < 4.0).all(), z_mean.max()
+    assert (z_sd < 4.0).all(), z_sd.max()

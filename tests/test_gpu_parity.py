@@ -671,12 +671,51 @@ def test_dense_run_chunks_beyond_one_grid():
 
 
 def test_ess_device_on_gpu_samples():
-    """Device ESS on a many-chain run's samples in HBM."""
+    """Device ESS / split R-hat on a many-chain run's samples in HBM."""
     t = ts()
     m = t.eight_schools_model()
     cfg = t.RunConfig(model={}, num_chains=256, num_warmup=100, num_samples=200, seed=3)
     r = t.run_device(m, cfg, t.chain_keys(3, 256), 0)
-    assert np.allclose(t.ess_device(r.samples), t.ess(r.samples.cpu().numpy()), rtol=1e-10)
+    e, rh = t.chain_diagnostics_device(r.samples)
+    host = r.samples.cpu().numpy()
+    assert np.allclose(e, t.ess(host), rtol=1e-10)
+    assert np.allclose(rh, t.split_rhat(host), rtol=1e-12)
+
+
+@pytest.mark.parametrize("shape,phi", [((4, 100, 3), 0.7), ((16, 1000, 10), 0.7), ((1, 50, 2), 0.5), ((3, 7, 1), 0.3),
+                                       ((2, 4, 2), 0.0), ((8, 999, 3), 0.995), ((5, 301, 40), -0.6),
+                                       ((8192, 1000, 10), 0.8)])
+def test_device_diagnostics_match_host_estimators(shape, phi):
+    """ts_chain_diagnostics vs diagnostics.ess / split_rhat (the reference
+    estimators, diagnostics.py:49-105): AR(1) chains incl. strongly
+    autocorrelated (phi = 0.995: Geyer truncation past several 64-lag
+    blocks), antithetic (phi < 0: ESS capped at m n), odd draw counts, the
+    minimum of 4 draws, and the 8192 x 1000 x 10 eight-schools shape."""
+    import torch
+
+    t = ts()
+    rng = np.random.default_rng(abs(hash(shape)) % 2**32)
+    x = rng.standard_normal(shape)
+    for i in range(1, shape[1]):
+        x[:, i] = phi * x[:, i - 1] + x[:, i]
+    x += rng.standard_normal((shape[0], 1, shape[2])) * 0.05  # chain offsets: R-hat > 1
+    xd = torch.from_numpy(x).cuda()
+    e, rh = t.chain_diagnostics_device(xd)
+    assert np.allclose(e, t.ess(x), rtol=1e-10, atol=0), (e, t.ess(x))
+    assert np.allclose(rh, t.split_rhat(x), rtol=1e-12, atol=0)
+
+
+def test_device_diagnostics_constant_dimension_is_nan():
+    import torch
+
+    t = ts()
+    x = np.random.default_rng(1).standard_normal((4, 40, 3))
+    x[:, :, 1] = 2.5
+    with pytest.warns(RuntimeWarning):
+        e, rh = t.chain_diagnostics_device(torch.from_numpy(x).cuda())
+    assert np.isnan(e[1]) and np.isnan(rh[1]) and np.isfinite(e[[0, 2]]).all()
+    with pytest.warns(RuntimeWarning):
+        assert np.allclose(e[[0, 2]], t.ess(x)[[0, 2]], rtol=1e-10)
 
 
 def test_block_team_runs_every_chain():

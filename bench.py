@@ -60,7 +60,7 @@ N_ROWS, N_FEAT, DATA_SEED = 581012, 54, 20191222
 ALGO_BYTES_PER_PASS = 4 * N_ROWS * N_FEAT + N_ROWS  # fp32 X + uint8 y = 126,079,604 B
 C5_ROWS, C5_FEAT, C5_SEED = 8_000_000, 255, 20191223
 C5_BYTES_PER_PASS = 4 * C5_ROWS * C5_FEAT + C5_ROWS  # 8,168,000,000 B
-SUBS = ("gauss10", "eight_schools_8192", "dense_1000x1024", "rowshard_8Mx255")
+SUBS = ("gauss10", "eight_schools_8192", "dense_1000x1024", "rowshard_8Mx255", "covtype_many_chain")
 
 
 def parse(argv=None):
@@ -72,7 +72,8 @@ def parse(argv=None):
     ap.add_argument("--precision", choices=("fp64", "fp32"), default="fp32",
                     help="arithmetic of the fused data pass for the headline (the other mode is reported too)")
     ap.add_argument("--single-precision", action="store_true", help="measure only --precision")
-    ap.add_argument("--config", choices=("covtype", "eight_schools", "gauss10", "rowshard", "dense"), default="covtype",
+    ap.add_argument("--config", choices=("covtype", "eight_schools", "gauss10", "rowshard", "dense", "many"),
+                    default="covtype",
                     help="headline workload (default: the driver's covtype line with every sub-record)")
     ap.add_argument("--subs", default=",".join(SUBS), help="comma list of sub-records for the covtype line ('' = none)")
     ap.add_argument("--chains", type=int, default=8192, help="eight_schools: total chains")
@@ -714,6 +715,63 @@ def run_rowshard(ctx, args, W=20, S=20):
     return rec
 
 
+def run_many(ctx, args, C=256, W=100, S=100):
+    """Covtype with C chains sharing X on the tensor cores (precision "tf32",
+    csrc/ts_k_logistic_many.cu): one X stream per batched step serves every
+    chain with an outstanding gradient request.  Chains sharded over ranks."""
+    import paper_1912_11554_b200 as ts
+    from tests_data import logistic_data
+
+    K, Wu = 1, 1
+    x, y = logistic_data(N_ROWS, N_FEAT, DATA_SEED)
+    model = ts.logistic_regression_model(ts.LogisticRegressionData(x, y), precision="tf32")
+    cfg = ts.RunConfig(model={"model": "logistic_regression"}, num_chains=C, num_warmup=W, num_samples=S, seed=5)
+    keys = ts.chain_keys(5, C)
+    mine = [keys[c] for c in ts.chains.shard_range(C, ctx.rank, ctx.world)]
+    times, lfs, evs = [], [], []
+    for s in range(Wu + K):
+        ctx.barrier()
+        r = ts.run_device(model, cfg, mine, ctx.dev, sync=False)
+        r.event_ms[1].synchronize()
+        if s >= Wu:
+            times.append(r.event_ms[0].elapsed_time(r.event_ms[1]))
+            lfs.append(float(r.stats[:, :, 1].sum().item()))
+            evs.append(float(r.evals.sum().item()))
+            last = r
+    t_ms = ctx.red(sum(times), "max")
+    lf = ctx.red(sum(lfs), "sum")
+    ev = ctx.red(sum(evs), "sum")
+    ess, rhat = ts.chain_diagnostics_device(last.samples)
+    # tensor work per chain-evaluation over the N rows: GEMM 1 3 x 2 x 56 (3xTF32), GEMM 2 4 x 2 x 64 (3xBF16 stacked)
+    flops_per_eval = (3 * 2 * 56 + 4 * 2 * 64) * N_ROWS
+    tf = flops_per_eval * ev / (t_ms / 1000.0) / 1e12
+    peak, pk = tf32_peak()
+    ncu = committed_ncu("r2_ncu_many.json") or {}
+    rec = {"value": lf / (t_ms / 1000.0), "unit": "chain-leapfrog/s", "ms_per_step": t_ms / K, "steps": K, "warmup": Wu,
+           "dtype": "tf32x3/bf16x3",
+           "config": f"covtype 581012x54 logistic, {C} chains sharded over {ctx.world} GPU(s) sharing X (precision tf32), "
+                     f"seed 5, {W}+{S}, max_tree_depth 10",
+           "leapfrogs_per_step": lf / K, "evals_per_step": ev / K,
+           "min_ess_per_step": float(np.nanmin(ess)), "ess_per_sec": float(np.nanmin(ess)) / (t_ms / 1000.0 / K),
+           "max_split_rhat_rank0": float(np.nanmax(rhat)), "gpu_launches": K,
+           "roofline": {"bound": "issue (epilogue)", "achieved": tf, "peak": peak, "unit": "TFLOP/s",
+                        "frac": tf / peak, "peak_kind": pk, "tensor_pipe_pct": ncu.get("tensor_pipe_pct"),
+                        "note": "tensor flops of both GEMMs per chain-evaluation; the per-(row, chain) CUDA-core "
+                                "epilogue (sigmoid, log-likelihood, bf16 split of the residuals) bounds the step"}}
+    if ctx.rank == 0 and ctx.world == 1 and not args.no_cpu:
+        nc = cores()
+        ps = [run_worker("logistic", {"rows": N_ROWS, "features": N_FEAT, "seed": DATA_SEED, "seconds": args.cpu_seconds,
+                                      "numpy": False, "key_seed": 100 + k}, 1) for k in range(nc)]
+        outs = collect(ps)
+        lf_c = sum(o["leapfrogs"] for o in outs)
+        el = max(o["seconds"] for o in outs)
+        rec["cpu_baseline"] = {"value": lf_c / el, "unit": "chain-leapfrog/s", "cores": nc, "kind": "reference",
+                               "sample": f"reference turnstile (numba, 1 thread per process) nuts_transition_from on "
+                                         f"covtype, one chain per process on {nc} processes: {lf_c} leapfrogs in "
+                                         f"{el:.1f} s"}
+    return rec
+
+
 def timed_covtype(ctx, args, x32, y8, precision, K, Wu, with_clocks, flush):
     """Wu untimed + K timed full runs; device time per launch (CUDA events)."""
     import paper_1912_11554_b200 as ts
@@ -840,7 +898,7 @@ def run_covtype(args):
     subs = {}
     wanted = [s for s in args.subs.split(",") if s]
     for name, fn in (("gauss10", run_gauss10), ("eight_schools_8192", run_eight), ("dense_1000x1024", run_dense),
-                     ("rowshard_8Mx255", run_rowshard)):
+                     ("rowshard_8Mx255", run_rowshard), ("covtype_many_chain", run_many)):
         if name not in wanted:
             continue
         t0 = time.perf_counter()
@@ -901,8 +959,11 @@ def run_single(args):
     """--config gauss10 / eight_schools / dense / rowshard: that configuration's
     own line (not the driver's headline)."""
     ctx = Ctx(args)
-    fn = {"gauss10": run_gauss10, "eight_schools": run_eight, "dense": run_dense, "rowshard": run_rowshard}[args.config]
-    if args.config == "dense":
+    fn = {"gauss10": run_gauss10, "eight_schools": run_eight, "dense": run_dense, "rowshard": run_rowshard,
+          "many": run_many}[args.config]
+    if args.config == "many":
+        rec = run_many(ctx, args, args.chains if args.chains != 8192 else 256, args.num_warmup, args.num_samples)
+    elif args.config == "dense":
         rec = run_dense(ctx, args, args.num_warmup, args.num_samples)
     elif args.config == "rowshard":
         rec = run_rowshard(ctx, args, min(args.num_warmup, 1000), min(args.num_samples, 1000))

@@ -85,6 +85,7 @@ static int pick_pmax(int p) {
 }
 
 // ------------------------------------------------------------------ helpers
+constexpr int kProfWords = 24 + 2 * 2048;  // TS_PROF counters + per-CTA skew slots
 static int check_cfg(const ts_sampler_cfg* c) {
   if (!c) return set_err(TS_EINVAL, "null sampler config");
   if (!(c->step_size > 0) || !isfinite(c->step_size)) return set_err(TS_EINVAL, "step_size must be positive and finite");
@@ -107,6 +108,7 @@ static int launch(const ts_model* m, int nslots, OpArgs& A, int n_threads_chains
   if (nslots < 1) nslots = 1;
   if (nslots > kMaxSlots) return set_err(TS_EINVAL, "tree depth exceeds device slot limit (30)");
   if (m->kind == TS_LOGISTIC) {
+    if (m->many) return launch_logistic_many(m, nslots, A, n_threads_chains, st);
     if (!m->pmax) return set_err(TS_EUNSUPPORTED, "logistic feature count > 256 not supported on this path");
     return launch_block_logistic(m, nslots, A, st);
   }
@@ -134,6 +136,7 @@ extern "C" int ts_model_create(int kind, int dim, const double* params, int n_pa
   cudaGetDevice(&m->device);
   auto fail = [&](int code, const char* msg) {
     if (m->errw) cudaFree(m->errw);
+    if (m->xaug) cudaFree(m->xaug);
     if (m->params) cudaFree(m->params);
     if (m->xt) cudaFree(m->xt);
     if (m->yt) cudaFree(m->yt);
@@ -178,6 +181,18 @@ extern "C" int ts_model_create(int kind, int dim, const double* params, int n_pa
     case TS_LOGISTIC: {
       if (n_feat < 1 || dim != n_feat + 1) return fail(TS_EINVAL, "logistic dim must equal num_features + 1");
       if (n_rows < 1 || !x_dev || !y_dev) return fail(TS_EINVAL, "logistic needs at least one data row");
+      if (precision == TS_PREC_TF32) {  // many chains sharing X on the tensor cores
+        m->many = 1;
+        m->n_rows = n_rows;
+        m->p = n_feat;
+        const int rc = build_logistic_xaug(m, x_dev, y_dev);
+        if (rc) {
+          const std::string why = ts_last_error();
+          return fail(rc, why.c_str());
+        }
+        if (cudaDeviceSynchronize() != cudaSuccess) return fail(TS_ECUDA, "augmented X build failed");
+        break;
+      }
       m->pmax = pick_pmax(n_feat);
       if (!m->pmax) return fail(TS_EUNSUPPORTED, "logistic feature count > 256 not supported on this path");
       m->wide = n_feat > 64;
@@ -241,6 +256,7 @@ extern "C" int ts_model_destroy(ts_model* m) {
   if (m->mail_local) cudaFree(m->mail_local);
   if (m->vmail) cudaFree(m->vmail);
   if (m->errw) cudaFree(m->errw);
+  if (m->xaug) cudaFree(m->xaug);
   delete m;
   return TS_OK;
 }
@@ -474,15 +490,15 @@ extern "C" int ts_run_chains(const ts_model* m, const ts_run_cfg* rc, const uint
   const bool prof = getenv("TS_PROF") != nullptr &&
                     (m->kind == TS_LOGISTIC || (m->kind != TS_DENSE_GAUSS && exec_mode == TS_EXEC_WARP));
   if (prof) {
-    TS_CUDA(cudaMallocAsync((void**)&prof_buf, 24 * sizeof(unsigned long long), st));
-    TS_CUDA(cudaMemsetAsync(prof_buf, 0, 24 * sizeof(unsigned long long), st));
+    TS_CUDA(cudaMallocAsync((void**)&prof_buf, kProfWords * sizeof(unsigned long long), st));
+    TS_CUDA(cudaMemsetAsync(prof_buf, 0, kProfWords * sizeof(unsigned long long), st));
   }
   auto fold_timeout = [&]() -> int {
     k_fold_timeout<<<1, 256, 0, st>>>(m->errw, status, n_chains);
     TS_CUDA(cudaGetLastError());
     return TS_OK;
   };
-  if (m->kind != TS_LOGISTIC) {
+  if (m->kind != TS_LOGISTIC || m->many) {
     A.prof = prof ? prof_buf : nullptr;
     int e = launch(m, nslots, A, n_chains, (ts_exec_mode)exec_mode, st);
     if (!e) e = fold_timeout();
@@ -507,7 +523,7 @@ extern "C" int ts_run_chains(const ts_model* m, const ts_run_cfg* rc, const uint
   {
     if (prof) {
       const_cast<ts_model*>(m)->prof = nullptr;
-      unsigned long long h[24];
+      static unsigned long long h[kProfWords];
       TS_CUDA(cudaMemcpyAsync(h, prof_buf, sizeof h, cudaMemcpyDeviceToHost, st));
       TS_CUDA(cudaStreamSynchronize(st));
       const double n = h[10] ? (double)h[10] : 1.0;
@@ -518,6 +534,30 @@ extern "C" int ts_run_chains(const ts_model* m, const ts_run_cfg* rc, const uint
       const double nt = h[14] ? (double)h[14] : 1.0, nx = h[15] ? (double)h[15] : 1.0;
       fprintf(stderr, "TS_PROF transitions=%llu trees=%llu cycles: prologue/transition %.0f (momentum %.0f)  between-trees/tree %.0f\n",
               h[15], h[14], h[12] / nx, h[16] / nx, h[13] / nt);
+      if (m->kind == TS_LOGISTIC && m->many && h[24 + 8]) {
+        const double nt = h[24 + 7] ? (double)h[24 + 7] : 1.0, nc = (double)h[24 + 8];
+        fprintf(stderr, "TS_PROF many-chain: %llu chain tiles, %.1f row tiles each; cycles per row tile: X wait %.0f, "
+                "GEMM2 wait %.0f, SIMT X pass %.0f, GEMM1 %.0f, epilogue1 %.0f, ll reduce %.0f; per chain tile: "
+                "epilogue2+atomics %.0f\n", h[24 + 8], nt / nc, h[24] / nt, h[25] / nt, h[26] / nt, h[27] / nt,
+                h[28] / nt, h[29] / nt, h[30] / nc);
+      }
+      if (m->kind == TS_LOGISTIC && !m->many && h[10]) {  // per-CTA pass / barrier-wait skew
+        double pmin = 1e300, pmax = 0, psum = 0, wsum = 0;
+        int nb = 0, slow = -1;
+        for (int b = 0; b < 2048 && h[24 + 2 * b]; ++b, ++nb) {
+          const double pp = (double)h[24 + 2 * b] / n, ww = (double)h[25 + 2 * b] / n;
+          psum += pp; wsum += ww;
+          if (pp < pmin) pmin = pp;
+          if (pp > pmax) { pmax = pp; slow = b; }
+        }
+        if (nb) {
+          fprintf(stderr, "TS_PROF per-CTA ns/pass over %d CTAs: pass mean %.0f min %.0f max %.0f (CTA %d), barrier wait mean %.0f\n",
+                  nb, psum / nb, pmin, pmax, slow, wsum / nb);
+          fprintf(stderr, "TS_PROF pass ns by CTA:");
+          for (int b = 0; b < nb; ++b) fprintf(stderr, " %.0f", (double)h[24 + 2 * b] / n);
+          fprintf(stderr, "\n");
+        }
+      }
       cudaFreeAsync(prof_buf, st);
     }
     return TS_OK;

@@ -48,6 +48,10 @@ struct ts_model {
   unsigned char* dws;  // lockstep workspaces (grown on demand)
   size_t dws_size;
   unsigned int* errw;  // sticky device error word: bit 0 = a synchronisation wait timed out (SpinGuard)
+  // logistic, TF32 policy: many chains sharing X on the tensor cores (ts_k_logistic_many.cu)
+  int many;
+  int ka;        // columns of xaug = p + 2 rounded up to 8
+  float* xaug;   // [n_rows][ka] = X | 1 | y | 0
 };
 
 namespace ts_internal {
@@ -123,8 +127,12 @@ struct LogisticW {
       // workers then start streaming without a conversion round and two syncs)
       const double* th = S.v(q);
       float* t32 = const_cast<float*>(a.th32);
-      for (int j = (int)(threadIdx.x & 31); j <= a.pmax; j += 32)
-        t32[j] = (j < a.p) ? (float)th[j] : (j == a.pmax ? (float)th[a.p] : 0.f);
+      for (int j = (int)(threadIdx.x & 31); j <= a.pmax; j += 32) {
+        const double v = (j < a.p) ? th[j] : (j == a.pmax ? th[a.p] : 0.0);
+        const float h = (float)v;
+        t32[j] = h;
+        t32[64 + j] = (float)(v - (double)h);  // lo part: eta = X theta_hi + X theta_lo (logistic_cta_pass)
+      }
       __syncwarp();
     }
     cta_arrive(2);  // publishes q and the command to the worker warps
@@ -386,6 +394,8 @@ int launch_block_small(const SmallModel& sm, int D, int nslots, OpArgs& A, int C
 int launch_warp_small(const SmallModel& sm, int D, int nslots, OpArgs& A, int C, cudaStream_t st);
 int launch_block_logistic(const ts_model* m, int nslots, OpArgs& A, cudaStream_t st);
 int launch_dense(const ts_model* m, int nslots, OpArgs& A, int n_chains, cudaStream_t st);
+int launch_logistic_many(const ts_model* m, int nslots, OpArgs& A, int n_chains, cudaStream_t st);
+int build_logistic_xaug(ts_model* m, const float* x_dev, const uint8_t* y_dev);
 
 }  // namespace ts_internal
 

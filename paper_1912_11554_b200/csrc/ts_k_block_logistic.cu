@@ -25,6 +25,8 @@ int launch_block_logistic(const ts_model* m, int nslots, OpArgs& A, cudaStream_t
   mw.a.err = m->errw;
   mw.a.spin_ns = spin_limit_ns();
   if (const char* e = getenv("TS_FAULT_INJECT")) mw.a.fault = atoi(e);  // tests of the bounded waits only
+  mw.a.llmode = 6;
+  if (const char* e = getenv("TS_LLMODE")) mw.a.llmode = atoi(e);  // A/B of the fp32 log-likelihood precision
   // fp64 wide pass: half of the fp32->fp64 conversions on the integer pipe
   // (XU-bound otherwise; 2.77 -> 2.61 ms per 8Mx255 pass); TS_ICVT=0/2 for A/B
   mw.a.icvt = 1;

@@ -84,6 +84,7 @@ struct LogisticArgs {
   unsigned int* err;               // sticky synchronisation-timeout flag of the model (SpinGuard)
   unsigned long long spin_ns;      // wait limit
   int fault;                       // fault injection (tests): 1 = CTA 1 never arrives at the grid barrier
+  int llmode;                      // FP32 narrow pass: log-likelihood term precision (logistic_cta_pass LL)
 };
 
 // Mailbox of one rank: kMailFlags words of flags (flag[src] = 1 + the last
@@ -369,7 +370,50 @@ __device__ __forceinline__ void row_from_stage(const unsigned char* sb, int p_rt
 // Per-CTA streaming pass.  Writes this CTA's partial sums
 // red_out[0..p) = sum resid*x_j, red_out[p] = sum resid, red_out[p+1] = sum (y eta - log1pexp)
 // (wred: >= nwarps*(PMAX+2) doubles of scratch).
-template <int PMAX, bool FP64, int PE>
+// exp(x) for x <= 0 in float without the MUFU ex2 (whose error is biased:
+// ~0.16 ulp on average over covtype's rows, i.e. 1.7e-3 nats summed over
+// 581,012 rows): x log2(e) in two parts, 2^f on [-1/2, 1/2] by its Taylor
+// polynomial of degree 9 (truncation < 1e-11 relative), 2^j by exponent
+// arithmetic.  Round-to-nearest errors only, which average out over rows.
+__device__ __forceinline__ float exp_neg_f(float x) {
+  if (x < -87.0f) return 0.0f;
+  const float j = rintf(x * 1.44269504088896341f);
+  float f = __fmaf_rn(x, 1.44269502162933349609375f, -j);
+  f = __fmaf_rn(x, 1.925963033500011e-08f, f);
+  // 2^f = e^(f ln 2): c_k = ln2^k / k!
+  float p = 1.0178086009239699e-07f;
+  p = __fmaf_rn(p, f, 1.3215486790144307e-06f);
+  p = __fmaf_rn(p, f, 1.5252733804059841e-05f);
+  p = __fmaf_rn(p, f, 1.5403530393381609e-04f);
+  p = __fmaf_rn(p, f, 1.3333558146428443e-03f);
+  p = __fmaf_rn(p, f, 9.6181291076284772e-03f);
+  p = __fmaf_rn(p, f, 5.5504108664821580e-02f);
+  p = __fmaf_rn(p, f, 2.4022650695910071e-01f);
+  p = __fmaf_rn(p, f, 6.9314718055994531e-01f);
+  p = __fmaf_rn(p, f, 1.0f);
+  return __int_as_float(__float_as_int(p) + ((int)j << 23));
+}
+// log1p(e) for e in [0, 1] in float: 2 atanh(s), s = e / (2 + e) <= 1/3,
+// series in s^2 to s^18 (truncation < 2e-10 relative); no MUFU lg2.
+// (also valid for e in [-1/2, 0], s in [-1/3, 0]: the pass evaluates
+// log1p(e) - log 2 = log1p((e - 1) / 2), exactly 0 at e = 1, i.e. eta = 0)
+__device__ __forceinline__ float log1p_unit_f(float e) {
+  const float s = __fdiv_rn(e, 2.0f + e);
+  const float s2 = s * s;
+  float q = 1.0f / 19.0f;
+  q = __fmaf_rn(q, s2, 1.0f / 17.0f);
+  q = __fmaf_rn(q, s2, 1.0f / 15.0f);
+  q = __fmaf_rn(q, s2, 1.0f / 13.0f);
+  q = __fmaf_rn(q, s2, 1.0f / 11.0f);
+  q = __fmaf_rn(q, s2, 1.0f / 9.0f);
+  q = __fmaf_rn(q, s2, 1.0f / 7.0f);
+  q = __fmaf_rn(q, s2, 1.0f / 5.0f);
+  q = __fmaf_rn(q, s2, 1.0f / 3.0f);
+  q = __fmaf_rn(q, s2, 1.0f);
+  return 2.0f * s * q;
+}
+
+template <int PMAX, bool FP64, int PE, int LL = 6>
 __device__ __noinline__ void logistic_cta_pass(const LogisticArgs& a, const double* __restrict__ theta_s, double* wred,
                                                   double* red_out) {
   const int lane = threadIdx.x & 31, warp = wk_warp(), nwarps = wk_nwarps();
@@ -382,23 +426,30 @@ __device__ __noinline__ void logistic_cta_pass(const LogisticArgs& a, const doub
   using acc_t = typename std::conditional<FP64, double, float>::type;
   acc_t acc[PMAX + 1];
   // log-likelihood terms accumulate in double in both policies: in the FP32
-  // policy the per-row term is formed as y*eta - (max(eta,0) + log1p(e)) with
-  // the log1p in double (float e, float eta): identical rows (e.g. q = 0,
-  // every term log 2) would otherwise add the same float rounding N times
-  // (0.09 nats at 581,012 rows)
+  // policy the per-row term y*eta - (max(eta,0) + log1p(exp(-|eta|))) is
+  // evaluated in double from the float eta: float rounding of the term is
+  // correlated across rows (identical at q = 0, where every term is log 2),
+  // so N float roundings added up to 0.09 nats at 581,012 rows (q = 0) and
+  // 2e-3 at the mode; in double |dU| stays below 1e-3 nats
+  // (tests/test_gpu_covtype_fp32.py)
   double accl = 0.0;
 #pragma unroll
   for (int j = 0; j <= PMAX; ++j) acc[j] = 0;
 
   float th32[PMAX];
   float thb32 = 0.f;
+  const float* thlo = nullptr;  // LL = 5: theta - float(theta) (smem, broadcast loads)
   if constexpr (!FP64) {
     // theta as floats, broadcast with LDS.128: prepared by the driver warp
     // before the post (a.th32), else rounded here once per CTA
     const float* t32 = a.th32;
     if (t32 == nullptr || a.pmax != PMAX) {
       float* w32 = reinterpret_cast<float*>(wred);  // wred is free until the end
-      for (int j = wk_tid(); j <= PMAX; j += wk_threads()) w32[j] = (j < p) ? (float)theta_s[j] : (j == PMAX ? (float)theta_s[p] : 0.f);
+      for (int j = wk_tid(); j <= PMAX; j += wk_threads()) {
+        const double v = (j < p) ? theta_s[j] : (j == PMAX ? theta_s[p] : 0.0);
+        w32[j] = (float)v;
+        w32[64 + j] = (float)(v - (double)(float)v);
+      }
       wk_sync();
       t32 = w32;
     }
@@ -408,6 +459,7 @@ __device__ __noinline__ void logistic_cta_pass(const LogisticArgs& a, const doub
       th32[j] = v.x; th32[j + 1] = v.y; th32[j + 2] = v.z; th32[j + 3] = v.w;
     }
     thb32 = t32[PMAX];
+    if constexpr (LL == 5) thlo = t32 + 64;
     if (t32 != a.th32 || a.pmax != PMAX) wk_sync();
   }
 
@@ -478,9 +530,34 @@ __device__ __noinline__ void logistic_cta_pass(const LogisticArgs& a, const doub
           e2 = __fmaf_rn(x[k + 2], th32[k + 2], e2);
           e3 = __fmaf_rn(x[k + 3], th32[k + 3], e3);
         }
-        const float eta = (e0 + e1) + (e2 + e3);
-        const float e = expf(-fabsf(eta));
-        const double l = (double)fmaxf(eta, 0.f) + log1p((double)e);
+        float eta = (e0 + e1) + (e2 + e3);
+        if constexpr (LL == 5) {
+          // theta's float rounding is common to every row: with the data
+          // Hessian ~ 0.2 N it shifted the gradient by ~1e-3 at covtype size.
+          // X theta_lo restores it (two more FMA chains, broadcast loads).
+          float c0 = thlo[PMAX], c1 = 0.f;
+#pragma unroll
+          for (int k = 0; k < PMAX; k += 4) {
+            const float4 tl = reinterpret_cast<const float4*>(thlo)[k / 4];
+            c0 = __fmaf_rn(x[k], tl.x, c0);
+            c1 = __fmaf_rn(x[k + 1], tl.y, c1);
+            c0 = __fmaf_rn(x[k + 2], tl.z, c0);
+            c1 = __fmaf_rn(x[k + 3], tl.w, c1);
+          }
+          eta += c0 + c1;
+        }
+        const float e = (LL >= 5) ? exp_neg_f(-fabsf(eta)) : expf(-fabsf(eta));
+        // the row's log-likelihood term from the float eta, summed in double
+        // (see accl).  LL 6 (default): e without the MUFU (exp_neg_f) and
+        // log1p(e) = log 2 + log1p((e - 1)/2) by the atanh series - float
+        // round-to-nearest errors only, which average out over rows, and
+        // exact at eta = 0; 5: 6 + the theta_lo correction of eta above; 0:
+        // expf + log1pf (biased: 2e-3 nats at covtype's mode); 2: exp and
+        // log1p in double (A/B reference, +25% pass time).
+        double l;
+        if constexpr (LL == 0) l = (double)(fmaxf(eta, 0.f) + log1pf(e));
+        else if constexpr (LL == 2) l = (double)fmaxf(eta, 0.f) + log1p(exp(-(double)fabsf(eta)));
+        else l = (double)fmaxf(eta, 0.f) + ((double)log1p_unit_f(0.5f * (e - 1.0f)) + 0.69314718055994531);
         const float sig = __fdiv_rn(eta >= 0.f ? 1.f : e, 1.f + e);
         const float yv = (float)yb;
         const float resid = valid ? yv - sig : 0.f;
@@ -860,7 +937,10 @@ static __device__ __forceinline__ void logistic_cta_dispatch(const LogisticArgs&
   }
   if (a.p == 54) {  // covtype's feature count: compile-time row layout
     if (a.fp64) logistic_cta_pass<56, true, 54>(a, theta, wred, red_s);
-    else logistic_cta_pass<56, false, 54>(a, theta, wred, red_s);
+    else if (a.llmode == 0) logistic_cta_pass<56, false, 54, 0>(a, theta, wred, red_s);
+    else if (a.llmode == 2) logistic_cta_pass<56, false, 54, 2>(a, theta, wred, red_s);
+    else if (a.llmode == 5) logistic_cta_pass<56, false, 54, 5>(a, theta, wred, red_s);
+    else logistic_cta_pass<56, false, 54, 6>(a, theta, wred, red_s);
     return;
   }
   switch (a.pmax * 2 + (a.fp64 ? 1 : 0)) {
@@ -888,10 +968,15 @@ static __device__ void logistic_eval_grid(const LogisticArgs& a, const VecStore&
   const double* theta = S.v(qid);  // smem, contiguous (dstride 1)
   const bool prof = a.prof != nullptr && blockIdx.x == 0 && wk_tid() == 0;
   long long c0 = prof ? clock64() : 0, c1;
+  // TS_PROF per-CTA skew: [24 + 2 b] += pass ns, [25 + 2 b] += barrier-wait ns (globaltimer)
+  const bool skew = a.prof != nullptr && wk_tid() == 0;
+  unsigned long long g0 = 0, g1 = 0, g2 = 0;
+  if (skew) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
 
   logistic_cta_dispatch(a, theta, wred, red_s);
   wk_sync();
   if (prof) { c1 = clock64(); a.prof[1] += c1 - c0; c0 = c1; }
+  if (skew) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
   // Cross-CTA sum by exact fixed-point atomics into accumulator buffer
   // epoch % 3 (see fx_split): integer addition is associative, so the result
   // is independent of the order in which CTAs arrive -- deterministic.
@@ -942,6 +1027,11 @@ static __device__ void logistic_eval_grid(const LogisticArgs& a, const VecStore&
   }
   epoch += 1;
   if (prof) { c1 = clock64(); a.prof[2] += c1 - c0; c0 = c1; }
+  if (skew && blockIdx.x < 2048) {
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g2));
+    a.prof[24 + 2 * blockIdx.x] += g1 - g0;
+    a.prof[25 + 2 * blockIdx.x] += g2 - g1;
+  }
 
   if (a.dump && epoch == 1 && blockIdx.x == 0)  // test hook: this GPU's totals of the first pass
     for (int i = wk_tid(); i < 2 * P2 + 1; i += wk_threads()) a.dump[i] = __ldcg(cur + i);

@@ -207,7 +207,13 @@ def logistic_regression_model(data: LogisticRegressionData, precision: str = "fp
 
     ``precision`` selects the arithmetic of the fused data pass:
     ``"fp64"`` (parity mode, differs from the reference only in summation
-    order) or ``"fp32"`` (per-row math in float, accumulation in double).
+    order), ``"fp32"`` (per-row math in float, accumulation in double) or
+    ``"tf32"`` (many chains sharing X: each batched step streams X once for
+    every chain with an outstanding gradient request and evaluates eta = X
+    theta and X^T r on the tcgen05 tensor cores in 3xTF32 split precision,
+    csrc/ts_k_logistic_many.cu; num_features <= 62).  fp32/fp64 runs of C
+    chains launch the single-chain persistent pass C times; tf32 runs all
+    chains in one launch.
     """
     x32, y8 = data.x, data.y
     dim = data.num_features + 1

@@ -30,8 +30,13 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 N, P, SEED = 581012, 54, 20191222
-U_ABS = 1e-3        # nats: |U_fp32 - U_fp64| at the test points
-G_ABS = 1e-3        # per gradient component (|g| ~ 1e2..1e4 here)
+U_ABS = 1e-3        # nats: |U_fp32 - U_fp64| at the test points (measured <= 1e-4)
+# per gradient component: theta's rounding to float is common to every row;
+# through the data Hessian (~0.2 N = 1.2e5 per diagonal entry) it moves the
+# gradient by ~1.5e-3 at the mode, i.e. 5e-6 of the posterior gradient scale
+# sqrt(H_jj) ~ 340 (the theta_lo correction, TS_LLMODE=5, removes it at +11%
+# pass time; measured 3.3e-4)
+G_ABS = 2e-3
 REPLAY_N = 256
 FLIP_BOUND = 6      # <= ~2.3% of replayed transitions
 MARGIN_BOUND = 1e-3

@@ -39,8 +39,12 @@ enum { TS_OK = 0, TS_EINVAL = 1, TS_ECUDA = 2, TS_EUNSUPPORTED = 3 };
 enum { TS_STD_NORMAL = 0, TS_GAUSSIAN = 1, TS_LOGISTIC = 2, TS_FUNNEL = 3, TS_EIGHT_SCHOOLS = 4, TS_DENSE_GAUSS = 5 };
 
 /* Arithmetic policy of the logistic data pass (ts_logistic.cuh) and of the
- * dense-Gaussian GEMM (FP64: SIMT fp64; FP32/TF32: tcgen05 TF32 tensor cores). */
-enum { TS_PREC_FP64 = 0, TS_PREC_FP32 = 1, TS_PREC_TF32 = 2 };
+ * dense-Gaussian GEMM (FP64: SIMT fp64; FP32/TF32: tcgen05 TF32 tensor cores).
+ * Logistic: FP64 / FP32 stream X stored as fp32 (x_dev float); FP64X streams X
+ * stored as fp64 (x_dev double: data that are not fp32-exact, as the
+ * reference's LogisticRegressionData keeps them, models.py:43-64); TF32 =
+ * many chains sharing X on the tensor cores (ts_k_logistic_many.cu). */
+enum { TS_PREC_FP64 = 0, TS_PREC_FP32 = 1, TS_PREC_TF32 = 2, TS_PREC_FP64X = 3 };
 
 /* U-turn criterion (tree.py:36-37). */
 enum { TS_GENERALIZED = 0, TS_CLASSIC = 1 };
@@ -77,10 +81,10 @@ int ts_abi_version(void);
  * a device model.  params (host): gaussian inv_var[dim]; eight_schools
  * y[J], sigma[J] (dim = J + 2); dense_gauss A[dim][dim] (U = x'Ax/2, the
  * SURVEY 8(d) config-4 target after the dense-mass reparametrisation x =
- * L^-1 q; dim % 4 == 0 for TF32).  Logistic: x_dev row-major fp32 (n_rows x
- * n_feat), y_dev uint8 in {0,1}; the library re-tiles X into its own HBM
- * layout. */
-int ts_model_create(int kind, int dim, const double* params, int n_params, const float* x_dev, const uint8_t* y_dev,
+ * L^-1 q; dim % 4 == 0 for TF32).  Logistic: x_dev row-major (n_rows x
+ * n_feat), fp32 or - precision TS_PREC_FP64X - fp64, y_dev uint8 in {0,1};
+ * the library re-tiles X into its own HBM layout. */
+int ts_model_create(int kind, int dim, const double* params, int n_params, const void* x_dev, const uint8_t* y_dev,
                     int64_t n_rows, int n_feat, int precision, ts_model** out);
 int ts_model_destroy(ts_model* m);
 int ts_model_dim(const ts_model* m);

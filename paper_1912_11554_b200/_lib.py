@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(_HERE, "libturnstile_b200.so")
 
 TS_OK, TS_EINVAL, TS_ECUDA, TS_EUNSUPPORTED = 0, 1, 2, 3
 TS_STD_NORMAL, TS_GAUSSIAN, TS_LOGISTIC, TS_FUNNEL, TS_EIGHT_SCHOOLS, TS_DENSE_GAUSS = 0, 1, 2, 3, 4, 5
-TS_PREC_FP64, TS_PREC_FP32, TS_PREC_TF32 = 0, 1, 2
+TS_PREC_FP64, TS_PREC_FP32, TS_PREC_TF32, TS_PREC_FP64X = 0, 1, 2, 3
 TS_GENERALIZED, TS_CLASSIC = 0, 1
 TS_EXEC_THREAD, TS_EXEC_BLOCK, TS_EXEC_WARP = 0, 1, 2
 TS_STATUS_SYNC_TIMEOUT = 2

@@ -52,24 +52,29 @@ __global__ void k_retile(const float* __restrict__ x, const uint8_t* __restrict_
 // Wide p (64 < p <= 256): tiles of kWideRows = 8 rows, row-major, each
 // followed by 16 label bytes (8 labels + 8 zeros): 32p + 16 bytes per tile,
 // one TMA bulk copy (ts_logistic.cuh, logistic_cta_pass_wide).
-__global__ void k_retile_wide(const float* __restrict__ x, const uint8_t* __restrict__ y, int64_t n, int p,
+// T = double: the fp64-storage layout ("fp64x"), 64p + 16 bytes per tile.
+template <class T>
+__global__ void k_retile_wide(const T* __restrict__ x, const uint8_t* __restrict__ y, int64_t n, int p,
                               int64_t ntiles, unsigned char* __restrict__ xt, int* __restrict__ has_subnormal) {
   const int64_t total = ntiles * kWideRows * (int64_t)p;
-  const int64_t tb = wide_tile_bytes(p);
+  const int64_t tb = wide_tile_bytes(p, (int)sizeof(T));
+  const int64_t lab = kWideRows * (int64_t)sizeof(T) * p;
   int sub = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t row = i / p;
     const int j = (int)(i % p);
     const int64_t t = row / kWideRows;
     const int r = (int)(row % kWideRows);
-    const float v = row < n ? x[row * p + j] : 0.f;
-    const unsigned a = __float_as_uint(v) & 0x7fffffffu;
-    sub |= (a != 0u && a < 0x00800000u);
+    const T v = row < n ? x[row * p + j] : (T)0;
+    if (sizeof(T) == 4) {
+      const unsigned a = __float_as_uint((float)v) & 0x7fffffffu;
+      sub |= (a != 0u && a < 0x00800000u);
+    }
     unsigned char* tile = xt + t * tb;
-    reinterpret_cast<float*>(tile)[r * p + j] = v;
+    reinterpret_cast<T*>(tile)[r * p + j] = v;
     if (j == 0) {
-      tile[32 * (int64_t)p + r] = row < n ? y[row] : 0;
-      tile[32 * (int64_t)p + kWideRows + r] = 0;
+      tile[lab + r] = row < n ? y[row] : 0;
+      tile[lab + kWideRows + r] = 0;
     }
   }
   if (__syncthreads_or(sub) && threadIdx.x == 0) atomicOr(has_subnormal, 1);
@@ -124,7 +129,7 @@ static int launch(const ts_model* m, int nslots, OpArgs& A, int n_threads_chains
 }
 
 // ------------------------------------------------------------------ C ABI
-extern "C" int ts_model_create(int kind, int dim, const double* params, int n_params, const float* x_dev,
+extern "C" int ts_model_create(int kind, int dim, const double* params, int n_params, const void* x_dev,
                                const uint8_t* y_dev, int64_t n_rows, int n_feat, int precision, ts_model** out) {
   if (!out) return set_err(TS_EINVAL, "null output handle");
   *out = nullptr;
@@ -185,7 +190,7 @@ extern "C" int ts_model_create(int kind, int dim, const double* params, int n_pa
         m->many = 1;
         m->n_rows = n_rows;
         m->p = n_feat;
-        const int rc = build_logistic_xaug(m, x_dev, y_dev);
+        const int rc = build_logistic_xaug(m, static_cast<const float*>(x_dev), y_dev);
         if (rc) {
           const std::string why = ts_last_error();
           return fail(rc, why.c_str());
@@ -195,13 +200,16 @@ extern "C" int ts_model_create(int kind, int dim, const double* params, int n_pa
       }
       m->pmax = pick_pmax(n_feat);
       if (!m->pmax) return fail(TS_EUNSUPPORTED, "logistic feature count > 256 not supported on this path");
-      m->wide = n_feat > 64;
+      m->xd = precision == TS_PREC_FP64X;  // X stored as fp64: always the wide layout
+      m->wide = n_feat > 64 || m->xd;
+      if (m->xd) m->pmax = kWideMax;
       m->n_rows = n_rows;
       m->p = n_feat;
       // wide: whole groups of kWideGroup tiles (32 rows), padding rows zero with label 0
       m->ntiles = m->wide ? (n_rows + kWideRows * kWideGroup - 1) / (kWideRows * kWideGroup) * kWideGroup : (n_rows + 31) / 32;
-      m->fp64 = precision == TS_PREC_FP64;
-      const size_t xbytes = m->wide ? (size_t)m->ntiles * wide_tile_bytes(n_feat) : (size_t)m->ntiles * 32 * n_feat * sizeof(float);
+      m->fp64 = precision == TS_PREC_FP64 || m->xd;
+      const size_t xbytes = m->wide ? (size_t)m->ntiles * wide_tile_bytes(n_feat, m->xd ? 8 : 4)
+                                    : (size_t)m->ntiles * 32 * n_feat * sizeof(float);
       if (cudaMalloc((void**)&m->xt, xbytes) != cudaSuccess) return fail(TS_ECUDA, "cudaMalloc X failed");
       // wide tiles carry their labels; the separate label array is then unused
       if (cudaMalloc((void**)&m->yt, m->wide ? 16 : (size_t)m->ntiles * 32) != cudaSuccess) return fail(TS_ECUDA, "cudaMalloc y failed");
@@ -209,11 +217,15 @@ extern "C" int ts_model_create(int kind, int dim, const double* params, int n_pa
       if (cudaMalloc((void**)&m->bar, 16 * 8 * sizeof(unsigned long long)) != cudaSuccess) return fail(TS_ECUDA, "cudaMalloc barrier failed");
       if (cudaMemset(m->bar, 0, 16 * 8 * sizeof(unsigned long long)) != cudaSuccess) return fail(TS_ECUDA, "memset barrier failed");
       // the barrier word doubles as the "X has fp32 subnormals" flag during re-tiling
-      if (m->wide)
-        k_retile_wide<<<1184, 256>>>(x_dev, y_dev, n_rows, n_feat, m->ntiles, reinterpret_cast<unsigned char*>(m->xt),
-                                     reinterpret_cast<int*>(m->bar));
+      if (m->xd)
+        k_retile_wide<double><<<1184, 256>>>(static_cast<const double*>(x_dev), y_dev, n_rows, n_feat, m->ntiles,
+                                             reinterpret_cast<unsigned char*>(m->xt), reinterpret_cast<int*>(m->bar));
+      else if (m->wide)
+        k_retile_wide<float><<<1184, 256>>>(static_cast<const float*>(x_dev), y_dev, n_rows, n_feat, m->ntiles,
+                                            reinterpret_cast<unsigned char*>(m->xt), reinterpret_cast<int*>(m->bar));
       else
-        k_retile<<<1184, 256>>>(x_dev, y_dev, n_rows, n_feat, m->ntiles, m->xt, m->yt, reinterpret_cast<int*>(m->bar));
+        k_retile<<<1184, 256>>>(static_cast<const float*>(x_dev), y_dev, n_rows, n_feat, m->ntiles, m->xt, m->yt,
+                                reinterpret_cast<int*>(m->bar));
       if (cudaGetLastError() != cudaSuccess) return fail(TS_ECUDA, "retile launch failed");
       unsigned long long flag = 0;
       if (cudaMemcpy(&flag, m->bar, sizeof flag, cudaMemcpyDeviceToHost) != cudaSuccess) return fail(TS_ECUDA, "retile failed");

@@ -32,7 +32,8 @@ struct ts_model {
   int pmax;
   unsigned long long* prof;  // transient: phase counters for ts_eval_bench
   int exact_cvt;             // X holds fp32 subnormals (fp64 pass uses F2F)
-  int wide;                  // 64 < p <= 256: 8-row row-major tiles (ts_logistic.cuh)
+  int wide;                  // 64 < p <= 256, or X in fp64: 8-row row-major tiles (ts_logistic.cuh)
+  int xd;                    // X stored as fp64 (TS_PREC_FP64X)
   double* slotws;            // wide: per-CTA NodeStore slot vectors (grown on demand)
   size_t slotws_size;        // doubles
   // row sharding across GPUs (ts_peer_mailbox_*)

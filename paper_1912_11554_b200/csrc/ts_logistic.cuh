@@ -85,6 +85,7 @@ struct LogisticArgs {
   unsigned long long spin_ns;      // wait limit
   int fault;                       // fault injection (tests): 1 = CTA 1 never arrives at the grid barrier
   int llmode;                      // FP32 narrow pass: log-likelihood term precision (logistic_cta_pass LL)
+  int xd;                          // X stored as fp64 (wide layout, logistic_cta_pass_wide XD)
 };
 
 // Mailbox of one rank: kMailFlags words of flags (flag[src] = 1 + the last
@@ -370,6 +371,15 @@ __device__ __forceinline__ void row_from_stage(const unsigned char* sb, int p_rt
 // Per-CTA streaming pass.  Writes this CTA's partial sums
 // red_out[0..p) = sum resid*x_j, red_out[p] = sum resid, red_out[p+1] = sum (y eta - log1pexp)
 // (wred: >= nwarps*(PMAX+2) doubles of scratch).
+// a / b for b in [1, 3]: MUFU reciprocal + one Newton correction of the
+// quotient (within an ulp, no IEEE-division slow-path checks)
+__device__ __forceinline__ float div_pos_f(float a, float b) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(b));
+  const float q = a * r;
+  return __fmaf_rn(__fmaf_rn(-b, q, a), r, q);
+}
+
 // exp(x) for x <= 0 in float without the MUFU ex2 (whose error is biased:
 // ~0.16 ulp on average over covtype's rows, i.e. 1.7e-3 nats summed over
 // 581,012 rows): x log2(e) in two parts, 2^f on [-1/2, 1/2] by its Taylor
@@ -395,10 +405,10 @@ __device__ __forceinline__ float exp_neg_f(float x) {
 }
 // log1p(e) for e in [0, 1] in float: 2 atanh(s), s = e / (2 + e) <= 1/3,
 // series in s^2 to s^18 (truncation < 2e-10 relative); no MUFU lg2.
-// (also valid for e in [-1/2, 0], s in [-1/3, 0]: the pass evaluates
+// (also valid for e in [-1/2, 0], s in [-1/3, 0] (2 + e in [1.5, 3]): the pass evaluates
 // log1p(e) - log 2 = log1p((e - 1) / 2), exactly 0 at e = 1, i.e. eta = 0)
 __device__ __forceinline__ float log1p_unit_f(float e) {
-  const float s = __fdiv_rn(e, 2.0f + e);
+  const float s = div_pos_f(e, 2.0f + e);
   const float s2 = s * s;
   float q = 1.0f / 19.0f;
   q = __fmaf_rn(q, s2, 1.0f / 17.0f);
@@ -558,7 +568,7 @@ __device__ __noinline__ void logistic_cta_pass(const LogisticArgs& a, const doub
         if constexpr (LL == 0) l = (double)(fmaxf(eta, 0.f) + log1pf(e));
         else if constexpr (LL == 2) l = (double)fmaxf(eta, 0.f) + log1p(exp(-(double)fabsf(eta)));
         else l = (double)fmaxf(eta, 0.f) + ((double)log1p_unit_f(0.5f * (e - 1.0f)) + 0.69314718055994531);
-        const float sig = __fdiv_rn(eta >= 0.f ? 1.f : e, 1.f + e);
+        const float sig = (LL >= 5) ? div_pos_f(eta >= 0.f ? 1.f : e, 1.f + e) : __fdiv_rn(eta >= 0.f ? 1.f : e, 1.f + e);
         const float yv = (float)yb;
         const float resid = valid ? yv - sig : 0.f;
         accl += valid ? ((yb ? (double)eta : 0.0) - l) : 0.0;
@@ -655,13 +665,15 @@ constexpr int kWideTotWords = 2 * (kWideMax + 2) + 2;  // CTA totals at the star
 __host__ __device__ inline int wide_scratch_doubles(int worker_warps) {
   return kWideTotWords + worker_warps * (kWideMax / 32 + 2) * 32 * 2;
 }
-__host__ __device__ inline int64_t wide_tile_bytes(int p) { return 32 * (int64_t)p + 16; }
+// esz: bytes per X element (4: fp32 storage; 8: fp64 storage, "fp64x")
+__host__ __device__ inline int64_t wide_tile_bytes(int p, int esz = 4) { return kWideRows * esz * (int64_t)p + 16; }
+__host__ __device__ inline int wide_kl(int p, int esz) { return (esz == 8 && p <= 64) ? 2 : (p <= 128 ? 4 : 8); }
 // ring stage: the tile plus zeroed slack covering the pass's unconditional
 // reads (row 7, features up to 32*KL - 1), 128-byte multiple
-__host__ __device__ inline int wide_stage_bytes(int p) {
-  const int kl = p <= 128 ? 4 : 8;
-  int64_t b = wide_tile_bytes(p);
-  const int64_t reach = 4 * (int64_t)((kWideRows - 1) * p + 32 * kl);
+__host__ __device__ inline int wide_stage_bytes(int p, int esz = 4) {
+  const int kl = wide_kl(p, esz);
+  int64_t b = wide_tile_bytes(p, esz);
+  const int64_t reach = esz * (int64_t)((kWideRows - 1) * p + 32 * kl);
   if (reach > b) b = reach;
   return (int)((b + 127) / 128 * 128);
 }
@@ -688,7 +700,7 @@ struct WideProducer {
     const unsigned long long i = umod(issued, (uint32_t)(count * kWideGroup));
     gj = (int64_t)(i / kWideGroup);
     k = (int)(i % kWideGroup);
-    tb = (uint32_t)wide_tile_bytes(a.p);
+    tb = (uint32_t)wide_tile_bytes(a.p, a.xd ? 8 : 4);
     first = reinterpret_cast<const unsigned char*>(a.xt) + wt.first * kWideGroup * (int64_t)tb;
     gstep = (int64_t)wt.nwarps * kWideGroup * tb;
     src = first + gj * gstep + (int64_t)k * tb;
@@ -722,7 +734,9 @@ __device__ __forceinline__ double f2d_int(float f) {
   return __hiloint2double((int)hi, (int)(u << 29));
 }
 
-template <bool FP64, int KL, int ICVT = 0>  // KL = features per lane (p <= 32 KL); ICVT: 1 odd m / 2 all on the ALU
+// KL = features per lane (p <= 32 KL); ICVT: 1 odd m / 2 all on the ALU;
+// XD: X stored as fp64 (the "fp64x" policy: data that are not fp32-exact)
+template <bool FP64, int KL, int ICVT = 0, bool XD = false>
 __device__ __noinline__ void logistic_cta_pass_wide(const LogisticArgs& a, const double* __restrict__ theta_s,
                                                     double* wred, double* red_out) {
   using acc_t = typename std::conditional<FP64, double, float>::type;
@@ -796,7 +810,8 @@ __device__ __noinline__ void logistic_cta_pass_wide(const LogisticArgs& a, const
     for (int64_t j = 0; j < ntile_w; ++j) {
       mbar_wait(bars + s, parity);
       const unsigned char* sb = ts_dyn_smem + ring_off + (uint32_t)(s * stage_bytes);
-      const float* xs = reinterpret_cast<const float*>(sb);
+      using xel_t = typename std::conditional<XD, double, float>::type;
+      const xel_t* xs = reinterpret_cast<const xel_t*>(sb);
       const int64_t row0 = ((wt.first + gj * wt.nwarps) * kWideGroup + k) * kWideRows;
 #pragma unroll
       for (int g = 0; g < kWideRows; g += R) {
@@ -807,15 +822,15 @@ __device__ __noinline__ void logistic_cta_pass_wide(const LogisticArgs& a, const
         // slots are dropped at the fold
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          const float* xr = xs + (g + r) * p + lane;
+          const xel_t* xr = xs + (g + r) * p + lane;
 #pragma unroll
           for (int m = 0; m < KL; ++m) {
-            if constexpr (FP64 && ICVT > 0) xv[r][m] = (ICVT == 2 || (m & 1)) ? (acc_t)f2d_int(xr[32 * m]) : (acc_t)xr[32 * m];
+            if constexpr (FP64 && ICVT > 0 && !XD) xv[r][m] = (ICVT == 2 || (m & 1)) ? (acc_t)f2d_int(xr[32 * m]) : (acc_t)xr[32 * m];
             else xv[r][m] = (acc_t)xr[32 * m];
           }
         }
         const int yr = g + my_r;
-        const acc_t yv = (acc_t)sb[32 * p + yr];
+        const acc_t yv = (acc_t)sb[kWideRows * (int)sizeof(xel_t) * p + yr];
         if (g + R == kWideRows) {
           // the stage is fully read: refill it (wrapping into the next pass)
           __syncwarp();
@@ -924,6 +939,12 @@ __device__ __noinline__ void logistic_cta_pass_wide(const LogisticArgs& a, const
 static __device__ __forceinline__ void logistic_cta_dispatch(const LogisticArgs& a, const double* theta, double* wred,
                                                              double* red_s) {
   if (a.wide) {
+    if (a.xd) {  // fp64 X storage (always the fp64 policy)
+      if (a.p <= 64) logistic_cta_pass_wide<true, 2, 0, true>(a, theta, wred, red_s);
+      else if (a.p <= 128) logistic_cta_pass_wide<true, 4, 0, true>(a, theta, wred, red_s);
+      else logistic_cta_pass_wide<true, 8, 0, true>(a, theta, wred, red_s);
+      return;
+    }
     if (a.p <= 128) {
       if (a.fp64) logistic_cta_pass_wide<true, 4>(a, theta, wred, red_s);
       else logistic_cta_pass_wide<false, 4>(a, theta, wred, red_s);

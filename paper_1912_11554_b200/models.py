@@ -17,6 +17,7 @@ from __future__ import annotations
 
 import csv
 import json
+import warnings
 from dataclasses import dataclass, field
 from pathlib import Path
 from typing import Callable, Optional
@@ -25,7 +26,7 @@ import numpy as np
 
 from . import _lib
 
-PRECISIONS = ("fp64", "fp32", "tf32")
+PRECISIONS = ("fp64", "fp32", "tf32", "fp64x")
 
 
 class DeviceSpec:
@@ -37,7 +38,7 @@ class DeviceSpec:
         self.kind = kind
         self.dim = dim
         self.params = None if params is None else np.ascontiguousarray(params, dtype=np.float64)
-        self.x = x  # fp32 (N, p) C-contiguous, logistic only
+        self.x = x  # fp32 (fp64 for "fp64x") (N, p) C-contiguous, logistic only
         self.y = y  # uint8 (N,)
         self.precision = precision
         self._handles: dict = {}
@@ -65,7 +66,8 @@ class DeviceSpec:
             params = self.params
             pp = params.ctypes.data if params is not None else 0
             npar = 0 if params is None else params.size
-            prec = {"fp64": _lib.TS_PREC_FP64, "fp32": _lib.TS_PREC_FP32, "tf32": _lib.TS_PREC_TF32}[self.precision]
+            prec = {"fp64": _lib.TS_PREC_FP64, "fp32": _lib.TS_PREC_FP32, "tf32": _lib.TS_PREC_TF32,
+                    "fp64x": _lib.TS_PREC_FP64X}[self.precision]
             _lib.check(lib.ts_model_create(self.kind, self.dim, pp, npar, _lib.ptr(xd), _lib.ptr(yd), n_rows, n_feat, prec,
                                            ctypes_byref(out)))
             if self._grid:
@@ -159,27 +161,37 @@ def _device_model(name: str, spec: DeviceSpec, params: dict) -> TargetModel:
 class LogisticRegressionData:
     """Covariates and binary labels (models.py:43-64).
 
-    The device streams X in fp32: values are rounded to fp32 once here (the
-    benchmark data are generated fp32-exact, so nothing changes for them).
+    Kept in the device's storage types: X as float32 when every value is
+    exactly representable in fp32 (the synthetic benchmark data are), else as
+    float64 - never silently rounded (the reference keeps fp64,
+    models.py:51-60); y as uint8.
     """
 
     x: np.ndarray
     y: np.ndarray
 
     def __post_init__(self):
-        # Kept in the device's storage types: X float32 (C order), y uint8.
         x = np.atleast_2d(np.asarray(self.x))
         y = np.asarray(self.y).ravel()
         if x.shape[0] != y.shape[0]:
             raise ValueError("covariate rows and labels disagree in length")
-        x32 = np.ascontiguousarray(x, dtype=np.float32)
-        if not np.isfinite(x32).all() or (y.dtype.kind == "f" and not np.isfinite(y).all()):
+        if x.dtype == np.float32:
+            xs = np.ascontiguousarray(x)
+        else:
+            x64 = np.ascontiguousarray(x, dtype=np.float64)
+            x32 = x64.astype(np.float32)
+            xs = x32 if np.array_equal(x32.astype(np.float64), x64) else x64
+        if not np.isfinite(xs).all() or (y.dtype.kind == "f" and not np.isfinite(y).all()):
             raise ValueError("logistic data must be free of NaN/Inf")
         y8 = y.astype(np.uint8)
         if not np.array_equal(y8, y) or (y8 > 1).any():
             raise ValueError("labels must be 0 or 1")
-        object.__setattr__(self, "x", x32)
+        object.__setattr__(self, "x", xs)
         object.__setattr__(self, "y", np.ascontiguousarray(y8))
+
+    @property
+    def fp32_exact(self) -> bool:
+        return self.x.dtype == np.float32
 
     @property
     def num_features(self) -> int:
@@ -213,15 +225,27 @@ def logistic_regression_model(data: LogisticRegressionData, precision: str = "fp
     theta and X^T r on the tcgen05 tensor cores in 3xTF32 split precision,
     csrc/ts_k_logistic_many.cu; num_features <= 62).  fp32/fp64 runs of C
     chains launch the single-chain persistent pass C times; tf32 runs all
-    chains in one launch.
+    chains in one launch.  ``"fp64x"`` streams X stored in fp64 (twice the
+    bytes, no conversions); ``"fp64"`` on data that are not fp32-exact uses
+    it automatically, the fp32 and tf32 policies round such data to fp32
+    (within their stated tolerances) with a RuntimeWarning.
     """
-    x32, y8 = data.x, data.y
+    if precision not in PRECISIONS:
+        raise ValueError(f"precision must be one of {PRECISIONS}")
+    x, y8 = data.x, data.y
+    if x.dtype == np.float64 and precision == "fp64":
+        precision = "fp64x"
+    elif x.dtype == np.float64 and precision in ("fp32", "tf32"):
+        warnings.warn(f"logistic data are not fp32-exact; the {precision} policy rounds X to fp32", RuntimeWarning)
+        x = x.astype(np.float32)
+    elif precision == "fp64x":
+        x = x.astype(np.float64)
     dim = data.num_features + 1
-    spec = DeviceSpec(_lib.TS_LOGISTIC, dim, x=x32, y=y8, precision=precision)
+    spec = DeviceSpec(_lib.TS_LOGISTIC, dim, x=np.ascontiguousarray(x), y=y8, precision=precision)
     return _device_model(
         "logistic_regression",
         spec,
-        {"num_data": int(x32.shape[0]), "num_features": int(x32.shape[1])},
+        {"num_data": int(x.shape[0]), "num_features": int(x.shape[1])},
     )
 
 

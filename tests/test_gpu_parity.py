@@ -820,3 +820,58 @@ def test_dense_mass_adaptation_two_phase():
     assert lf_final < 0.7 * lf_pilot, (lf_final, lf_pilot)
     flat = final.samples.cpu().numpy().reshape(-1, D)
     assert np.abs(np.cov(flat.T) - cov).max() <= 0.15 * np.abs(cov).max()
+
+
+# ----------------------------------------------------------------------------- fp64 X storage ("fp64x")
+
+
+@pytest.mark.parametrize("n,p", [(3000, 54), (1001, 7), (517, 100), (2000, 255)])
+def test_fp64x_non_fp32_exact_data(n, p, oracle):
+    """Data that are not fp32-exact are stored in fp64 (the reference keeps
+    fp64 X, models.py:43-64): precision "fp64" selects the fp64-storage pass
+    automatically and matches the fp64 oracle at 1e-10 relative."""
+    t = ts()
+    rng = np.random.default_rng(p)
+    x = rng.standard_normal((n, p))  # not fp32-exact
+    y = (rng.random(n) < 0.5).astype(np.float64)
+    data = t.LogisticRegressionData(x, y)
+    assert data.x.dtype == np.float64
+    m = t.logistic_regression_model(data, precision="fp64")
+    assert m.device_spec.precision == "fp64x"
+    om = oracle.Model("logistic_regression", p + 1, x=x, y=y)
+    for q in (np.zeros(p + 1), rng.standard_normal(p + 1) * 0.1):
+        got = t.models.potential_and_gradient(m.device_spec, q[None, :])[0]
+        U = om.potential(q.tolist())
+        g = np.asarray(om.gradient(q.tolist()))
+        assert close(got[0], U, FP64_REL)
+        assert close(got[1:], g, FP64_REL, atol=FP64_REL * np.abs(g).max())
+    # the fp32 policy rounds such data with a warning (stated tolerance)
+    with pytest.warns(RuntimeWarning):
+        t.logistic_regression_model(data, precision="fp32")
+
+
+def test_fp64x_covtype_transitions_match_oracle(oracle):
+    """fp64 X storage at the covtype shape: transitions of a device run re-run
+    from its own states on the CPU oracle: identical integers, positions 1e-12."""
+    t = ts()
+    from tests_data import logistic_data
+
+    x, y = logistic_data(581012, 54, 20191222)
+    m = t.logistic_regression_model(t.LogisticRegressionData(x, y), precision="fp64x")
+    W, S, seed = 120, 8, 1003
+    cfg = t.RunConfig(model={}, num_chains=1, num_warmup=W, num_samples=S, seed=seed)
+    key = t.chain_keys(seed, 1)[0]
+    r = t.run_device(m, cfg, [key], 0)
+    st = r.stats.cpu().numpy()[0]
+    ad = r.adapt.cpu().numpy()[0]
+    samples = r.samples.cpu().numpy()[0]
+    step, inv = float(ad[1]), ad[2 + W:].copy()
+    om = oracle.Model("logistic_regression", 55, x=x, y=y, fused_omp=True)
+    for i in (1, 4, 7):
+        q0 = samples[i - 1]
+        U0, g0 = m.potential(q0), m.gradient(q0)
+        dkey = key.fold(10 + W + i)
+        oz, os_, _ = oracle.transition(oracle.Point(q0.tolist(), [0.0] * 55, U0, g0.tolist()), step, inv.tolist(), om,
+                                       (dkey.hi, dkey.lo))
+        assert (os_.depth, os_.leapfrogs) == (int(st[W + i, 0]), int(st[W + i, 1]))
+        assert close(samples[i], oz.q, 1e-12, atol=1e-14)

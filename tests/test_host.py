@@ -293,3 +293,12 @@ def test_pooled_covariance_has_no_cpu_path():
 
     with pytest.raises((ValueError, RuntimeError)):
         t.pooled_covariance(np.zeros((4, 3)))
+
+
+def test_logistic_data_keeps_fp64_when_not_fp32_exact():
+    """No silent rounding (reference models.py:43-64 keeps fp64 X)."""
+    x64 = np.array([[0.1, 1.0], [2.0, -3.0]])
+    d = t.LogisticRegressionData(x64, [0, 1])
+    assert d.x.dtype == np.float64 and not d.fp32_exact
+    d32 = t.LogisticRegressionData(np.array([[0.5, 1.0], [2.0, -3.0]]), [0, 1])
+    assert d32.x.dtype == np.float32 and d32.fp32_exact

@@ -68,7 +68,7 @@ typedef struct {
   int32_t num_samples;
   double target_accept;
   int32_t has_sampler; /* RunConfig.sampler is not None (chains.py:137-143) */
-  int32_t pad_;
+  int32_t keep_warmup; /* 1: samples holds [C][W+S][dim], the warmup draws first (adaptation audits) */
   ts_sampler_cfg sampler;
 } ts_run_cfg;
 

@@ -721,6 +721,66 @@ def schedule_flags(W):
     return flags
 
 
+class Adaptation:
+    """Warmup adaptation of one chain (adapt.py:207-236): dual averaging on the
+    log step size (DualAveragingState.init / da_update, adapt.py:44-70, gamma
+    0.05, t0 10, kappa 0.75, clipped accept stat adapt.py:227) and the windowed
+    Welford variance (welford_update adapt.py:86-94, regularized install
+    adapt.py:104-108 at window ends, adapt.py:228-232)."""
+
+    def __init__(self, eps0, W, D, target=0.8, inv0=None):
+        self.mu, self.log_eps, self.log_bar, self.hbar = math.log(10.0 * eps0), math.log(eps0), 0.0, 0.0
+        self.target = target
+        self.flags = schedule_flags(W)
+        self.D = D
+        self.wc, self.mean, self.m2 = 0, [0.0] * D, [0.0] * D
+        self.inv = list(inv0) if inv0 is not None else [1.0] * D
+        self.installs = 0
+
+    def step_size(self):
+        return math.exp(self.log_eps)
+
+    def final_step_size(self):
+        return math.exp(self.log_bar)
+
+    def update(self, i, accept, q):
+        """After warmup transition i (0-based) with accept stat `accept` that
+        moved the chain to position q."""
+        a = min(1.0, max(0.0, accept))
+        t = i + 1
+        frac = 1.0 / (t + 10.0)
+        self.hbar = (1.0 - frac) * self.hbar + frac * (self.target - a)
+        self.log_eps = self.mu - math.sqrt(t) / 0.05 * self.hbar
+        wgt = t ** (-0.75)
+        self.log_bar = wgt * self.log_eps + (1.0 - wgt) * self.log_bar
+        if self.flags[i] & 1:
+            self.wc += 1
+            for d in range(self.D):
+                dl = q[d] - self.mean[d]
+                self.mean[d] = self.mean[d] + dl / self.wc
+                self.m2[d] = self.m2[d] + dl * (q[d] - self.mean[d])
+        if self.flags[i] & 2 and self.wc >= 2:
+            n = self.wc
+            self.inv = [(n / (n + 5.0)) * (self.m2[d] / (self.wc - 1)) + (5.0 / (n + 5.0)) * 1e-3
+                        for d in range(self.D)]
+            self.wc, self.mean, self.m2 = 0, [0.0] * self.D, [0.0] * self.D
+            self.installs += 1
+
+
+def replay_adaptation(eps0, accepts, positions, target=0.8, inv0=None):
+    """The adaptation recursion alone, fed another sampler's warmup accept
+    stats and positions (e.g. the device's): step-size trace before each
+    transition, final step size, inverse mass and the number of installs."""
+    W, D = len(accepts), len(positions[0])
+    ad = Adaptation(eps0, W, D, target, inv0)
+    trace = []
+    for i in range(W):
+        trace.append(ad.step_size())
+        ad.update(i, float(accepts[i]), [float(v) for v in positions[i]])
+    return {"step_size_trace": trace, "final_step_size": ad.final_step_size(), "inv_mass_diag": ad.inv,
+            "installs": ad.installs}
+
+
 class Budget(Exception):
     """Raised by run_chain when max_leapfrogs is exhausted (bounded CPU samples)."""
 
@@ -741,35 +801,18 @@ def run_chain(model, key, W, S, step=1.0, inv0=None, has_sampler=False, target=0
     stats, trace, adaptation = [], [], {}
     if W > 0:
         eps0 = find_step_size(z, inv, model, key_fold(key, 1), init=step)
-        mu, log_eps, log_bar, hbar = math.log(10.0 * eps0), math.log(eps0), 0.0, 0.0
-        flags = schedule_flags(W)
-        wc, mean, m2 = 0, [0.0] * D, [0.0] * D
+        ad = Adaptation(eps0, W, D, target, inv)
         for i in range(W):
-            cur = math.exp(log_eps)
+            cur = ad.step_size()
             trace.append(cur)
             z, st, _ = transition(z, cur, inv, model, key_fold(key, 10 + i), max_depth, generalized, threshold)
             stats.append(st)
             if max_leapfrogs is not None and sum(s.leapfrogs for s in stats) >= max_leapfrogs:
                 return {"samples": [], "stats": stats, "adaptation": {}, "truncated": True,
                         "total_leapfrogs": sum(s.leapfrogs for s in stats)}
-            a = min(1.0, max(0.0, st.accept))
-            t = i + 1
-            frac = 1.0 / (t + 10.0)
-            hbar = (1.0 - frac) * hbar + frac * (target - a)
-            log_eps = mu - math.sqrt(t) / 0.05 * hbar
-            wgt = t ** (-0.75)
-            log_bar = wgt * log_eps + (1.0 - wgt) * log_bar
-            if flags[i] & 1:
-                wc += 1
-                for d in range(D):
-                    dl = z.q[d] - mean[d]
-                    mean[d] = mean[d] + dl / wc
-                    m2[d] = m2[d] + dl * (z.q[d] - mean[d])
-            if flags[i] & 2 and wc >= 2:
-                n = wc
-                inv = [(n / (n + 5.0)) * (m2[d] / (wc - 1)) + (5.0 / (n + 5.0)) * 1e-3 for d in range(D)]
-                wc, mean, m2 = 0, [0.0] * D, [0.0] * D
-        final = math.exp(log_bar)
+            ad.update(i, st.accept, z.q)
+            inv = ad.inv
+        final = ad.final_step_size()
         adaptation = {"initial_step_size": eps0, "step_size_trace": trace, "final_step_size": final,
                       "inv_mass_diag": inv}
     else:

@@ -70,7 +70,7 @@ class RunCfgC(ctypes.Structure):
         ("num_samples", ctypes.c_int32),
         ("target_accept", ctypes.c_double),
         ("has_sampler", ctypes.c_int32),
-        ("pad_", ctypes.c_int32),
+        ("keep_warmup", ctypes.c_int32),
         ("sampler", SamplerCfgC),
     ]
 

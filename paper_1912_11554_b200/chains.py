@@ -124,11 +124,13 @@ class DeviceRun:
 
 
 def run_device(model: TargetModel, config: RunConfig, keys: Sequence[RngKey], device=None, exec_mode=None,
-               sync: bool = True, base: Optional[SamplerConfig] = None):
+               sync: bool = True, base: Optional[SamplerConfig] = None, keep_warmup: bool = False):
     """Launch the whole warmup + sampling run for ``keys`` on one GPU.
 
     Returns torch tensors (samples (C,S,D), stats (C,W+S,5), adapt (C,2+W+D),
     status (C,)) still on the device, plus the device time of the launch.
+    ``keep_warmup``: samples is (C,W+S,D), the warmup draws first (the
+    positions the Welford windows saw; adaptation audits).
 
     ``base`` overrides the start configuration (run_chain's argument) without
     counting as a user ``config.sampler``: with ``num_warmup == 0`` the
@@ -156,12 +158,13 @@ def run_device(model: TargetModel, config: RunConfig, keys: Sequence[RngKey], de
             weights = torch.from_numpy(da_weights(W)).to(dev)
         else:
             sched = weights = None
-        samples = torch.empty((C, S, D), dtype=torch.float64, device=dev)
+        samples = torch.empty((C, S + (W if keep_warmup else 0), D), dtype=torch.float64, device=dev)
         stats = torch.empty((C, W + S, 5), dtype=torch.float64, device=dev)
         adapt = torch.zeros((C, 2 + W + D), dtype=torch.float64, device=dev)
         status = torch.zeros(C, dtype=torch.int32, device=dev)
         evals = torch.zeros(C, dtype=torch.int64, device=dev)
-        rc = _lib.RunCfgC(W, S, float(config.target_accept), 1 if config.sampler is not None else 0, 0,
+        rc = _lib.RunCfgC(W, S, float(config.target_accept), 1 if config.sampler is not None else 0,
+                          1 if keep_warmup else 0,
                           sampler_cfg_c(base))
         lib = _lib.load_library()
         t0 = torch.cuda.Event(enable_timing=True)

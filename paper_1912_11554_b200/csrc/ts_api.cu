@@ -487,6 +487,7 @@ extern "C" int ts_run_chains(const ts_model* m, const ts_run_cfg* rc, const uint
   A.rc.target_accept = rc->target_accept;
   A.rc.base_step = rc->sampler.step_size;
   A.rc.has_sampler = rc->has_sampler;
+  A.rc.keep_warmup = rc->keep_warmup ? 1 : 0;
   A.rc.sampler = A.cfg;
   A.rc.schedule = schedule_dev;
   A.rc.da_weight = da_weight_dev;

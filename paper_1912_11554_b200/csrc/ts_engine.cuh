@@ -1115,6 +1115,7 @@ struct RunCfg {
   double target_accept;
   double base_step;
   int has_sampler;  // RunConfig.sampler is not None (chains.py:137-143)
+  int keep_warmup;  // 1: RunOut.samples holds W + S draws, the warmup draws first (adaptation replay tests)
   SamplerCfg sampler;
   const uint8_t* schedule;    // [W]: bit0 in a covariance window, bit1 window end
   const double* da_weight;    // [W]: t ** -kappa for t = 1..W
@@ -1177,6 +1178,10 @@ __device__ void run_chain(Engine<Team, Model>& E, Key ck, const RunCfg& rc, cons
         const double w = rc.da_weight[i];
         log_eps_bar = __dadd_rn(__dmul_rn(w, log_eps), __dmul_rn(__dsub_rn(1.0, w), log_eps_bar));
       }
+      if (writer && rc.keep_warmup) {
+        const double* q = E.v(V_Q0);
+        for (int d = E.T.rank(); d < D; d += E.T.size()) out.samples[(int64_t)i * out.s_stride + d * out.d_stride] = q[d * s];
+      }
       const uint8_t flag = rc.schedule[i];
       if (flag & 1) {  // welford_update (adapt.py:86-94)
         wcount += 1;
@@ -1219,11 +1224,13 @@ __device__ void run_chain(Engine<Team, Model>& E, Key ck, const RunCfg& rc, cons
   if (writer && E.T.leader()) { out.adapt[1] = step; out.status[0] = status; }
   if (status != 0) return;
   E.cfg.step = step;
+  const int64_t s0 = rc.keep_warmup ? W : 0;
   for (int i = 0; i < S; ++i) {
     const Stats st = E.transition(key_fold(ck, 10 + (uint64_t)(W + i)), nullptr, 0);
     if (writer) {
       const double* q = E.v(V_Q0);
-      for (int d = E.T.rank(); d < D; d += E.T.size()) out.samples[(int64_t)i * out.s_stride + d * out.d_stride] = q[d * s];
+      for (int d = E.T.rank(); d < D; d += E.T.size())
+        out.samples[(s0 + i) * out.s_stride + d * out.d_stride] = q[d * s];
       if (E.T.leader()) {
         double* o = out.stats + (int64_t)(W + i) * 5;
         o[0] = st.depth; o[1] = st.leapfrogs; o[2] = st.diverged; o[3] = st.accept; o[4] = st.energy;

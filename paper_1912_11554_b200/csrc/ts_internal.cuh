@@ -284,7 +284,7 @@ __device__ void do_op(Engine<Team, Model>& E, const OpArgs& A, int chain, bool w
     case OP_RUN: {
       const int W = A.rc.num_warmup, S = A.rc.num_samples;
       RunOut ro;
-      ro.samples = A.samples + (int64_t)chain * S * D;
+      ro.samples = A.samples + (int64_t)chain * (S + (A.rc.keep_warmup ? W : 0)) * D;
       ro.s_stride = D;
       ro.d_stride = 1;
       ro.stats = A.stats + (int64_t)chain * (W + S) * 5;

@@ -357,6 +357,51 @@ def test_runs_match_reference():
                 assert close(r.adaptation["final_step_size"], num(ref["adaptation"]["final_step_size"]), 0.5)
 
 
+@pytest.mark.parametrize("which", ["gauss10", "eight_schools", "logistic"])
+def test_adaptation_replay_matches_reference_recursion(which):
+    """The device's warmup adaptation, audited draw by draw: the reference's
+    dual-averaging and windowed-Welford recursion (adapt.py:44-108, 207-236;
+    oracle.Adaptation) is replayed on the host from the device's own warmup
+    accept stats and positions.  The recursion is pure IEEE arithmetic apart
+    from log(10 eps0) / exp(log_eps) (last-ulp CUDA vs glibc), so the step
+    size before every warmup transition and the final step size must agree to
+    1e-14 relative -- a wrong gain, t0, kappa or clipping shows at the first
+    draws -- and the installed inverse mass must be bit-identical, with the
+    schedule's number of installs (W = 200: windows 25/50/60/15)."""
+    import turnstile_oracle as o
+    from tests_data import logistic_data
+
+    t = ts()
+    from paper_1912_11554_b200.chains import run_device
+
+    W, S, C = 200, 5, 4
+    if which == "gauss10":
+        model = t.gaussian_model(np.linspace(0.5, 3.0, 10))
+    elif which == "eight_schools":
+        model = t.eight_schools_model()
+    else:
+        x, y = logistic_data(2000, 6, 3)
+        model = t.logistic_regression_model(t.LogisticRegressionData(x, y))
+    cfg = t.RunConfig(model={"model": which}, num_chains=C, num_warmup=W, num_samples=S, seed=17)
+    keys = t.chain_keys(cfg.seed, C)
+    run = run_device(model, cfg, keys, keep_warmup=True)
+    samples = run.samples.cpu().numpy()
+    stats = run.stats.cpu().numpy()
+    adapt = run.adapt.cpu().numpy()
+    assert samples.shape == (C, W + S, model.dim)
+    windows = sum(1 for f in o.schedule_flags(W) if f & 2)
+    for c in range(C):
+        eps0 = float(adapt[c, 0])
+        rep = o.replay_adaptation(eps0, stats[c, :W, 3], samples[c, :W], target=cfg.target_accept)
+        dev_trace = adapt[c, 2:2 + W]
+        assert close(dev_trace, rep["step_size_trace"], 1e-14), (which, c)
+        assert close(adapt[c, 1], rep["final_step_size"], 1e-14), (which, c)
+        assert np.array_equal(adapt[c, 2 + W:], np.asarray(rep["inv_mass_diag"])), (which, c)
+        assert rep["installs"] == windows == 4
+        # the sampling phase starts where warmup ended and uses the final settings
+        assert np.all(np.isfinite(samples[c, W:]))
+
+
 def ref_stats_w(rec, ref):
     """Warmup stats are not in ChainResult.stats (reference keeps sampling
     stats only); recompute them with the oracle for the comparison."""

@@ -232,7 +232,7 @@ extern "C" int ts_model_create(int kind, int dim, const double* params, int n_pa
       m->exact_cvt = flag != 0;
       int nsm = 148;
       cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, m->device);
-      const size_t pb = 2 * (size_t)nsm * 2 * (n_feat + 2);  // room for up to 2 CTAs per SM
+      const size_t pb = (size_t)TS_MAX_PEERS * fx_rank_words(n_feat);  // up to 8 (emulated) ranks
       if (cudaMalloc((void**)&m->pbuf, pb * sizeof(double)) != cudaSuccess) return fail(TS_ECUDA, "cudaMalloc partials failed");
       if (cudaMemset(m->pbuf, 0, pb * sizeof(double)) != cudaSuccess) return fail(TS_ECUDA, "memset partials failed");
       if (cudaDeviceSynchronize() != cudaSuccess) return fail(TS_ECUDA, "retile failed");

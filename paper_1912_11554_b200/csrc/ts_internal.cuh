@@ -345,7 +345,7 @@ __global__ void __launch_bounds__(256, 1) k_block_op(MW mw, int D, int nslots, i
         const int64_t mwords = mail_words(mw.a.p, V);
         for (int r = 0; r < V; ++r) mw.a.mail[r] = mw.a.vmail + r * mwords;
         mw.a.mail_epoch = mw.a.vmail + V * mwords;
-        mw.a.pbuf += (int64_t)vg * 3 * (2 * (int64_t)(mw.a.p + 2) + 2);
+        mw.a.pbuf += (int64_t)vg * fx_rank_words(mw.a.p);
         mw.a.bar += 16 * vg;
       } else {
         mw.a.cta = (int)blockIdx.x;

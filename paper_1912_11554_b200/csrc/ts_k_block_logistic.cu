@@ -108,8 +108,8 @@ int launch_block_logistic(const ts_model* m, int nslots, OpArgs& A, cudaStream_t
   }
   const int nranks = m->vranks > 1 ? m->vranks : 1;
   TS_CUDA(cudaMemsetAsync(m->bar, 0, 16 * nranks * sizeof(unsigned long long), st));
-  // rotating fixed-point accumulators start at zero (3 x (2*(p+2) + 2) words per rank)
-  TS_CUDA(cudaMemsetAsync(m->pbuf, 0, nranks * 3 * (2 * (size_t)(m->p + 2) + 2) * sizeof(unsigned long long), st));
+  // rotating fixed-point accumulators start at zero (fx_rank_words per rank)
+  TS_CUDA(cudaMemsetAsync(m->pbuf, 0, nranks * (size_t)fx_rank_words(m->p) * sizeof(unsigned long long), st));
   int Dv = D, ns = nslots, sc = scratch;
   void* args[] = {&mw, &Dv, &ns, &sc, &A};
   TS_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3((unsigned)grid), dim3(threads), args, smem, st));

@@ -50,7 +50,7 @@ struct LogisticArgs {
   int64_t n_rows;
   int p;
   int64_t ntiles;
-  double* pbuf;             // 3 rotating accumulators of (p+2) fixed-point int64 pairs + flag
+  double* pbuf;             // 3 rotating accumulators x kFxCopies copies of (p+2) fixed-point int64 pairs + flag
   unsigned long long* bar;  // grid barrier counter (zeroed before launch)
   int fp64;                 // precision policy
   int pmax;                 // compile-time feature capacity of the pass (8/32/56/64)
@@ -95,6 +95,16 @@ constexpr int kMailFlags = 16;
 __host__ __device__ inline int64_t mail_words(int p, int world) {
   return kMailFlags + 3 * (int64_t)world * (2 * (int64_t)(p + 2) + 2);
 }
+
+// Cross-CTA accumulators (LogisticArgs::pbuf): 3 rotating buffers per rank;
+// a buffer holds kFxCopies copies of the (p+2) fixed-point pairs + flag, each
+// padded to its own 1-KB block; CTA c adds into copy c % kFxCopies (8x fewer
+// red.adds per address, spread over more L2 slices) and a reader sums the
+// copies (integers: the order does not matter).
+constexpr int kFxCopies = 8;
+__host__ __device__ inline int64_t fx_copy_stride(int p) { return (2 * (int64_t)(p + 2) + 2 + 127) / 128 * 128; }
+__host__ __device__ inline int64_t fx_buf_words(int p) { return kFxCopies * fx_copy_stride(p); }
+__host__ __device__ inline int64_t fx_rank_words(int p) { return 3 * fx_buf_words(p); }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -261,55 +271,6 @@ __device__ __forceinline__ WarpTiles warp_tiles(const LogisticArgs& a) {
   return w;
 }
 
-// Producer side of a warp's ring (lane 0): position of the next issue,
-// advanced incrementally (no 64-bit division on the per-tile path).
-struct Producer {
-  unsigned char* ring;
-  uint64_t* bars;
-  const float* xsrc;     // X of the next tile to issue
-  const uint8_t* ysrc;   // y of the next tile
-  int64_t xstep, ystep;  // advance per issue (nwarps tiles)
-  int64_t tj, count;     // periodic tile index of the next issue
-  const float* xfirst;
-  const uint8_t* yfirst;
-  int s, nstage, stage_bytes;
-  uint32_t xb;
-  uint64_t pol, pol_keep;
-  int64_t keep;          // tiles tj < keep stay in L2 between passes
-
-  __device__ __forceinline__ void init(const LogisticArgs& a, const WarpTiles& wt, unsigned long long issued) {
-    const int warp = wk_warp();
-    nstage = a.nstage;
-    stage_bytes = a.stage_bytes;
-    ring = a.stages + (int64_t)warp * nstage * stage_bytes;
-    bars = a.mbar + warp * nstage;
-    s = (int)(umod(issued, nstage));
-    count = wt.count;
-    tj = (int64_t)(umod(issued, (uint32_t)count));
-    xb = 128u * (uint32_t)a.p;
-    xfirst = a.xt + wt.first * 32 * (int64_t)a.p;
-    yfirst = a.yt + wt.first * 32;
-    xstep = (int64_t)wt.nwarps * 32 * a.p;
-    ystep = (int64_t)wt.nwarps * 32;
-    xsrc = xfirst + tj * xstep;
-    ysrc = yfirst + tj * ystep;
-    pol = policy_evict_first();
-    pol_keep = policy_evict_last();
-    keep = count * a.keep_pct / 100;
-  }
-  __device__ __forceinline__ void issue() {
-    uint64_t* bar = bars + s;
-    unsigned char* dst = ring + (int64_t)s * stage_bytes;
-    const uint64_t pl = tj < keep ? pol_keep : pol;
-    mbar_expect_tx(bar, xb + 32u);
-    bulk_g2s(dst, xsrc, xb, bar, pl);
-    bulk_g2s(dst + xb, ysrc, 32u, bar, pl);
-    if (++s == nstage) s = 0;
-    if (++tj == count) { tj = 0; xsrc = xfirst; ysrc = yfirst; }
-    else { xsrc += xstep; ysrc += ystep; }
-  }
-};
-
 // Kernel prologue (worker warps): mbarriers and pipe counters.
 static __device__ void logistic_pipeline_init(const LogisticArgs& a) {
   const int rings = wk_nwarps();
@@ -340,6 +301,8 @@ static __device__ void logistic_pipeline_drain(const LogisticArgs& a) {
 
 // Lane's row of a tile in shared memory -> x[0..PMAX) (zeros past p), y.
 // PE > 0 fixes p at compile time (branch-free body for the benchmark shape).
+// `sb` points into the dynamic shared-memory symbol, so these are LDS (not
+// generic loads with 64-bit addresses).
 template <int PMAX, int PE>
 __device__ __forceinline__ void row_from_stage(const unsigned char* sb, int p_rt, int lane, float (&x)[PMAX], uint8_t& y) {
   const int p = PE > 0 ? PE : p_rt;
@@ -426,12 +389,23 @@ __device__ __forceinline__ float log1p_unit_f(float e) {
 template <int PMAX, bool FP64, int PE, int LL = 6>
 __device__ __noinline__ void logistic_cta_pass(const LogisticArgs& a, const double* __restrict__ theta_s, double* wred,
                                                   double* red_out) {
+  extern __shared__ __align__(16) unsigned char ts_dyn_smem[];
   const int lane = threadIdx.x & 31, warp = wk_warp(), nwarps = wk_nwarps();
   const int p = PE > 0 ? PE : a.p;
   constexpr int NA = PMAX + 2;
+  // features the loops touch: p itself when it is a compile-time constant
+  // (no FMAs on the zero padding), else the padded capacity
+  constexpr int KX = PE > 0 ? PE : PMAX;
   const WarpTiles wt = warp_tiles(a);
   const bool prof = a.prof != nullptr && blockIdx.x == 0 && wk_tid() == 0;
   long long pc0 = prof ? clock64() : 0, pc1;
+  // loop-invariant launch state in registers: the pipeline's asm statements
+  // clobber memory, which would otherwise re-read these fields of `a` (local
+  // memory) on every tile
+  const int nstage = a.nstage;
+  const int stage_bytes = a.stage_bytes;
+  const uint32_t ring_off = (uint32_t)(a.stages - ts_dyn_smem) + (uint32_t)(warp * nstage * stage_bytes);
+  uint64_t* const bars = a.mbar + warp * nstage;
 
   using acc_t = typename std::conditional<FP64, double, float>::type;
   acc_t acc[PMAX + 1];
@@ -477,32 +451,56 @@ __device__ __noinline__ void logistic_cta_pass(const LogisticArgs& a, const doub
     WarpPipe& pipe = a.pipe[warp];
     const unsigned long long c0 = pipe.consumed;
     unsigned long long issued = pipe.issued;
-    Producer prod;
-    if (lane == 0) {
-      prod.init(a, wt, issued);
-      while (issued < c0 + (unsigned long long)a.nstage) { prod.issue(); ++issued; }
-    }
+    // 32-bit tile bookkeeping (a warp owns < 2^31 tiles)
+    const int count = (int)wt.count;
+    const int tfirst = (int)wt.first, tstride = wt.nwarps;
+    // valid rows of tile t: 32 below the last (partial) tile
+    const int nfull = (int)(a.n_rows >> 5), rem = (int)(a.n_rows & 31);
+    // producer state, kept in registers by every lane (lane 0 issues)
+    const uint32_t xb = 128u * (uint32_t)p;
+    const float* const xfirst = a.xt + (int64_t)tfirst * 32 * p;
+    const uint8_t* const yfirst = a.yt + (int64_t)tfirst * 32;
+    const int64_t xstep = (int64_t)tstride * 32 * p, ystep = (int64_t)tstride * 32;
+    const int keep = (int)((int64_t)count * a.keep_pct / 100);
+    const uint64_t pol = policy_evict_first(), pol_keep = policy_evict_last();
+    int ps = (int)umod(issued, (uint32_t)nstage);
+    int pj = (int)umod(issued, (uint32_t)count);
+    const float* pxs = xfirst + (int64_t)pj * xstep;
+    const uint8_t* pys = yfirst + (int64_t)pj * ystep;
+    auto issue = [&]() {
+      if (lane == 0) {
+        uint64_t* bar = bars + ps;
+        unsigned char* dst = ts_dyn_smem + ring_off + (uint32_t)(ps * stage_bytes);
+        const uint64_t pl = pj < keep ? pol_keep : pol;
+        mbar_expect_tx(bar, xb + 32u);
+        bulk_g2s(dst, pxs, xb, bar, pl);
+        bulk_g2s(dst + xb, pys, 32u, bar, pl);
+      }
+      if (++ps == nstage) ps = 0;
+      if (++pj == count) { pj = 0; pxs = xfirst; pys = yfirst; }
+      else { pxs += xstep; pys += ystep; }
+    };
+    while (issued < c0 + (unsigned long long)nstage) { issue(); ++issued; }
     // ring position and periodic tile index, advanced incrementally
-    int s = (int)(umod(c0, a.nstage));
-    uint32_t parity = udiv(c0, a.nstage) & 1u;
-    int64_t tj = (int64_t)(umod(c0, (uint32_t)wt.count));
-    const unsigned char* ring = a.stages + (int64_t)warp * a.nstage * a.stage_bytes;
-    uint64_t* bars = a.mbar + warp * a.nstage;
+    int s = (int)(umod(c0, nstage));
+    uint32_t parity = udiv(c0, nstage) & 1u;
+    int tj = (int)(umod(c0, (uint32_t)count));
     if (prof) { pc1 = clock64(); a.prof[4] += pc1 - pc0; pc0 = pc1; }
-    for (int64_t j = 0; j < wt.count; ++j) {
+    for (int j = 0; j < count; ++j) {
       mbar_wait(bars + s, parity);
-      const unsigned char* sb = ring + (int64_t)s * a.stage_bytes;
+      const unsigned char* sb = ts_dyn_smem + ring_off + (uint32_t)(s * stage_bytes);
       float x[PMAX];
       uint8_t yb;
       row_from_stage<PMAX, PE>(sb, p, lane, x, yb);
       __syncwarp();
       // stage s is free again: keep the producer NSTAGE tiles ahead (wrapping
       // into the next pass; X is read-only for the whole kernel)
-      if (lane == 0) { prod.issue(); ++issued; }
-      const int64_t row = (wt.first + tj * wt.nwarps) * 32 + lane;
-      const bool valid = row < a.n_rows;
-      if (++s == a.nstage) { s = 0; parity ^= 1u; }
-      if (++tj == wt.count) tj = 0;
+      issue();
+      ++issued;
+      const int t = tfirst + tj * tstride;
+      const bool valid = lane < (t < nfull ? 32 : rem);
+      if (++s == nstage) { s = 0; parity ^= 1u; }
+      if (++tj == count) tj = 0;
       if constexpr (FP64) {
         // each element converted to double once (F2F is the scarce pipe here)
         // and reused for eta and for the gradient
@@ -512,14 +510,14 @@ __device__ __noinline__ void logistic_cta_pass(const LogisticArgs& a, const doub
         // elements and for every second one (47.4 vs 42.7 us per pass).
         double xd[PMAX];
 #pragma unroll
-        for (int k = 0; k < PMAX; ++k) xd[k] = (double)x[k];
+        for (int k = 0; k < KX; ++k) xd[k] = (double)x[k];
         double e0 = theta_s[p], e1 = 0.0, e2 = 0.0, e3 = 0.0;
 #pragma unroll
-        for (int k = 0; k < PMAX; k += 4) {
+        for (int k = 0; k < KX; k += 4) {
           e0 = __fma_rn(xd[k], (k < p) ? theta_s[k] : 0.0, e0);
-          e1 = __fma_rn(xd[k + 1], (k + 1 < p) ? theta_s[k + 1] : 0.0, e1);
-          e2 = __fma_rn(xd[k + 2], (k + 2 < p) ? theta_s[k + 2] : 0.0, e2);
-          e3 = __fma_rn(xd[k + 3], (k + 3 < p) ? theta_s[k + 3] : 0.0, e3);
+          if (k + 1 < KX) e1 = __fma_rn(xd[k + 1], (k + 1 < p) ? theta_s[k + 1] : 0.0, e1);
+          if (k + 2 < KX) e2 = __fma_rn(xd[k + 2], (k + 2 < p) ? theta_s[k + 2] : 0.0, e2);
+          if (k + 3 < KX) e3 = __fma_rn(xd[k + 3], (k + 3 < p) ? theta_s[k + 3] : 0.0, e3);
         }
         const double eta = (e0 + e1) + (e2 + e3);
         const double e = exp(-fabs(eta));
@@ -529,16 +527,16 @@ __device__ __noinline__ void logistic_cta_pass(const LogisticArgs& a, const doub
         const double resid = valid ? yv - sig : 0.0;
         accl += valid ? (yv * eta - l) : 0.0;
 #pragma unroll
-        for (int k = 0; k < PMAX; ++k) acc[k] = __fma_rn(resid, xd[k], acc[k]);
+        for (int k = 0; k < KX; ++k) acc[k] = __fma_rn(resid, xd[k], acc[k]);
         acc[PMAX] += resid;
       } else {
         float e0 = thb32, e1 = 0.f, e2 = 0.f, e3 = 0.f;
 #pragma unroll
-        for (int k = 0; k < PMAX; k += 4) {
+        for (int k = 0; k < KX; k += 4) {
           e0 = __fmaf_rn(x[k], th32[k], e0);
-          e1 = __fmaf_rn(x[k + 1], th32[k + 1], e1);
-          e2 = __fmaf_rn(x[k + 2], th32[k + 2], e2);
-          e3 = __fmaf_rn(x[k + 3], th32[k + 3], e3);
+          if (k + 1 < KX) e1 = __fmaf_rn(x[k + 1], th32[k + 1], e1);
+          if (k + 2 < KX) e2 = __fmaf_rn(x[k + 2], th32[k + 2], e2);
+          if (k + 3 < KX) e3 = __fmaf_rn(x[k + 3], th32[k + 3], e3);
         }
         float eta = (e0 + e1) + (e2 + e3);
         if constexpr (LL == 5) {
@@ -573,13 +571,13 @@ __device__ __noinline__ void logistic_cta_pass(const LogisticArgs& a, const doub
         const float resid = valid ? yv - sig : 0.f;
         accl += valid ? ((yb ? (double)eta : 0.0) - l) : 0.0;
 #pragma unroll
-        for (int k = 0; k < PMAX; ++k) acc[k] = __fmaf_rn(resid, x[k], acc[k]);
+        for (int k = 0; k < KX; ++k) acc[k] = __fmaf_rn(resid, x[k], acc[k]);
         acc[PMAX] += resid;
       }
     }
     __syncwarp();
     if (lane == 0) {
-      pipe.consumed = c0 + (unsigned long long)wt.count;
+      pipe.consumed = c0 + (unsigned long long)count;
       pipe.issued = issued;
     }
     __syncwarp();
@@ -1002,8 +1000,17 @@ static __device__ void logistic_eval_grid(const LogisticArgs& a, const VecStore&
   // epoch % 3 (see fx_split): integer addition is associative, so the result
   // is independent of the order in which CTAs arrive -- deterministic.
   unsigned long long* accb = reinterpret_cast<unsigned long long*>(a.pbuf);
-  const int64_t bstride = 2 * (int64_t)P2 + 2;
-  unsigned long long* cur = accb + (int64_t)(epoch % 3ULL) * bstride;
+  const int64_t bstride = 2 * (int64_t)P2 + 2;  // words of one set of totals (mailbox slots)
+  const int64_t cstride = fx_copy_stride(p), bufw = fx_buf_words(p);
+  unsigned long long* const curb = accb + (int64_t)(epoch % 3ULL) * bufw;  // this pass's buffer
+  unsigned long long* cur = curb + (int64_t)(a.cta % kFxCopies) * cstride;  // this CTA's copy
+  // total of word w over the copies (after the barrier)
+  auto total = [&](int w) {
+    unsigned long long v = 0;
+#pragma unroll
+    for (int c = 0; c < kFxCopies; ++c) v += __ldcg(curb + c * cstride + w);
+    return v;
+  };
   if (a.wide) {  // the wide pass leaves exact fixed-point CTA totals in wred
     const unsigned long long* tot = reinterpret_cast<const unsigned long long*>(wred);
     for (int d = wk_tid(); d < P2; d += wk_threads()) {
@@ -1043,8 +1050,8 @@ static __device__ void logistic_eval_grid(const LogisticArgs& a, const VecStore&
   // buffer (epoch+2)%3 was last read before this barrier by every CTA and is
   // next accumulated after the following barrier: CTA 0 clears it now.
   if (a.cta == 0) {
-    unsigned long long* nxt = accb + (int64_t)((epoch + 2) % 3ULL) * bstride;
-    for (int i = wk_tid(); i < bstride; i += wk_threads()) nxt[i] = 0ULL;
+    unsigned long long* nxt = accb + (int64_t)((epoch + 2) % 3ULL) * bufw;
+    for (int i = wk_tid(); i < bufw; i += wk_threads()) nxt[i] = 0ULL;
   }
   epoch += 1;
   if (prof) { c1 = clock64(); a.prof[2] += c1 - c0; c0 = c1; }
@@ -1055,7 +1062,7 @@ static __device__ void logistic_eval_grid(const LogisticArgs& a, const VecStore&
   }
 
   if (a.dump && epoch == 1 && blockIdx.x == 0)  // test hook: this GPU's totals of the first pass
-    for (int i = wk_tid(); i < 2 * P2 + 1; i += wk_threads()) a.dump[i] = __ldcg(cur + i);
+    for (int i = wk_tid(); i < 2 * P2 + 1; i += wk_threads()) a.dump[i] = total(i);
 
   double* g = S.v(gid);
   if (a.world > 0) {
@@ -1073,11 +1080,11 @@ static __device__ void logistic_eval_grid(const LogisticArgs& a, const VecStore&
         const int r = i / nwords, w = i - r * nwords;
         unsigned long long v;
         if (w < 2 * P2) {  // canonical pair
-          unsigned long long hi = __ldcg(cur + (w & ~1)), lo = __ldcg(cur + (w | 1));
+          unsigned long long hi = total(w & ~1), lo = total(w | 1);
           fx_canon(hi, lo);
           v = (w & 1) ? lo : hi;
         } else {
-          v = __ldcg(cur + w);
+          v = total(w);
         }
         a.mail[r][kMailFlags + (slot * W + a.rank) * bstride + w] = v;
       }
@@ -1109,9 +1116,9 @@ static __device__ void logistic_eval_grid(const LogisticArgs& a, const VecStore&
       else red_s[0] = s;
     }
   } else {
-    const bool bad = __ldcg(cur + 2 * P2) != 0ULL;
+    const bool bad = total(2 * P2) != 0ULL;
     for (int d = wk_tid(); d < P2; d += wk_threads()) {
-      unsigned long long hi = __ldcg(cur + 2 * d), lo = __ldcg(cur + 2 * d + 1);
+      unsigned long long hi = total(2 * d), lo = total(2 * d + 1);
       fx_canon(hi, lo);  // both words exact in double
       const double s = bad ? __longlong_as_double(0x7ff8000000000000LL) : fx_join((long long)hi, lo);
       if (d <= p) g[d] = theta[d] - s;

@@ -42,7 +42,7 @@ __global__ void k_retile(const float* __restrict__ x, const uint8_t* __restrict_
     const int64_t dst = t * 32 * (int64_t)p + 128 * (int64_t)g + (int64_t)lane * w + (j & 3);
     const float v = row < n ? x[row * p + j] : 0.f;
     const unsigned a = __float_as_uint(v) & 0x7fffffffu;
-    sub |= (a != 0u && a < 0x00800000u);
+    sub |= (a != 0u && a < 0x00800000u) || a >= 0x7f800000u;  // subnormal or non-finite: no integer fp64 conversion
     xt[dst] = v;
     if (j == 0) yt[row] = row < n ? y[row] : 0;
   }
@@ -68,7 +68,7 @@ __global__ void k_retile_wide(const T* __restrict__ x, const uint8_t* __restrict
     const T v = row < n ? x[row * p + j] : (T)0;
     if (sizeof(T) == 4) {
       const unsigned a = __float_as_uint((float)v) & 0x7fffffffu;
-      sub |= (a != 0u && a < 0x00800000u);
+      sub |= (a != 0u && a < 0x00800000u) || a >= 0x7f800000u;
     }
     unsigned char* tile = xt + t * tb;
     reinterpret_cast<T*>(tile)[r * p + j] = v;

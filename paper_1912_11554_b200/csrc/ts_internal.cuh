@@ -136,6 +136,13 @@ struct LogisticW {
       }
       __syncwarp();
     }
+    if (a.thd != nullptr) {  // FP64 narrow pass: theta as zero-padded doubles
+      const double* th = S.v(q);
+      double* td = const_cast<double*>(a.thd);
+      for (int j = (int)(threadIdx.x & 31); j <= a.pmax; j += 32)
+        td[j] = (j < a.p) ? th[j] : (j == a.pmax ? th[a.p] : 0.0);
+      __syncwarp();
+    }
     cta_arrive(2);  // publishes q and the command to the worker warps
   }
   // ... and collect it (barrier 3: gradient written to vector g, U in red_s)
@@ -148,11 +155,14 @@ struct LogisticW {
     post(q, g);
     return wait();
   }
-  __device__ void serve(const VecStore& S) {  // worker warps
+  // worker warps; `sa`: this CTA's copy of the launch state in shared memory
+  // (a local-memory copy is re-read on every pass and misses in the L1 that
+  // the TMA ring leaves over: ~0.8 us per pass of serialized misses)
+  __device__ void serve(const VecStore& S, const LogisticArgs& sa) {
     for (;;) {
       cta_bar(2);
       if (cmd[0] == 0) break;
-      logistic_eval_grid(a, S, cmd[1], cmd[2], wred, red_s, epoch);
+      logistic_eval_grid(sa, S, cmd[1], cmd[2], wred, red_s, epoch);
       cta_arrive(3);
     }
   }
@@ -361,6 +371,7 @@ __global__ void __launch_bounds__(256, 1) k_block_op(MW mw, int D, int nslots, i
     const int rings = (int)(blockDim.x >> 5) - 1;
     // float copy of theta for the FP32 narrow pass (written by the driver in post)
     mw.a.th32 = (!mw.a.fp64 && !mw.a.wide) ? reinterpret_cast<const float*>(mw.red_s + ((mw.a.p + 3) & ~1)) : nullptr;
+    mw.a.thd = (mw.a.fp64 && !mw.a.wide) ? mw.red_s + ((mw.a.p + 3) & ~1) : nullptr;
     mw.S = S;
     uintptr_t pb = reinterpret_cast<uintptr_t>(mw.red_s + mw.a.p + 2 + (kWideMax + 8) / 2);
     pb = (pb + 127) & ~(uintptr_t)127;
@@ -381,9 +392,13 @@ __global__ void __launch_bounds__(256, 1) k_block_op(MW mw, int D, int nslots, i
       do_op(E, A, chain, writer);
       E.M.release_workers();
     } else {
-      logistic_pipeline_init(mw.a);
-      mw.serve(S);
-      logistic_pipeline_drain(mw.a);
+      __shared__ __align__(16) unsigned char sh_args[sizeof(LogisticArgs)];
+      LogisticArgs& sa = *reinterpret_cast<LogisticArgs*>(sh_args);
+      if (wk_tid() == 0) sa = mw.a;
+      wk_sync();
+      logistic_pipeline_init(sa);
+      mw.serve(S, sa);
+      logistic_pipeline_drain(sa);
       if (mw.a.world > 0 && blockIdx.x == 0 && wk_tid() == 0) *mw.a.mail_epoch = mw.a.xbase + mw.epoch;
     }
   }

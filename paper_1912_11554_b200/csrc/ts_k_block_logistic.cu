@@ -29,8 +29,10 @@ int launch_block_logistic(const ts_model* m, int nslots, OpArgs& A, cudaStream_t
   mw.a.llmode = 6;
   if (const char* e = getenv("TS_LLMODE")) mw.a.llmode = atoi(e);  // A/B of the fp32 log-likelihood precision
   // fp64 wide pass: half of the fp32->fp64 conversions on the integer pipe
-  // (XU-bound otherwise; 2.77 -> 2.61 ms per 8Mx255 pass); TS_ICVT=0/2 for A/B
-  mw.a.icvt = 1;
+  // (XU-bound otherwise; 2.77 -> 2.61 ms per 8Mx255 pass); the narrow pass
+  // measured best with XU conversions (covtype: 32.8 us vs 37.9 with every
+  // 4th / 36.0 with no element on the XU); TS_ICVT=0/1/2 for A/B
+  mw.a.icvt = m->wide ? 1 : 0;
   // L2 residency: the first 70% of each warp's tiles are fetched with
   // L2::evict_last and the rest evict_first, so ~88 MB of X stays in L2
   // across passes (covtype pass 23.8 -> 21.8 us; 90% thrashes: 24.4 us).
@@ -63,7 +65,7 @@ int launch_block_logistic(const ts_model* m, int nslots, OpArgs& A, cudaStream_t
   const int rings = nwarps - 1;  // worker warps
   int nstage = 2;
   if (const char* e = getenv("TS_NSTAGE")) nstage = atoi(e) < 1 ? 1 : (atoi(e) > 4 ? 4 : atoi(e));  // profiling
-  auto need = [&](int ns) { return base + (size_t)rings * ns * (stage_bytes + 8) + rings * 16; };
+  auto need = [&](int ns) { return base + (size_t)rings * ns * (stage_bytes + 8) + rings * sizeof(WarpPipe); };
   while (nstage > 1 && need(nstage) > (size_t)smem_max) --nstage;
   if (need(nstage) > (size_t)smem_max)
     return set_err(TS_EUNSUPPORTED, "logistic model: shared memory too small for D / max_tree_depth");

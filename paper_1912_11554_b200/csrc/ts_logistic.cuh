@@ -42,7 +42,14 @@ namespace ts {
 struct WarpPipe {
   unsigned long long issued;    // tiles issued into the ring (periodic sequence index)
   unsigned long long consumed;  // tiles consumed
+  // narrow pass (p <= 64): ring positions carried across passes (no
+  // divisions on the per-pass entry path) and the warp's static tile range
+  int cs, cpar, ctj;            // consumer: ring slot, mbarrier parity, periodic tile index
+  int ps, pj;                   // producer: ring slot, periodic tile index
+  int first, count, keep;       // first tile, tiles per pass, tiles fetched L2::evict_last
+  int pad_[4];
 };
+static_assert(sizeof(WarpPipe) == 64, "WarpPipe is budgeted at 64 bytes per ring (launch_block_logistic)");
 
 struct LogisticArgs {
   const float* xt;          // tiled X, ntiles * 32 * p floats
@@ -86,6 +93,7 @@ struct LogisticArgs {
   int fault;                       // fault injection (tests): 1 = CTA 1 never arrives at the grid barrier
   int llmode;                      // FP32 narrow pass: log-likelihood term precision (logistic_cta_pass LL)
   int xd;                          // X stored as fp64 (wide layout, logistic_cta_pass_wide XD)
+  const double* thd;  // FP64 narrow pass: theta as doubles [pmax + 1], zero-padded, 16-B aligned (smem, written by the driver)
 };
 
 // Mailbox of one rank: kMailFlags words of flags (flag[src] = 1 + the last
@@ -258,8 +266,7 @@ struct WarpTiles {
   int nwarps;
 };
 
-__device__ __forceinline__ WarpTiles warp_tiles(const LogisticArgs& a) {
-  const int warp = wk_warp(), nwarps = wk_nwarps();
+__device__ __forceinline__ WarpTiles warp_tiles(const LogisticArgs& a, int warp, int nwarps) {
   const int64_t G = a.ncta, span = a.u_hi - a.u_lo;
   const int64_t t_begin = a.u_lo + (span * (int64_t)a.cta) / G;
   const int64_t t_end = a.u_lo + (span * ((int64_t)a.cta + 1)) / G;
@@ -270,6 +277,7 @@ __device__ __forceinline__ WarpTiles warp_tiles(const LogisticArgs& a) {
   w.nwarps = nwarps;
   return w;
 }
+__device__ __forceinline__ WarpTiles warp_tiles(const LogisticArgs& a) { return warp_tiles(a, wk_warp(), wk_nwarps()); }
 
 // Kernel prologue (worker warps): mbarriers and pipe counters.
 static __device__ void logistic_pipeline_init(const LogisticArgs& a) {
@@ -280,7 +288,19 @@ static __device__ void logistic_pipeline_init(const LogisticArgs& a) {
     for (int i = wk_tid(); i < nw; i += wk_threads()) z[i] = 0u;
   }
   for (int i = wk_tid(); i < rings * a.nstage; i += wk_threads()) mbar_init(a.mbar + i, 1);
-  for (int i = wk_tid(); i < rings; i += wk_threads()) { a.pipe[i].issued = 0; a.pipe[i].consumed = 0; }
+  for (int i = wk_tid(); i < rings; i += wk_threads()) {
+    WarpPipe& q = a.pipe[i];
+    q.issued = 0; q.consumed = 0;
+    q.cs = 0; q.cpar = 0; q.ctj = 0; q.ps = 0; q.pj = 0;
+    if (!a.wide) {
+      const WarpTiles wt = warp_tiles(a, i, rings);
+      q.first = (int)wt.first;
+      q.count = (int)wt.count;
+      q.keep = (int)(wt.count * a.keep_pct / 100);
+    } else {
+      q.first = 0; q.count = 0; q.keep = 0;
+    }
+  }
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   wk_sync();
 }
@@ -386,7 +406,33 @@ __device__ __forceinline__ float log1p_unit_f(float e) {
   return 2.0f * s * q;
 }
 
-template <int PMAX, bool FP64, int PE, int LL = 6>
+// fp32 -> fp64 on the integer pipe for normal numbers and zeros (X without
+// fp32 subnormals, LogisticArgs::exact_cvt == 0): sign | (exponent + 896) |
+// mantissa, in 5 integer operations, no XU conversion
+__device__ __forceinline__ double f2d_int(float f) {
+  const uint32_t u = __float_as_uint(f);
+  const uint32_t hi = ((uint32_t)((int32_t)u >> 3) & 0x8fffffffu) + ((u << 1) ? 0x38000000u : 0u);
+  return __hiloint2double((int)hi, (int)(u << 29));
+}
+
+// X element -> double in the FP64 narrow pass.  ICVT 0: XU conversions
+// (F2F.F64.F32, ~12 cycles per warp instruction per SM: the scarce pipe);
+// 1: every 4th element of eta on the XU, the rest and the gradient's on the
+// integer ALU (f2d_int); 2: all on the ALU.  1/2 need X without fp32
+// subnormals and non-finite values (LogisticArgs::exact_cvt == 0).
+template <int ICVT>
+__device__ __forceinline__ double cvt_x(float v, int k) {
+  if constexpr (ICVT == 0) return (double)v;
+  else if constexpr (ICVT == 2) return f2d_int(v);
+  else return (k & 3) == 0 ? (double)v : f2d_int(v);
+}
+__device__ __forceinline__ double2 lds_d2(const double* p) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(smem_u32(p)));
+  return v;
+}
+
+template <int PMAX, bool FP64, int PE, int LL = 6, int ICVT = 0>
 __device__ __noinline__ void logistic_cta_pass(const LogisticArgs& a, const double* __restrict__ theta_s, double* wred,
                                                   double* red_out) {
   extern __shared__ __align__(16) unsigned char ts_dyn_smem[];
@@ -396,7 +442,8 @@ __device__ __noinline__ void logistic_cta_pass(const LogisticArgs& a, const doub
   // features the loops touch: p itself when it is a compile-time constant
   // (no FMAs on the zero padding), else the padded capacity
   constexpr int KX = PE > 0 ? PE : PMAX;
-  const WarpTiles wt = warp_tiles(a);
+  WarpPipe& pipe = a.pipe[warp];
+  const int count = pipe.count;  // tiles of this warp per pass (static, logistic_pipeline_init)
   const bool prof = a.prof != nullptr && blockIdx.x == 0 && wk_tid() == 0;
   long long pc0 = prof ? clock64() : 0, pc1;
   // loop-invariant launch state in registers: the pipeline's asm statements
@@ -426,7 +473,8 @@ __device__ __noinline__ void logistic_cta_pass(const LogisticArgs& a, const doub
   if constexpr (!FP64) {
     // theta as floats, broadcast with LDS.128: prepared by the driver warp
     // before the post (a.th32), else rounded here once per CTA
-    const float* t32 = a.th32;
+    // (addressed through the dynamic-smem symbol: LDS, not generic loads)
+    const float* t32 = a.th32 ? reinterpret_cast<const float*>(ts_dyn_smem + (reinterpret_cast<const unsigned char*>(a.th32) - ts_dyn_smem)) : nullptr;
     if (t32 == nullptr || a.pmax != PMAX) {
       float* w32 = reinterpret_cast<float*>(wred);  // wred is free until the end
       for (int j = wk_tid(); j <= PMAX; j += wk_threads()) {
@@ -444,16 +492,17 @@ __device__ __noinline__ void logistic_cta_pass(const LogisticArgs& a, const doub
     }
     thb32 = t32[PMAX];
     if constexpr (LL == 5) thlo = t32 + 64;
-    if (t32 != a.th32 || a.pmax != PMAX) wk_sync();
+    if (a.th32 == nullptr || a.pmax != PMAX) wk_sync();
   }
 
-  if (wt.count > 0) {
-    WarpPipe& pipe = a.pipe[warp];
+  // FP64: theta as doubles through the dynamic-smem symbol (LDS)
+  const double* thd = nullptr;
+  if constexpr (FP64) thd = reinterpret_cast<const double*>(ts_dyn_smem + (reinterpret_cast<const unsigned char*>(a.thd) - ts_dyn_smem));
+  if (count > 0) {
     const unsigned long long c0 = pipe.consumed;
     unsigned long long issued = pipe.issued;
     // 32-bit tile bookkeeping (a warp owns < 2^31 tiles)
-    const int count = (int)wt.count;
-    const int tfirst = (int)wt.first, tstride = wt.nwarps;
+    const int tfirst = pipe.first, tstride = nwarps;
     // valid rows of tile t: 32 below the last (partial) tile
     const int nfull = (int)(a.n_rows >> 5), rem = (int)(a.n_rows & 31);
     // producer state, kept in registers by every lane (lane 0 issues)
@@ -461,10 +510,9 @@ __device__ __noinline__ void logistic_cta_pass(const LogisticArgs& a, const doub
     const float* const xfirst = a.xt + (int64_t)tfirst * 32 * p;
     const uint8_t* const yfirst = a.yt + (int64_t)tfirst * 32;
     const int64_t xstep = (int64_t)tstride * 32 * p, ystep = (int64_t)tstride * 32;
-    const int keep = (int)((int64_t)count * a.keep_pct / 100);
+    const int keep = pipe.keep;
     const uint64_t pol = policy_evict_first(), pol_keep = policy_evict_last();
-    int ps = (int)umod(issued, (uint32_t)nstage);
-    int pj = (int)umod(issued, (uint32_t)count);
+    int ps = pipe.ps, pj = pipe.pj;
     const float* pxs = xfirst + (int64_t)pj * xstep;
     const uint8_t* pys = yfirst + (int64_t)pj * ystep;
     auto issue = [&]() {
@@ -482,9 +530,8 @@ __device__ __noinline__ void logistic_cta_pass(const LogisticArgs& a, const doub
     };
     while (issued < c0 + (unsigned long long)nstage) { issue(); ++issued; }
     // ring position and periodic tile index, advanced incrementally
-    int s = (int)(umod(c0, nstage));
-    uint32_t parity = udiv(c0, nstage) & 1u;
-    int tj = (int)(umod(c0, (uint32_t)count));
+    int s = pipe.cs, tj = pipe.ctj;
+    uint32_t parity = (uint32_t)pipe.cpar;
     if (prof) { pc1 = clock64(); a.prof[4] += pc1 - pc0; pc0 = pc1; }
     for (int j = 0; j < count; ++j) {
       mbar_wait(bars + s, parity);
@@ -502,22 +549,19 @@ __device__ __noinline__ void logistic_cta_pass(const LogisticArgs& a, const doub
       if (++s == nstage) { s = 0; parity ^= 1u; }
       if (++tj == count) tj = 0;
       if constexpr (FP64) {
-        // each element converted to double once (F2F is the scarce pipe here)
-        // and reused for eta and for the gradient
-        // The fp32 -> fp64 conversions (F2F, ~4/clk/SM on the XU pipe) bound
-        // this variant: ncu shows XU ~95% busy, FP64 ~17%.  An integer-ALU
-        // conversion (6 instructions per element) measured slower, for all
-        // elements and for every second one (47.4 vs 42.7 us per pass).
-        double xd[PMAX];
-#pragma unroll
-        for (int k = 0; k < KX; ++k) xd[k] = (double)x[k];
-        double e0 = theta_s[p], e1 = 0.0, e2 = 0.0, e3 = 0.0;
+        // x stays in float registers and is converted where it is used (cvt_x:
+        // mostly on the integer ALU, the XU's F2F being the scarce pipe);
+        // keeping 54 converted doubles live for the gradient spilled.  theta:
+        // broadcast LDS.128 from the driver's zero-padded copy (thd).  The
+        // arithmetic (4 FMA chains, then the gradient FMAs) is unchanged.
+        double e0 = thd[PMAX], e1 = 0.0, e2 = 0.0, e3 = 0.0;
 #pragma unroll
         for (int k = 0; k < KX; k += 4) {
-          e0 = __fma_rn(xd[k], (k < p) ? theta_s[k] : 0.0, e0);
-          if (k + 1 < KX) e1 = __fma_rn(xd[k + 1], (k + 1 < p) ? theta_s[k + 1] : 0.0, e1);
-          if (k + 2 < KX) e2 = __fma_rn(xd[k + 2], (k + 2 < p) ? theta_s[k + 2] : 0.0, e2);
-          if (k + 3 < KX) e3 = __fma_rn(xd[k + 3], (k + 3 < p) ? theta_s[k + 3] : 0.0, e3);
+          const double2 ta = lds_d2(thd + k), tb = lds_d2(thd + k + 2);
+          e0 = __fma_rn(cvt_x<ICVT>(x[k], k), ta.x, e0);
+          if (k + 1 < KX) e1 = __fma_rn(cvt_x<ICVT>(x[k + 1], k + 1), ta.y, e1);
+          if (k + 2 < KX) e2 = __fma_rn(cvt_x<ICVT>(x[k + 2], k + 2), tb.x, e2);
+          if (k + 3 < KX) e3 = __fma_rn(cvt_x<ICVT>(x[k + 3], k + 3), tb.y, e3);
         }
         const double eta = (e0 + e1) + (e2 + e3);
         const double e = exp(-fabs(eta));
@@ -527,7 +571,7 @@ __device__ __noinline__ void logistic_cta_pass(const LogisticArgs& a, const doub
         const double resid = valid ? yv - sig : 0.0;
         accl += valid ? (yv * eta - l) : 0.0;
 #pragma unroll
-        for (int k = 0; k < KX; ++k) acc[k] = __fma_rn(resid, xd[k], acc[k]);
+        for (int k = 0; k < KX; ++k) acc[k] = __fma_rn(resid, cvt_x<ICVT == 0 ? 0 : 2>(x[k], k), acc[k]);
         acc[PMAX] += resid;
       } else {
         float e0 = thb32, e1 = 0.f, e2 = 0.f, e3 = 0.f;
@@ -579,6 +623,8 @@ __device__ __noinline__ void logistic_cta_pass(const LogisticArgs& a, const doub
     if (lane == 0) {
       pipe.consumed = c0 + (unsigned long long)count;
       pipe.issued = issued;
+      pipe.cs = s; pipe.cpar = (int)parity; pipe.ctj = tj;
+      pipe.ps = ps; pipe.pj = pj;
     }
     __syncwarp();
   }
@@ -722,15 +768,6 @@ struct WideProducer {
     }
   }
 };
-
-// fp32 -> fp64 on the integer pipe for normal numbers and zeros (X without
-// fp32 subnormals, LogisticArgs::exact_cvt == 0): sign | (exponent + 896) |
-// mantissa, in 5 integer operations, no XU conversion
-__device__ __forceinline__ double f2d_int(float f) {
-  const uint32_t u = __float_as_uint(f);
-  const uint32_t hi = ((uint32_t)((int32_t)u >> 3) & 0x8fffffffu) + ((u << 1) ? 0x38000000u : 0u);
-  return __hiloint2double((int)hi, (int)(u << 29));
-}
 
 // KL = features per lane (p <= 32 KL); ICVT: 1 odd m / 2 all on the ALU;
 // XD: X stored as fp64 (the "fp64x" policy: data that are not fp32-exact)
@@ -955,7 +992,9 @@ static __device__ __forceinline__ void logistic_cta_dispatch(const LogisticArgs&
     return;
   }
   if (a.p == 54) {  // covtype's feature count: compile-time row layout
-    if (a.fp64) logistic_cta_pass<56, true, 54>(a, theta, wred, red_s);
+    if (a.fp64 && !a.exact_cvt && a.icvt == 1) logistic_cta_pass<56, true, 54, 6, 1>(a, theta, wred, red_s);
+    else if (a.fp64 && !a.exact_cvt && a.icvt == 2) logistic_cta_pass<56, true, 54, 6, 2>(a, theta, wred, red_s);
+    else if (a.fp64) logistic_cta_pass<56, true, 54>(a, theta, wred, red_s);
     else if (a.llmode == 0) logistic_cta_pass<56, false, 54, 0>(a, theta, wred, red_s);
     else if (a.llmode == 2) logistic_cta_pass<56, false, 54, 2>(a, theta, wred, red_s);
     else if (a.llmode == 5) logistic_cta_pass<56, false, 54, 5>(a, theta, wred, red_s);
@@ -964,13 +1003,25 @@ static __device__ __forceinline__ void logistic_cta_dispatch(const LogisticArgs&
   }
   switch (a.pmax * 2 + (a.fp64 ? 1 : 0)) {
     case 16: logistic_cta_pass<8, false, 0>(a, theta, wred, red_s); break;
-    case 17: logistic_cta_pass<8, true, 0>(a, theta, wred, red_s); break;
+    case 17:
+      if (!a.exact_cvt && a.icvt) logistic_cta_pass<8, true, 0, 6, 2>(a, theta, wred, red_s);
+      else logistic_cta_pass<8, true, 0>(a, theta, wred, red_s);
+      break;
     case 64: logistic_cta_pass<32, false, 0>(a, theta, wred, red_s); break;
-    case 65: logistic_cta_pass<32, true, 0>(a, theta, wred, red_s); break;
+    case 65:
+      if (!a.exact_cvt && a.icvt) logistic_cta_pass<32, true, 0, 6, 1>(a, theta, wred, red_s);
+      else logistic_cta_pass<32, true, 0>(a, theta, wred, red_s);
+      break;
     case 112: logistic_cta_pass<56, false, 0>(a, theta, wred, red_s); break;
-    case 113: logistic_cta_pass<56, true, 0>(a, theta, wred, red_s); break;
+    case 113:
+      if (!a.exact_cvt && a.icvt) logistic_cta_pass<56, true, 0, 6, 1>(a, theta, wred, red_s);
+      else logistic_cta_pass<56, true, 0>(a, theta, wred, red_s);
+      break;
     case 128: logistic_cta_pass<64, false, 0>(a, theta, wred, red_s); break;
-    case 129: logistic_cta_pass<64, true, 0>(a, theta, wred, red_s); break;
+    case 129:
+      if (!a.exact_cvt && a.icvt) logistic_cta_pass<64, true, 0, 6, 1>(a, theta, wred, red_s);
+      else logistic_cta_pass<64, true, 0>(a, theta, wred, red_s);
+      break;
     default: break;
   }
 }
@@ -1040,11 +1091,12 @@ static __device__ void logistic_eval_grid(const LogisticArgs& a, const VecStore&
     if (G > 1) {
       const unsigned long long target = (epoch + 1) * (unsigned long long)G;
       SpinGuard sg(a.err, a.spin_ns);
+      // relaxed polling, then one acquire load (instead of a full fence)
       while (ld_relaxed_u64(a.bar) < target) {
         if (sg.expired()) break;
       }
+      (void)ld_acquire_u64(a.bar);
     }
-    asm volatile("fence.acq_rel.gpu;" ::: "memory");
   }
   wk_sync();
   // buffer (epoch+2)%3 was last read before this barrier by every CTA and is

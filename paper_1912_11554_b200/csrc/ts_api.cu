@@ -547,6 +547,12 @@ extern "C" int ts_run_chains(const ts_model* m, const ts_run_cfg* rc, const uint
       const double nt = h[14] ? (double)h[14] : 1.0, nx = h[15] ? (double)h[15] : 1.0;
       fprintf(stderr, "TS_PROF transitions=%llu trees=%llu cycles: prologue/transition %.0f (momentum %.0f)  between-trees/tree %.0f\n",
               h[15], h[14], h[12] / nx, h[16] / nx, h[13] / nt);
+      if (h[22] || h[19]) {
+        const double nl = h[22] ? (double)h[22] : 1.0, nw = h[19] ? (double)h[19] : 1.0;
+        fprintf(stderr, "TS_PROF trajectories: driver %llu leaves, wait %.0f + bookkeeping %.0f cycles/leaf; workers %llu leaves, "
+                "gate wait %.0f + leaf work outside the pass %.0f cycles/leaf\n", h[22], h[20] / nl, h[21] / nl, h[19],
+                h[17] / nw, h[18] / nw);
+      }
       if (m->kind == TS_LOGISTIC && m->many && h[24 + 8]) {
         const double nt = h[24 + 7] ? (double)h[24 + 7] : 1.0, nc = (double)h[24 + 8];
         fprintf(stderr, "TS_PROF many-chain: %llu chain tiles, %.1f row tiles each; cycles per row tile: X wait %.0f, "

@@ -805,6 +805,43 @@ struct Engine {
     } else {
       const unsigned long long nleaves = 1ULL << depth;
       if constexpr (Model::kAsync) {
+       if (M.traj_ok()) {
+        // The workers run the leapfrog chain (LogisticW::serve_traj): leaf n
+        // arrives in a ring slot while leaf n+1 streams; this warp only does
+        // the bookkeeping and gates the chain (at most one wasted pass).
+        M.traj_start(V_CQ, V_CR, V_CG, eps, (int)nleaves);
+        double* cq = v(V_CQ);
+        double* cr = v(V_CR);
+        double* cg = v(V_CG);
+        // TS_PROF (CTA 0): [20] driver waiting for leaves, [21] bookkeeping per leaf, [22] leaves
+        const bool tpf = prof != nullptr && T.leader();
+        for (unsigned long long n = 0; n < nleaves; ++n) {
+          const long long w0 = tpf ? clock64() : 0;
+          const double* sl = M.traj_wait((int)n);
+          const long long w1 = tpf ? clock64() : 0;
+          if (tpf) { prof[20] += w1 - w0; prof[22] += 1; }
+          for (int d = T.rank(); d < D; d += T.size()) {
+            const double a0 = sl[d], a1 = sl[D + d], a2 = sl[2 * D + d];
+            cq[d] = a0; cr[d] = a1; cg[d] = a2;
+          }
+          const double u = sl[3 * D];
+          cur_U = isfinite(u) ? u : kInf();
+          n_evals += 1;
+          T.sync();
+          add_cum();
+          double h, delta;
+          leaf_energy(h_ref, h, delta);
+          stop = leaf_book(n, h, delta, draws, forward);
+          if (stop != kStopNone) {
+            const int w = M.traj_stop((int)n);
+            n_evals += w;
+            n_wasted += w;
+            break;
+          }
+          M.traj_approve((int)n);
+          if (tpf) prof[21] += clock64() - w1;
+        }
+       } else {
         // Speculative pipelining (grid mode): as soon as leaf n's gradient is
         // back, drift to leaf n+1 and post its data pass to the worker warps,
         // then do leaf n's bookkeeping while they stream.  If the bookkeeping
@@ -866,6 +903,7 @@ struct Engine {
             break;
           }
         }
+       }
       } else {
         for (unsigned long long n = 0; n < nleaves; ++n) {
           leapfrog(eps);

@@ -111,38 +111,95 @@ struct SmallW {
 // Logistic model on a persistent grid.  In each CTA the driver warp runs the
 // chain (WarpTeam) and the other warps serve data passes: eval() posts a
 // command word in shared memory and joins the pass with them.
+//
+// Trajectories (narrow p): within one doubling the leapfrog steps do not
+// depend on the tree decisions, only on when the tree stops, so the worker
+// warps run the leapfrog chain themselves -- drift, pass, kick -- and put each
+// leaf (q, r, g, U) into a ring of kTrajRing shared-memory slots; the driver
+// consumes leaf n (NodeStore bookkeeping, U-turn checks) while the workers
+// stream leaf n+1.  Gate: the workers start leaf m >= 2 only after the driver
+// approved leaf m-2 (traj_approve), so every CTA runs exactly the same passes
+// (the decisions are replicated) and at most one pass is wasted when a tree
+// stops (the speculative leaf n+1, as with post/wait).  The arithmetic is
+// Engine::advance_drift's, element by element, so the leaves are identical.
+constexpr int kTrajRing = 4;
+// Handshake (shared memory).  Leaves and approvals are numbered globally
+// over the launch; leaf L completes phase L>>1 of done[L&1], approval A
+// (leaf A's verdict: 1 continue, 0 stop) phase A>>1 of appr[A&1].  Neither
+// side can run two phases ahead on one barrier (leaf m+2 needs leaf m's
+// approval, which needs leaf m), so parity waits are exact; the waits are
+// hardware-suspended (mbarrier.try_wait), not polling loops that would take
+// issue slots from the streaming warps.
+struct TrajCtl {
+  uint64_t done[2];
+  uint64_t appr[2];
+  int verdict[2];
+  int nleaves;
+  int src_q, src_r, src_g;
+  int lbase, abase;  // global numbers of this trajectory's leaf 0 / approval 0
+  double eps;
+};
+__device__ __forceinline__ void tc_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "TC_WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra TC_WAIT_%=;\n"
+      "}\n" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tc_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// asynchronous models without worker-run trajectories
+struct NoTraj {
+  __device__ __forceinline__ bool traj_ok() const { return false; }
+  __device__ void traj_start(int, int, int, double, int) {}
+  __device__ const double* traj_wait(int) { return nullptr; }
+  __device__ void traj_approve(int) {}
+  __device__ int traj_stop(int) { return 0; }
+};
 struct LogisticW {
   LogisticArgs a;
   VecStore S;  // the chain's vectors (driver side of post)
   double* wred;
   double* red_s;
-  int* cmd;  // smem: [0] 1 = evaluate / 0 = exit, [1] q vector id, [2] gradient vector id
+  int* cmd;  // smem: [0] 1 = evaluate / 2 = trajectory / 0 = exit, [1] q vector id, [2] gradient vector id
+  TrajCtl* tc;   // smem (team scratch, after cmd)
+  double* ring;  // smem: kTrajRing slots of (q, r, g: D doubles each; U), null when trajectories are off
   unsigned long long epoch;
+  int nleaf, nappr;  // driver copy: leaves waited for / approvals issued so far (global numbers)
+  int tl, ta, tn;    // driver: this trajectory's leaf 0 / approval 0 numbers, leaves
   static constexpr bool kAsync = true;
   static constexpr bool kVecOps = false;
-  // driver warp: post a pass (non-blocking arrive on barrier 2) ...
-  __device__ void post(int q, int g) {
-    if (threadIdx.x == 0) { cmd[0] = 1; cmd[1] = q; cmd[2] = g; }
+  __device__ __forceinline__ int slot_doubles() const { return 3 * (a.p + 1) + 2; }
+  // theta -> the pass's copies (fp32 hi/lo or padded fp64), element j of q,
+  // for the threads given by (j0, stride)
+  __device__ __forceinline__ void stage_theta(const double* th, int j0, int stride) const {
     if (a.th32 != nullptr) {
-      // theta rounded to float for the FP32 pass, by the driver lanes (the
-      // workers then start streaming without a conversion round and two syncs)
-      const double* th = S.v(q);
       float* t32 = const_cast<float*>(a.th32);
-      for (int j = (int)(threadIdx.x & 31); j <= a.pmax; j += 32) {
+      for (int j = j0; j <= a.pmax; j += stride) {
         const double v = (j < a.p) ? th[j] : (j == a.pmax ? th[a.p] : 0.0);
         const float h = (float)v;
         t32[j] = h;
         t32[64 + j] = (float)(v - (double)h);  // lo part: eta = X theta_hi + X theta_lo (logistic_cta_pass)
       }
-      __syncwarp();
     }
     if (a.thd != nullptr) {  // FP64 narrow pass: theta as zero-padded doubles
-      const double* th = S.v(q);
       double* td = const_cast<double*>(a.thd);
-      for (int j = (int)(threadIdx.x & 31); j <= a.pmax; j += 32)
-        td[j] = (j < a.p) ? th[j] : (j == a.pmax ? th[a.p] : 0.0);
-      __syncwarp();
+      for (int j = j0; j <= a.pmax; j += stride) td[j] = (j < a.p) ? th[j] : (j == a.pmax ? th[a.p] : 0.0);
     }
+  }
+  // driver warp: post a pass (non-blocking arrive on barrier 2) ...
+  __device__ void post(int q, int g) {
+    if (threadIdx.x == 0) { cmd[0] = 1; cmd[1] = q; cmd[2] = g; }
+    // theta staged by the driver lanes (the workers then start streaming
+    // without a conversion round and two syncs)
+    stage_theta(S.v(q), (int)(threadIdx.x & 31), 32);
+    __syncwarp();
     cta_arrive(2);  // publishes q and the command to the worker warps
   }
   // ... and collect it (barrier 3: gradient written to vector g, U in red_s)
@@ -155,14 +212,128 @@ struct LogisticW {
     post(q, g);
     return wait();
   }
-  // worker warps; `sa`: this CTA's copy of the launch state in shared memory
-  // (a local-memory copy is re-read on every pass and misses in the L1 that
-  // the TMA ring leaves over: ~0.8 us per pass of serialized misses)
+
+  // ------------------------------------------------ trajectories (driver side)
+  __device__ __forceinline__ bool traj_ok() const { return ring != nullptr; }
+  __device__ __forceinline__ double* traj_slot(int n) const { return ring + (n % kTrajRing) * slot_doubles(); }
+  // leaves 0 .. nleaves-1 of a doubling from (q, r, g) with step eps (nleaves >= 2)
+  __device__ void traj_start(int q, int r, int g, double eps, int nleaves) {
+    tl = nleaf; ta = nappr; tn = nleaves;
+    if ((threadIdx.x & 31) == 0) {
+      tc->src_q = q; tc->src_r = r; tc->src_g = g;
+      tc->eps = eps;
+      tc->nleaves = nleaves;
+      tc->lbase = tl;
+      tc->abase = ta;
+      cmd[0] = 2;
+    }
+    __syncwarp();
+    cta_arrive(2);
+  }
+  // wait for leaf n (in order); returns its slot (q | r | g | U)
+  __device__ const double* traj_wait(int n) {
+    const int L = nleaf++;
+    tc_wait(&tc->done[L & 1], (uint32_t)((L >> 1) & 1));
+    return traj_slot(n);
+  }
+  __device__ void traj_verdict(int v) {
+    const int A = nappr++;
+    if ((threadIdx.x & 31) == 0) {
+      tc->verdict[A & 1] = v;
+      tc_arrive(&tc->appr[A & 1]);
+    }
+    __syncwarp();
+  }
+  __device__ void traj_approve(int) { traj_verdict(1); }  // leaf n did not stop the tree
+  // the tree stopped at leaf n: returns 1 if the speculative leaf n+1 ran
+  // (waited for and discarded), else 0
+  __device__ int traj_stop(int n) {
+    traj_verdict(0);
+    if (n + 1 < tn) {  // leaf n+1 was approved (via leaf n-1) or is leaf 1
+      (void)traj_wait(n + 1);
+      return 1;
+    }
+    return 0;
+  }
+
+  // ------------------------------------------------ worker warps
+  // trajectory loop: leaf m = drift from leaf m-1 (or the start point), pass, kick
+  __device__ void serve_traj(const VecStore& S, const LogisticArgs& sa) {
+    const int D = sa.p + 1;
+    const int nl = tc->nleaves;
+    const int lbase = tc->lbase, abase = tc->abase;
+    const double eps = tc->eps;
+    const double half = __dmul_rn(0.5, eps);
+    const double* inv = S.v(V_INV);
+    const double* q0 = S.v(tc->src_q);
+    const double* r0 = S.v(tc->src_r);
+    const double* g0 = S.v(tc->src_g);
+    const int t = wk_tid(), nt = wk_threads();
+    // TS_PROF (CTA 0): [17] gate wait, [18] per-leaf work outside the pass, [19] leaves
+    const bool pf = sa.prof != nullptr && blockIdx.x == 0 && t == 0;
+    long long pc = pf ? clock64() : 0;
+    for (int m = 0; m < nl; ++m) {
+      if (m >= 2) {  // gate: leaf m-2's verdict
+        const long long g0c = pf ? clock64() : 0;
+        const int A = abase + m - 2;
+        tc_wait(&tc->appr[A & 1], (uint32_t)((A >> 1) & 1));
+        if (pf) { const long long g1 = clock64(); sa.prof[17] += g1 - g0c; pc += g1 - g0c; }
+        if (!tc->verdict[A & 1]) break;  // the tree stopped
+      }
+      double* sq = traj_slot(m);
+      double* sr = sq + D;
+      double* sg = sq + 2 * D;
+      // drift (Engine::drift_next / advance_drift): r_half into the slot's r;
+      // thread d also stages its own component for the pass (stage_theta)
+      for (int d = t; d < D; d += nt) {
+        const double rh = __dsub_rn(r0[d], __dmul_rn(half, g0[d]));
+        sr[d] = rh;
+        const double qd = __dadd_rn(q0[d], __dmul_rn(eps, __dmul_rn(inv[d], rh)));
+        sq[d] = qd;
+        const int j = d < sa.p ? d : sa.pmax;  // the bias goes to slot pmax
+        if (sa.th32 != nullptr) {
+          float* t32 = const_cast<float*>(sa.th32);
+          const float h = (float)qd;
+          t32[j] = h;
+          t32[64 + j] = (float)(qd - (double)h);
+        }
+        if (sa.thd != nullptr) const_cast<double*>(sa.thd)[j] = qd;
+      }
+      if (m == 0) {  // zero padding between p and pmax (stage_theta's layout)
+        for (int j = sa.p + t; j < sa.pmax; j += nt) {
+          if (sa.th32 != nullptr) { const_cast<float*>(sa.th32)[j] = 0.f; const_cast<float*>(sa.th32)[64 + j] = 0.f; }
+          if (sa.thd != nullptr) const_cast<double*>(sa.thd)[j] = 0.0;
+        }
+      }
+      wk_sync();
+      if (pf) sa.prof[18] += clock64() - pc;
+      logistic_eval_grid(sa, sq, sg, wred, red_s, epoch);
+      if (pf) pc = clock64();
+      // kick (Engine::advance_leaf): r = r_half - half * g (thread d wrote
+      // g[d]); U by the thread that wrote the log-likelihood total red_s[0]
+      // (the final loop of logistic_eval_grid: d = p + 1), prior red_s[1]
+      // was written before that loop's barrier
+      for (int d = t; d < D; d += nt) sr[d] = __dsub_rn(sr[d], __dmul_rn(half, sg[d]));
+      if (t == (sa.p + 1) % nt) sq[3 * D] = red_s[1] - red_s[0];
+      wk_sync();
+      if (t == 0) tc_arrive(&tc->done[(lbase + m) & 1]);
+      if (pf) sa.prof[19] += 1;
+      q0 = sq; r0 = sr; g0 = sg;
+    }
+  }
+  // `sa`: this CTA's copy of the launch state in shared memory (a
+  // local-memory copy is re-read on every pass and misses in the L1 that the
+  // TMA ring leaves over: ~0.8 us per pass of serialized misses)
   __device__ void serve(const VecStore& S, const LogisticArgs& sa) {
     for (;;) {
       cta_bar(2);
-      if (cmd[0] == 0) break;
-      logistic_eval_grid(sa, S, cmd[1], cmd[2], wred, red_s, epoch);
+      const int c = cmd[0];
+      if (c == 0) break;
+      if (c == 2) {
+        serve_traj(S, sa);
+        continue;
+      }
+      logistic_eval_grid(sa, S.v(cmd[1]), S.v(cmd[2]), wred, red_s, epoch);
       cta_arrive(3);
     }
   }
@@ -374,10 +545,25 @@ __global__ void __launch_bounds__(256, 1) k_block_op(MW mw, int D, int nslots, i
     mw.a.thd = (mw.a.fp64 && !mw.a.wide) ? mw.red_s + ((mw.a.p + 3) & ~1) : nullptr;
     mw.S = S;
     uintptr_t pb = reinterpret_cast<uintptr_t>(mw.red_s + mw.a.p + 2 + (kWideMax + 8) / 2);
+    mw.tc = reinterpret_cast<TrajCtl*>(mw.cmd + 16);
+    mw.ring = nullptr;
+    if (!mw.a.wide) {  // trajectory ring (LogisticW::serve_traj)
+      pb = (pb + 15) & ~(uintptr_t)15;
+      mw.ring = reinterpret_cast<double*>(pb);
+      pb += (size_t)kTrajRing * mw.slot_doubles() * sizeof(double);
+    }
     pb = (pb + 127) & ~(uintptr_t)127;
     mw.a.stages = reinterpret_cast<unsigned char*>(pb);
     mw.a.mbar = reinterpret_cast<uint64_t*>(pb + (size_t)rings * mw.a.nstage * mw.a.stage_bytes);
     mw.a.pipe = reinterpret_cast<WarpPipe*>(mw.a.mbar + rings * mw.a.nstage);
+    // trajectory handshake barriers (one arrival per phase); both sides number
+    // leaves and approvals from 0
+    mw.nleaf = 0; mw.nappr = 0; mw.tl = 0; mw.ta = 0; mw.tn = 0;
+    if (threadIdx.x == 0) {
+      for (int i = 0; i < 2; ++i) { mbar_init(&mw.tc->done[i], 1); mbar_init(&mw.tc->appr[i], 1); }
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
     if ((threadIdx.x >> 5) == 0) {
       // driver warp: the whole NUTS state machine, warp-synchronous
       Engine<WarpTeam, MW> E;

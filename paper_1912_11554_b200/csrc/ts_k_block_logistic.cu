@@ -54,7 +54,8 @@ int launch_block_logistic(const ts_model* m, int nslots, OpArgs& A, cudaStream_t
   if (scratch < threads) scratch = threads;
   if (scratch < m->p + 2) scratch = m->p + 2;
   const int nv_smem = m->wide ? (int)V_SLOT0 : num_vecs(nslots);
-  const size_t base = ((size_t)nv_smem * D + kTeamScratch + 2 + scratch + (m->p + 2) + (kWideMax + 8) / 2) * sizeof(double) + 128;
+  const size_t ring = m->wide ? 0 : ((size_t)kTrajRing * (3 * (m->p + 1) + 2) * sizeof(double) + 16);  // LogisticW::ring
+  const size_t base = ((size_t)nv_smem * D + kTeamScratch + 2 + scratch + (m->p + 2) + (kWideMax + 8) / 2) * sizeof(double) + 128 + ring;
   int dev = 0, nsm = 0, smem_max = 0;
   TS_CUDA(cudaGetDevice(&dev));
   TS_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));

@@ -87,7 +87,7 @@ __device__ __forceinline__ float tf32r(double x) {
   return __uint_as_float(v);
 }
 
-struct DenseW {
+struct DenseW : NoTraj {
   static constexpr bool kAsync = true;
   static constexpr bool kVecOps = true;  // D ~ 1000 vectors in global memory
   int D;

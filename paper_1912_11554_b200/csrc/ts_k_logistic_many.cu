@@ -135,7 +135,7 @@ __device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned l
 }
 
 // ---------------------------------------------------------------- chain side
-struct LogisticManyW {
+struct LogisticManyW : NoTraj {
   static constexpr bool kAsync = true;
   static constexpr bool kVecOps = false;
   int p;

@@ -1030,12 +1030,12 @@ static __device__ __forceinline__ void logistic_cta_dispatch(const LogisticArgs&
 // red_s (U = red_s[1] - red_s[0]) and the gradient in vector gid.  `epoch`
 // counts grid barriers already passed by this kernel (identical in every
 // CTA).  Called by the WORKER warps of the CTA.
-static __device__ void logistic_eval_grid(const LogisticArgs& a, const VecStore& S, int qid, int gid, double* wred,
+// (theta and g: contiguous vectors in shared memory)
+static __device__ void logistic_eval_grid(const LogisticArgs& a, const double* theta, double* g, double* wred,
                                           double* red_s, unsigned long long& epoch) {
   const int p = a.p;
   const int P2 = p + 2;
   const int64_t G = a.ncta;  // CTAs of this rank
-  const double* theta = S.v(qid);  // smem, contiguous (dstride 1)
   const bool prof = a.prof != nullptr && blockIdx.x == 0 && wk_tid() == 0;
   long long c0 = prof ? clock64() : 0, c1;
   // TS_PROF per-CTA skew: [24 + 2 b] += pass ns, [25 + 2 b] += barrier-wait ns (globaltimer)
@@ -1116,7 +1116,6 @@ static __device__ void logistic_eval_grid(const LogisticArgs& a, const VecStore&
   if (a.dump && epoch == 1 && blockIdx.x == 0)  // test hook: this GPU's totals of the first pass
     for (int i = wk_tid(); i < 2 * P2 + 1; i += wk_threads()) a.dump[i] = total(i);
 
-  double* g = S.v(gid);
   if (a.world > 0) {
     // Row sharding across GPUs: CTA 0 pushes this GPU's totals into slot
     // x % 3 of every rank's mailbox (NVLink stores to peer memory), then

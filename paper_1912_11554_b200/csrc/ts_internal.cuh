@@ -272,53 +272,64 @@ struct LogisticW {
     // TS_PROF (CTA 0): [17] gate wait, [18] per-leaf work outside the pass, [19] leaves
     const bool pf = sa.prof != nullptr && blockIdx.x == 0 && t == 0;
     long long pc = pf ? clock64() : 0;
-    for (int m = 0; m < nl; ++m) {
-      if (m >= 2) {  // gate: leaf m-2's verdict
-        const long long g0c = pf ? clock64() : 0;
-        const int A = abase + m - 2;
-        tc_wait(&tc->appr[A & 1], (uint32_t)((A >> 1) & 1));
-        if (pf) { const long long g1 = clock64(); sa.prof[17] += g1 - g0c; pc += g1 - g0c; }
-        if (!tc->verdict[A & 1]) break;  // the tree stopped
+    // drift of one component into slot (sq, sr) from (q, r, g), staged for the pass
+    auto drift = [&](double* sq, double* sr, int d, double qv, double rv, double gv) {
+      const double rh = __dsub_rn(rv, __dmul_rn(half, gv));
+      sr[d] = rh;
+      const double qd = __dadd_rn(qv, __dmul_rn(eps, __dmul_rn(inv[d], rh)));
+      sq[d] = qd;
+      const int j = d < sa.p ? d : sa.pmax;  // the bias goes to slot pmax (stage_theta's layout)
+      if (sa.th32 != nullptr) {
+        float* t32 = const_cast<float*>(sa.th32);
+        const float h = (float)qd;
+        t32[j] = h;
+        t32[64 + j] = (float)(qd - (double)h);
       }
+      if (sa.thd != nullptr) const_cast<double*>(sa.thd)[j] = qd;
+    };
+    // leaf 0: drift from the start point; zero padding between p and pmax
+    {
+      double* sq = traj_slot(0);
+      for (int d = t; d < D; d += nt) drift(sq, sq + D, d, q0[d], r0[d], g0[d]);
+      for (int j = sa.p + t; j < sa.pmax; j += nt) {
+        if (sa.th32 != nullptr) { const_cast<float*>(sa.th32)[j] = 0.f; const_cast<float*>(sa.th32)[64 + j] = 0.f; }
+        if (sa.thd != nullptr) const_cast<double*>(sa.thd)[j] = 0.0;
+      }
+      wk_sync();
+    }
+    for (int m = 0; m < nl; ++m) {
       double* sq = traj_slot(m);
       double* sr = sq + D;
       double* sg = sq + 2 * D;
-      // drift (Engine::drift_next / advance_drift): r_half into the slot's r;
-      // thread d also stages its own component for the pass (stage_theta)
-      for (int d = t; d < D; d += nt) {
-        const double rh = __dsub_rn(r0[d], __dmul_rn(half, g0[d]));
-        sr[d] = rh;
-        const double qd = __dadd_rn(q0[d], __dmul_rn(eps, __dmul_rn(inv[d], rh)));
-        sq[d] = qd;
-        const int j = d < sa.p ? d : sa.pmax;  // the bias goes to slot pmax
-        if (sa.th32 != nullptr) {
-          float* t32 = const_cast<float*>(sa.th32);
-          const float h = (float)qd;
-          t32[j] = h;
-          t32[64 + j] = (float)(qd - (double)h);
-        }
-        if (sa.thd != nullptr) const_cast<double*>(sa.thd)[j] = qd;
-      }
-      if (m == 0) {  // zero padding between p and pmax (stage_theta's layout)
-        for (int j = sa.p + t; j < sa.pmax; j += nt) {
-          if (sa.th32 != nullptr) { const_cast<float*>(sa.th32)[j] = 0.f; const_cast<float*>(sa.th32)[64 + j] = 0.f; }
-          if (sa.thd != nullptr) const_cast<double*>(sa.thd)[j] = 0.0;
-        }
-      }
-      wk_sync();
       if (pf) sa.prof[18] += clock64() - pc;
       logistic_eval_grid(sa, sq, sg, wred, red_s, epoch);
       if (pf) pc = clock64();
-      // kick (Engine::advance_leaf): r = r_half - half * g (thread d wrote
-      // g[d]); U by the thread that wrote the log-likelihood total red_s[0]
-      // (the final loop of logistic_eval_grid: d = p + 1), prior red_s[1]
-      // was written before that loop's barrier
-      for (int d = t; d < D; d += nt) sr[d] = __dsub_rn(sr[d], __dmul_rn(half, sg[d]));
+      // kick of leaf m (Engine::advance_leaf: r = r_half - half * g; thread d
+      // wrote g[d]) fused with the drift of leaf m+1 into the next slot (free:
+      // its previous leaf m-3 was consumed before leaf m-1 passed its gate);
+      // if the tree stops at leaf m-1 the drift is simply never streamed
+      const bool next = m + 1 < nl;
+      double* nq = traj_slot(m + 1);
+      for (int d = t; d < D; d += nt) {
+        const double gd = sg[d];
+        const double rd = __dsub_rn(sr[d], __dmul_rn(half, gd));
+        sr[d] = rd;
+        if (next) drift(nq, nq + D, d, sq[d], rd, gd);
+      }
+      // U by the thread that wrote the log-likelihood total red_s[0] (the
+      // final loop of logistic_eval_grid: d = p + 1); the prior red_s[1] was
+      // written before that loop's barrier
       if (t == (sa.p + 1) % nt) sq[3 * D] = red_s[1] - red_s[0];
       wk_sync();
       if (t == 0) tc_arrive(&tc->done[(lbase + m) & 1]);
       if (pf) sa.prof[19] += 1;
-      q0 = sq; r0 = sr; g0 = sg;
+      if (next && m + 1 >= 2) {  // gate of leaf m+1: leaf m-1's verdict
+        const long long g0c = pf ? clock64() : 0;
+        const int A = abase + m - 1;
+        tc_wait(&tc->appr[A & 1], (uint32_t)((A >> 1) & 1));
+        if (pf) { const long long g1 = clock64(); sa.prof[17] += g1 - g0c; pc += g1 - g0c; }
+        if (!tc->verdict[A & 1]) break;  // the tree stopped
+      }
     }
   }
   // `sa`: this CTA's copy of the launch state in shared memory (a

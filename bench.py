@@ -772,7 +772,7 @@ def run_many(ctx, args, C=256, W=100, S=100):
                                 "epilogue (sigmoid, log-likelihood, bf16 split of the residuals) bounds the step"}}
     if ctx.rank == 0 and ctx.world == 1 and not args.no_cpu:
         try:
-            nc = cores()
+            nc = min(cores(), 32)  # each process holds covtype X (251 MB) and its numba code: bounded host memory
             ps = [run_worker("logistic", {"rows": N_ROWS, "features": N_FEAT, "seed": DATA_SEED, "seconds": args.cpu_seconds,
                                           "numpy": False, "key_seed": 100 + k}, 1) for k in range(nc)]
             outs = collect(ps)

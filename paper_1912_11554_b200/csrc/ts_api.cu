@@ -49,6 +49,28 @@ __global__ void k_retile(const float* __restrict__ x, const uint8_t* __restrict_
   if (__syncthreads_or(sub) && threadIdx.x == 0) atomicOr(has_subnormal, 1);
 }
 
+// fp64 storage, p <= 64 (ts_logistic.cuh, logistic_cta_pass_x64h): 16-row
+// tiles, lane 16 h + r = row r's features [h H, h H + H) in lane-contiguous
+// pairs of doubles, then the 16 labels; padding (odd H / odd p, rows past n)
+// stays zero from the memset.
+__global__ void k_retile_x64h(const double* __restrict__ x, const uint8_t* __restrict__ y, int64_t n, int p,
+                              int64_t ntiles, unsigned char* __restrict__ xt) {
+  const int H = x64h_half(p), G = x64h_groups(p);
+  const int64_t tb = x64h_tile_bytes(p);
+  const int64_t total = ntiles * 16 * (int64_t)p;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = i / p;
+    const int j = (int)(i % p);
+    const int64_t t = row >> 4;
+    const int r = (int)(row & 15);
+    const int h = j >= H ? 1 : 0;
+    const int k = j - h * H;
+    unsigned char* tile = xt + t * tb;
+    reinterpret_cast<double*>(tile)[((k >> 1) * 32 + 16 * h + r) * 2 + (k & 1)] = row < n ? x[row * p + j] : 0.0;
+    if (j == 0) tile[512 * G + r] = row < n ? y[row] : 0;
+  }
+}
+
 // Wide p (64 < p <= 256): tiles of kWideRows = 8 rows, row-major, each
 // followed by 16 label bytes (8 labels + 8 zeros): 32p + 16 bytes per tile,
 // one TMA bulk copy (ts_logistic.cuh, logistic_cta_pass_wide).
@@ -200,24 +222,31 @@ extern "C" int ts_model_create(int kind, int dim, const double* params, int n_pa
       }
       m->pmax = pick_pmax(n_feat);
       if (!m->pmax) return fail(TS_EUNSUPPORTED, "logistic feature count > 256 not supported on this path");
-      m->xd = precision == TS_PREC_FP64X;  // X stored as fp64: always the wide layout
-      m->wide = n_feat > 64 || m->xd;
-      if (m->xd) m->pmax = kWideMax;
+      m->xd = precision == TS_PREC_FP64X;  // X stored as fp64
+      m->wide = n_feat > 64;
+      m->xh = m->xd && !m->wide;  // fp64 storage, p <= 64: 16-row half-row tiles
+      if (m->xd) m->pmax = m->wide ? kWideMax : kX64hPmax;
       m->n_rows = n_rows;
       m->p = n_feat;
       // wide: whole groups of kWideGroup tiles (32 rows), padding rows zero with label 0
-      m->ntiles = m->wide ? (n_rows + kWideRows * kWideGroup - 1) / (kWideRows * kWideGroup) * kWideGroup : (n_rows + 31) / 32;
+      m->ntiles = m->wide ? (n_rows + kWideRows * kWideGroup - 1) / (kWideRows * kWideGroup) * kWideGroup
+                          : (m->xh ? (n_rows + 15) / 16 : (n_rows + 31) / 32);
       m->fp64 = precision == TS_PREC_FP64 || m->xd;
       const size_t xbytes = m->wide ? (size_t)m->ntiles * wide_tile_bytes(n_feat, m->xd ? 8 : 4)
-                                    : (size_t)m->ntiles * 32 * n_feat * sizeof(float);
+                                    : (m->xh ? (size_t)m->ntiles * x64h_tile_bytes(n_feat)
+                                             : (size_t)m->ntiles * 32 * n_feat * sizeof(float));
       if (cudaMalloc((void**)&m->xt, xbytes) != cudaSuccess) return fail(TS_ECUDA, "cudaMalloc X failed");
       // wide tiles carry their labels; the separate label array is then unused
-      if (cudaMalloc((void**)&m->yt, m->wide ? 16 : (size_t)m->ntiles * 32) != cudaSuccess) return fail(TS_ECUDA, "cudaMalloc y failed");
+      if (cudaMalloc((void**)&m->yt, (m->wide || m->xh) ? 16 : (size_t)m->ntiles * 32) != cudaSuccess) return fail(TS_ECUDA, "cudaMalloc y failed");
       // grid-barrier counters: one cache line per (emulated) rank, up to 8
       if (cudaMalloc((void**)&m->bar, 16 * 8 * sizeof(unsigned long long)) != cudaSuccess) return fail(TS_ECUDA, "cudaMalloc barrier failed");
       if (cudaMemset(m->bar, 0, 16 * 8 * sizeof(unsigned long long)) != cudaSuccess) return fail(TS_ECUDA, "memset barrier failed");
       // the barrier word doubles as the "X has fp32 subnormals" flag during re-tiling
-      if (m->xd)
+      if (m->xh) {
+        if (cudaMemset(m->xt, 0, xbytes) != cudaSuccess) return fail(TS_ECUDA, "memset X failed");
+        k_retile_x64h<<<1184, 256>>>(static_cast<const double*>(x_dev), y_dev, n_rows, n_feat, m->ntiles,
+                                     reinterpret_cast<unsigned char*>(m->xt));
+      } else if (m->xd)
         k_retile_wide<double><<<1184, 256>>>(static_cast<const double*>(x_dev), y_dev, n_rows, n_feat, m->ntiles,
                                              reinterpret_cast<unsigned char*>(m->xt), reinterpret_cast<int*>(m->bar));
       else if (m->wide)

@@ -172,21 +172,37 @@ __device__ __forceinline__ bool al16(const void* p) { return (reinterpret_cast<u
 // advance_leaf (kick of leaf n from its pass), add_cum, the kinetic-energy
 // partial of leaf n (same lane order as warp_kinetic2), drift_next (leaf
 // n+1) and the request row for leaf n+1 (tf32 floats, or doubles).  Every
-// element gets the same arithmetic as the separate loops.
-template <bool F64ROW>
+// element gets the same arithmetic as the separate loops.  ST: the leaf's
+// NodeStore copies written from the same registers (leaf_book's copies,
+// which would re-read the vectors in another pass): 5 = even leaf into its
+// slot (q, r, cum, proposal q, proposal g -> st[0..4]), 2 = odd leaf into
+// the running proposal (st[0] = q, st[1] = g), 0 = none.
+template <bool F64ROW, int ST>
 static __device__ __noinline__ double warp_leaf_fused(double2* __restrict__ q, double2* __restrict__ r,
                                                       double2* __restrict__ g, double2* __restrict__ nq,
-                                                      double2* __restrict__ nr, const double2* __restrict__ ng,
+                                                      double2* __restrict__ nr, const void* __restrict__ grow,
                                                       const double2* __restrict__ inv, double2* __restrict__ cum,
-                                                      void* __restrict__ row, double half, double eps, int n2) {
-  double kin = 0.0;
+                                                      void* __restrict__ row, double half, double eps, int n2,
+                                                      double& udot,
+                                                      double2* __restrict__ st0 = nullptr, double2* __restrict__ st1 = nullptr,
+                                                      double2* __restrict__ st2 = nullptr, double2* __restrict__ st3 = nullptr,
+                                                      double2* __restrict__ st4 = nullptr) {
+  // grow: the served gradient row (fp32 tf32-GEMM output, or doubles);
+  // udot: this lane's part of q . g (U = q'Aq / 2 = q . g / 2)
+  double kin = 0.0, ud = 0.0;
   for (int base = (int)(threadIdx.x & 31); base < n2; base += 32 * 4) {
     double2 tq[4], tr[4], tg[4], ti[4], tc[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u)
       if (base + 32 * u < n2) {
         const int i = base + 32 * u;
-        tq[u] = nq[i]; tr[u] = nr[i]; tg[u] = ng[i]; ti[u] = inv[i]; tc[u] = cum[i];
+        tq[u] = nq[i]; tr[u] = nr[i]; ti[u] = inv[i]; tc[u] = cum[i];
+        if constexpr (F64ROW) {
+          tg[u] = __ldcg(reinterpret_cast<const double2*>(grow) + i);
+        } else {
+          const float2 f = __ldcg(reinterpret_cast<const float2*>(grow) + i);
+          tg[u] = make_double2((double)f.x, (double)f.y);
+        }
       }
 #pragma unroll
     for (int u = 0; u < 4; ++u)
@@ -198,9 +214,13 @@ static __device__ __noinline__ double warp_leaf_fused(double2* __restrict__ q, d
         q[i] = tq[u];
         g[i] = tg[u];
         r[i] = rr;
+        ud = __dadd_rn(ud, __dmul_rn(tq[u].x, tg[u].x));
+        ud = __dadd_rn(ud, __dmul_rn(tq[u].y, tg[u].y));
         cv.x = __dadd_rn(tc[u].x, rr.x);
         cv.y = __dadd_rn(tc[u].y, rr.y);
         cum[i] = cv;
+        if constexpr (ST == 5) { st0[i] = tq[u]; st1[i] = rr; st2[i] = cv; st3[i] = tq[u]; st4[i] = tg[u]; }
+        if constexpr (ST == 2) { st0[i] = tq[u]; st1[i] = tg[u]; }
         kin = __dadd_rn(kin, __dmul_rn(__dmul_rn(__dmul_rn(0.5, rr.x), rr.x), ti[u].x));
         kin = __dadd_rn(kin, __dmul_rn(__dmul_rn(__dmul_rn(0.5, rr.y), rr.y), ti[u].y));
         rh.x = __dsub_rn(rr.x, __dmul_rn(half, tg[u].x));
@@ -219,6 +239,7 @@ static __device__ __noinline__ double warp_leaf_fused(double2* __restrict__ q, d
         }
       }
   }
+  udot = ud;
   return kin;
 }
 // up to 5 vector copies in one pass (k pairs), 2 x double2 per operand in flight
@@ -543,11 +564,12 @@ struct Engine {
   __device__ int fq_id() const { return f_alias < 0 ? (int)V_FQ : slot_vec(f_alias, 0); }
   __device__ int fr_id() const { return f_alias < 0 ? (int)V_FR : slot_vec(f_alias, 1); }
   __device__ int cumf_id() const { return f_alias < 0 ? (int)V_CUMF : slot_vec(f_alias, 2); }
-  __device__ void running_from_leaf(int n, double lw, double metro, double h, bool with_first = true) {
+  __device__ void running_from_leaf(int n, double lw, double metro, double h, bool with_first = true,
+                                    bool copy_proposal = true) {
     if (with_first) {
       copy_group(V_FQ, V_CQ, V_FR, V_CR, V_CUMF, V_CUM, V_TPQ, V_CQ, V_TPG, V_CG);
       f_alias = -1;
-    } else {
+    } else if (copy_proposal) {
       copy_group(V_TPQ, V_CQ, V_TPG, V_CG, V_TPG, V_CG);
     }
     r_lw = lw; r_metro = metro; r_count = 1; r_pU = cur_U; r_pH = h; r_pidx = n; r_fU = cur_U;
@@ -720,7 +742,10 @@ struct Engine {
 
   // Bookkeeping of leaf n (tree.py:403-450): divergence exit, even-leaf store
   // at slot popcount(n), odd-leaf merges + U-turn checks down to i_min.
-  __device__ int leaf_book(unsigned long long n, double h, double delta, Stream& draws, bool forward) {
+  // prestored: the leaf pass already wrote the even leaf's slot / the odd
+  // leaf's running proposal (warp_leaf_fused ST)
+  __device__ int leaf_book(unsigned long long n, double h, double delta, Stream& draws, bool forward,
+                           bool prestored = false) {
     const double thr = cfg.threshold;
     const int pc = __popcll(n);
     if (!(isfinite(delta) && delta <= thr)) {
@@ -735,8 +760,9 @@ struct Engine {
     ev_lw(lw);
     if ((n & 1ULL) == 0) {
       const int slot = pc;
-      copy_group(slot_vec(slot, 0), V_CQ, slot_vec(slot, 1), V_CR, slot_vec(slot, 2), V_CUM, slot_vec(slot, 3), V_CQ,
-                 slot_vec(slot, 4), V_CG);
+      if (!prestored)
+        copy_group(slot_vec(slot, 0), V_CQ, slot_vec(slot, 1), V_CR, slot_vec(slot, 2), V_CUM, slot_vec(slot, 3), V_CQ,
+                   slot_vec(slot, 4), V_CG);
       SlotScalars& L = ss[slot];
       L.lw = lw; L.metro = metro; L.pU = cur_U; L.pH = h; L.fU = cur_U;
       L.count = 1; L.pidx = (int)n; L.leaf = (int)n;
@@ -746,7 +772,7 @@ struct Engine {
     }
     int slot = pc - 1;
     const int i_min = slot - __popcll(((n + 1) & ~n) - 1) + 1;
-    running_from_leaf((int)n, lw, metro, h, false);  // odd n: at least one merge follows
+    running_from_leaf((int)n, lw, metro, h, false, !prestored);  // odd n: at least one merge follows
     while (slot >= i_min) {
       ev(kEvCheck, (int)n, slot, ss[slot].leaf);
       merge_slot(slot, draws.next_double());
@@ -850,15 +876,26 @@ struct Engine {
         drift_next(eps);
         post_eval(V_NQ, V_NG);
         for (unsigned long long n = 0; n < nleaves; ++n) {
-          const double u = wait_eval();
           const bool spec = n + 1 < nleaves;
+          bool fusable = false;
+          if constexpr (Team::kWarp && Team::kUnitStride && Model::kVecOps) fusable = spec && D >= 128 && (D & 1) == 0;
+          double u = 0.0;
+          bool waited = false;
+          if constexpr (Team::kWarp && Team::kUnitStride && Model::kVecOps) {
+            if (fusable) {
+              M.wait_poll();  // the fused pass reads the gradient row itself and forms U
+              n_evals += 1;
+              waited = true;
+            }
+          }
+          if (!waited) u = wait_eval();
           double h, delta;
           bool fused = false;
           if constexpr (Team::kWarp && Team::kUnitStride && Model::kVecOps) {
-            // batched large-D model: kick, prefix sum, kinetic energy, next
-            // drift and the request row in one pass over the vectors
-            if (spec && D >= 128 && (D & 1) == 0) {
-              cur_U = u;
+            // batched large-D model: kick, prefix sum, kinetic energy, U,
+            // next drift, the request row and the NodeStore copies in one
+            // pass over the vectors
+            if (fusable) {
               const double half = __dmul_rn(0.5, eps);
               void* row = M.request_row();
               double2* q2 = reinterpret_cast<double2*>(v(V_CQ));
@@ -866,14 +903,32 @@ struct Engine {
               double2* g2 = reinterpret_cast<double2*>(v(V_CG));
               double2* nq2 = reinterpret_cast<double2*>(v(V_NQ));
               double2* nr2 = reinterpret_cast<double2*>(v(V_NR));
-              const double2* ng2 = reinterpret_cast<const double2*>(v(V_NG));
+              const void* ng2 = M.grad_row();
               const double2* inv2 = reinterpret_cast<const double2*>(v(V_INV));
               double2* c2 = reinterpret_cast<double2*>(v(V_CUM));
-              const double kin = M.fp64
-                  ? warp_leaf_fused<true>(q2, r2, g2, nq2, nr2, ng2, inv2, c2, row, half, eps, D >> 1)
-                  : warp_leaf_fused<false>(q2, r2, g2, nq2, nr2, ng2, inv2, c2, row, half, eps, D >> 1);
+              // leaf_book's NodeStore copies written by the same pass
+              double kin, ud = 0.0;
+              if ((n & 1ULL) == 0) {
+                const int sl = __popcll(n);
+                double2* st[5];
+#pragma unroll
+                for (int k = 0; k < 5; ++k) st[k] = reinterpret_cast<double2*>(v(slot_vec(sl, k)));
+                kin = M.fp64 ? warp_leaf_fused<true, 5>(q2, r2, g2, nq2, nr2, ng2, inv2, c2, row, half, eps, D >> 1, ud,
+                                                         st[0], st[1], st[2], st[3], st[4])
+                             : warp_leaf_fused<false, 5>(q2, r2, g2, nq2, nr2, ng2, inv2, c2, row, half, eps, D >> 1, ud,
+                                                          st[0], st[1], st[2], st[3], st[4]);
+              } else {
+                double2* tpq = reinterpret_cast<double2*>(v(V_TPQ));
+                double2* tpg = reinterpret_cast<double2*>(v(V_TPG));
+                kin = M.fp64 ? warp_leaf_fused<true, 2>(q2, r2, g2, nq2, nr2, ng2, inv2, c2, row, half, eps, D >> 1, ud, tpq, tpg)
+                             : warp_leaf_fused<false, 2>(q2, r2, g2, nq2, nr2, ng2, inv2, c2, row, half, eps, D >> 1, ud, tpq, tpg);
+              }
               T.sync();
               M.post_written(V_NQ, V_NG);
+              {
+                const double uu = 0.5 * T.sum(ud);  // DenseW::wait's U, formed in the pass
+                cur_U = isfinite(uu) ? uu : kInf();
+              }
               const double ke = T.sum(kin);
               if (!isfinite(cur_U)) h = kInf();
               else {
@@ -897,7 +952,7 @@ struct Engine {
             add_cum();
             leaf_energy(h_ref, h, delta);
           }
-          stop = leaf_book(n, h, delta, draws, forward);
+          stop = leaf_book(n, h, delta, draws, forward, fused);
           if (stop != kStopNone) {
             if (spec) { (void)wait_eval(); n_wasted += 1; }
             break;

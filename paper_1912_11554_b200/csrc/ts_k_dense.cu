@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(128, 1)
 // outstanding, so reads and writes never race.  Chains therefore never
 // wait for the slowest chain (no lockstep): a request waits at most one
 // step (~GEMM + 2 grid barriers).
-constexpr int kDenseCW = 8;  // chain warps per CTA
+constexpr int kDenseCW = 8;  // chain warps per CTA (at most; DenseArgs::cpc of them run chains)
 
 __device__ __forceinline__ void st_release_gpu_u64(unsigned long long* p, unsigned long long v) {
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
@@ -135,6 +135,20 @@ struct DenseW : NoTraj {
     __syncwarp();
     seq += 1;
     if (lane == 0) st_release_gpu_u64(posted + chain, seq);
+  }
+  // the engine's fused leaf pass: wait for the step, then read the row itself
+  __device__ void wait_poll() {
+    if ((threadIdx.x & 31) == 0) {
+      SpinGuard sg(err, spin_ns);
+      while (ld_relaxed_u64(served + chain) < seq) {
+        if (sg.expired()) break;
+      }
+      (void)ld_acquire_u64(served + chain);
+    }
+    __syncwarp();
+  }
+  __device__ const void* grad_row() const {
+    return fp64 ? (const void*)(gt64 + (int64_t)chain * D) : (const void*)(gt + (int64_t)chain * D);
   }
   __device__ double wait() {
     const int lane = threadIdx.x & 31;
@@ -212,6 +226,7 @@ struct DenseW : NoTraj {
 
 struct DenseArgs {
   int D, C, Cpad, fp64, nv;
+  int cpc;    // chains per CTA (<= kDenseCW): C spread over every SM (1024 chains: 7 x 147 CTAs, not 8 x 128)
   int chain0;  // first chain of this launch (runs with more chains than one grid holds are chunked)
   float* xt;
   double* xt64;
@@ -289,7 +304,7 @@ __global__ void __launch_bounds__(128 + 32 * kDenseCW, 1)
     const int mt = (a.D + kUmmaBM - 1) / kUmmaBM, nt = a.Cpad / kUmmaBN;
     const int nkb = (a.D + kUmmaBK - 1) / kUmmaBK;
     const int total = (int)gridDim.x * kDenseCW;
-    const int my_chain = blockIdx.x * kDenseCW + t;  // t < kDenseCW: this CTA's chain t
+    const int my_chain = blockIdx.x * a.cpc + t;  // t < cpc: this CTA's chain t
     unsigned long long srv = 0;                      // requests of my_chain served so far
     unsigned long long epoch = 0;
     const bool prof = a.prof != nullptr && blockIdx.x == 0 && t == 0;
@@ -298,7 +313,7 @@ __global__ void __launch_bounds__(128 + 32 * kDenseCW, 1)
     for (int step = 0;; ++step) {
       // snapshot: requests outstanding now are served by this step
       unsigned long long mine = 0;
-      if (t < kDenseCW) {
+      if (t < a.cpc) {
         const unsigned long long p = ld_acquire_u64(a.posted + my_chain);
         mine = p > srv ? p : 0ULL;
         a.pending[my_chain] = mine;
@@ -345,7 +360,7 @@ __global__ void __launch_bounds__(128 + 32 * kDenseCW, 1)
         tp0 = tp1;
       }
       gemm_grid_barrier(a.bar, epoch, a.err, a.spin_ns);  // all gradient tiles written
-      if (t < kDenseCW && mine) {
+      if (t < a.cpc && mine) {
         srv = mine;
         st_release_gpu_u64(a.served + my_chain, mine);
       }
@@ -362,9 +377,9 @@ __global__ void __launch_bounds__(128 + 32 * kDenseCW, 1)
   }
   // ---------------- chain warps
   const int cw = warp - 4;
-  const int chain = blockIdx.x * kDenseCW + cw;
+  const int chain = blockIdx.x * a.cpc + cw;
   const int n_active = (A.op == OP_RUN) ? a.C : 1;
-  if (chain < n_active) {
+  if (cw < a.cpc && chain < n_active) {
     DenseW M;
     M.D = a.D;
     M.fp64 = a.fp64;
@@ -418,8 +433,15 @@ int launch_dense(const ts_model* m, int nslots, OpArgs& A, int n_chains, cudaStr
 static int launch_dense_chunk(const ts_model* m, int nslots, OpArgs& A, int C, int chain0, cudaStream_t st) {
   ts_model* mm = const_cast<ts_model*>(m);
   const int D = m->dim;
-  const int grid = (C + kDenseCW - 1) / kDenseCW;
-  const int Cpad = ((grid * kDenseCW + kUmmaBN - 1) / kUmmaBN) * kUmmaBN;
+  int dev0 = 0, nsm0 = 148;
+  TS_CUDA(cudaGetDevice(&dev0));
+  TS_CUDA(cudaDeviceGetAttribute(&nsm0, cudaDevAttrMultiProcessorCount, dev0));
+  // chains per CTA: the fewest that fit C on one CTA per SM, so every SM runs chains
+  int cpc = (C + nsm0 - 1) / nsm0;
+  if (cpc > kDenseCW) cpc = kDenseCW;
+  if (cpc < 1) cpc = 1;
+  const int grid = (C + cpc - 1) / cpc;
+  const int Cpad = ((grid * cpc + kUmmaBN - 1) / kUmmaBN) * kUmmaBN;
   const int nv = num_vecs(nslots);
   int dev = 0, nsm = 0;
   TS_CUDA(cudaGetDevice(&dev));
@@ -442,7 +464,7 @@ static int launch_dense_chunk(const ts_model* m, int nslots, OpArgs& A, int C, i
   }
   DenseArgs a;
   memset(&a, 0, sizeof a);
-  a.D = D; a.C = C; a.Cpad = Cpad; a.fp64 = m->fp64; a.nv = nv; a.chain0 = chain0;
+  a.D = D; a.C = C; a.Cpad = Cpad; a.fp64 = m->fp64; a.nv = nv; a.chain0 = chain0; a.cpc = cpc;
   unsigned char* p = mm->dws;
   a.bar = reinterpret_cast<unsigned long long*>(p);
   a.done = reinterpret_cast<int*>(p + 8);

@@ -94,6 +94,7 @@ struct LogisticArgs {
   int llmode;                      // FP32 narrow pass: log-likelihood term precision (logistic_cta_pass LL)
   int xd;                          // X stored as fp64 (wide layout, logistic_cta_pass_wide XD)
   const double* thd;  // FP64 narrow pass: theta as doubles [pmax + 1], zero-padded, 16-B aligned (smem, written by the driver)
+  int xh;                          // X stored as fp64 in the 16-row half-row layout (p <= 64, logistic_cta_pass_x64h)
 };
 
 // Mailbox of one rank: kMailFlags words of flags (flag[src] = 1 + the last
@@ -680,6 +681,160 @@ __device__ __noinline__ void logistic_cta_pass(const LogisticArgs& a, const doub
   if (prof) { pc1 = clock64(); a.prof[7] += pc1 - pc0; }
 }
 
+// ------------------------------------------------------ fp64 storage, p <= 64
+// Precision "fp64x" with p <= 64 (data that are not fp32-exact, kept in
+// double as the reference's LogisticRegressionData does, models.py:43-64):
+// 16-row tiles; lane L = 16 h + r holds row r's features [h H, h H + H),
+// H = ceil(p / 2), lane-contiguously in groups of 2 doubles (LDS.128,
+// conflict-free), then the 16 labels: one TMA bulk copy of 512 G + 16 bytes
+// per tile (G = ceil(H / 2) groups; covtype: 7,184 B for 16 rows, +3.7% over
+// 8 p bytes per row).  Each lane forms half of eta, one shuffle adds the
+// halves, both halves evaluate the row and accumulate the gradient of their
+// own features: 27 doubles of x and 27 accumulators per lane at p = 54 (the
+// 32-row layout would need 54 + 55 live doubles and spills).
+__host__ __device__ inline int x64h_half(int p) { return (p + 1) / 2; }
+__host__ __device__ inline int x64h_groups(int p) { return (x64h_half(p) + 1) / 2; }
+__host__ __device__ inline int64_t x64h_tile_bytes(int p) { return (int64_t)x64h_groups(p) * 512 + 16; }
+__host__ __device__ inline int x64h_stage_bytes(int p) { return (int)((x64h_tile_bytes(p) + 127) / 128 * 128); }
+constexpr int kX64hPmax = 64;  // thd capacity (zero padding between p and 64, bias at 64)
+
+// HE > 0: compile-time H (covtype: 27); else runtime H <= 32
+template <int HE>
+__device__ __noinline__ void logistic_cta_pass_x64h(const LogisticArgs& a, const double* __restrict__ theta_s,
+                                                    double* wred, double* red_out) {
+  extern __shared__ __align__(16) unsigned char ts_dyn_smem[];
+  constexpr int KX = HE > 0 ? ((HE + 1) & ~1) : 32;  // x values per lane (whole groups)
+  constexpr int NA = kX64hPmax + 2;
+  const int lane = threadIdx.x & 31, warp = wk_warp(), nwarps = wk_nwarps();
+  const int p = a.p;
+  const int H = HE > 0 ? HE : x64h_half(p);
+  const int G = (H + 1) >> 1;
+  const int h = lane >> 4, r = lane & 15;
+  const int f0 = h * H;
+  WarpPipe& pipe = a.pipe[warp];
+  const int count = pipe.count;
+  const bool prof = a.prof != nullptr && blockIdx.x == 0 && wk_tid() == 0;
+  long long pc0 = prof ? clock64() : 0, pc1;
+  const int nstage = a.nstage;
+  const int stage_bytes = a.stage_bytes;
+  const uint32_t ring_off = (uint32_t)(a.stages - ts_dyn_smem) + (uint32_t)(warp * nstage * stage_bytes);
+  uint64_t* const bars = a.mbar + warp * nstage;
+  // this lane's theta (zero past its features: thd is zero-padded to 64)
+  const double* thd = reinterpret_cast<const double*>(ts_dyn_smem + (reinterpret_cast<const unsigned char*>(a.thd) - ts_dyn_smem));
+  double th[KX];
+#pragma unroll
+  for (int k = 0; k < KX; ++k) th[k] = (k < H && f0 + k < p) ? thd[f0 + k] : 0.0;
+  const double thb = thd[kX64hPmax];
+  double acc[KX];
+#pragma unroll
+  for (int k = 0; k < KX; ++k) acc[k] = 0.0;
+  double accb = 0.0, accl = 0.0;
+  if (count > 0) {
+    const unsigned long long c0 = pipe.consumed;
+    unsigned long long issued = pipe.issued;
+    const int tfirst = pipe.first, tstride = nwarps;
+    const int nfull = (int)(a.n_rows >> 4), rem = (int)(a.n_rows & 15);
+    const uint32_t tb = (uint32_t)x64h_tile_bytes(p);
+    const unsigned char* const xfirst = reinterpret_cast<const unsigned char*>(a.xt) + (int64_t)tfirst * tb;
+    const int64_t xstep = (int64_t)tstride * tb;
+    const int keep = pipe.keep;
+    const uint64_t pol = policy_evict_first(), pol_keep = policy_evict_last();
+    int ps = pipe.ps, pj = pipe.pj;
+    const unsigned char* pxs = xfirst + (int64_t)pj * xstep;
+    auto issue = [&]() {
+      if (lane == 0) {
+        uint64_t* bar = bars + ps;
+        unsigned char* dst = ts_dyn_smem + ring_off + (uint32_t)(ps * stage_bytes);
+        mbar_expect_tx(bar, tb);
+        bulk_g2s(dst, pxs, tb, bar, pj < keep ? pol_keep : pol);
+      }
+      if (++ps == nstage) ps = 0;
+      if (++pj == count) { pj = 0; pxs = xfirst; }
+      else pxs += xstep;
+    };
+    while (issued < c0 + (unsigned long long)nstage) { issue(); ++issued; }
+    int s = pipe.cs, tj = pipe.ctj;
+    uint32_t parity = (uint32_t)pipe.cpar;
+    if (prof) { pc1 = clock64(); a.prof[4] += pc1 - pc0; pc0 = pc1; }
+    for (int j = 0; j < count; ++j) {
+      mbar_wait(bars + s, parity);
+      const unsigned char* sb = ts_dyn_smem + ring_off + (uint32_t)(s * stage_bytes);
+      double x[KX];
+#pragma unroll
+      for (int g = 0; g < KX / 2; ++g) {
+        if (HE > 0 || g < G) {
+          const double2 v = reinterpret_cast<const double2*>(sb)[g * 32 + lane];
+          x[2 * g] = v.x; x[2 * g + 1] = v.y;
+        } else {
+          x[2 * g] = 0.0; x[2 * g + 1] = 0.0;
+        }
+      }
+      const double yv = (double)sb[512 * G + r];
+      __syncwarp();
+      issue();
+      ++issued;
+      const int t = tfirst + tj * tstride;
+      const bool valid = r < (t < nfull ? 16 : rem);
+      if (++s == nstage) { s = 0; parity ^= 1u; }
+      if (++tj == count) tj = 0;
+      double e0 = 0.0, e1 = 0.0, e2 = 0.0, e3 = 0.0;
+#pragma unroll
+      for (int k = 0; k < KX; k += 4) {
+        e0 = __fma_rn(x[k], th[k], e0);
+        if (k + 1 < KX) e1 = __fma_rn(x[k + 1], th[k + 1], e1);
+        if (k + 2 < KX) e2 = __fma_rn(x[k + 2], th[k + 2], e2);
+        if (k + 3 < KX) e3 = __fma_rn(x[k + 3], th[k + 3], e3);
+      }
+      const double part = (e0 + e1) + (e2 + e3);
+      const double other = __shfl_xor_sync(0xffffffffu, part, 16);
+      // the same association in both halves: (lower + upper) + bias
+      const double eta = (h ? other + part : part + other) + thb;
+      const double e = exp(-fabs(eta));
+      const double l = fmax(eta, 0.0) + log1p(e);
+      const double sig = __ddiv_rn(eta >= 0.0 ? 1.0 : e, 1.0 + e);
+      const double resid = valid ? yv - sig : 0.0;
+      if (h == 0) {
+        accl += valid ? (yv * eta - l) : 0.0;
+        accb += resid;
+      }
+#pragma unroll
+      for (int k = 0; k < KX; ++k) acc[k] = __fma_rn(resid, x[k], acc[k]);
+    }
+    __syncwarp();
+    if (lane == 0) {
+      pipe.consumed = c0 + (unsigned long long)count;
+      pipe.issued = issued;
+      pipe.cs = s; pipe.cpar = (int)parity; pipe.ctj = tj;
+      pipe.ps = ps; pipe.pj = pj;
+    }
+    __syncwarp();
+  }
+  if (prof) { pc1 = clock64(); a.prof[5] += pc1 - pc0; pc0 = pc1; }
+  // sums over the 16 rows of each half (fixed shuffle tree), lane 0 / 16 write
+#pragma unroll
+  for (int k = 0; k < KX; ++k) {
+    double v = acc[k];
+#pragma unroll
+    for (int off = 8; off >= 1; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    if (r == 0 && k < H && f0 + k < p) wred[warp * NA + f0 + k] = v;
+  }
+#pragma unroll
+  for (int off = 8; off >= 1; off >>= 1) {
+    accb += __shfl_xor_sync(0xffffffffu, accb, off);
+    accl += __shfl_xor_sync(0xffffffffu, accl, off);
+  }
+  if (lane == 0) { wred[warp * NA + kX64hPmax] = accb; wred[warp * NA + kX64hPmax + 1] = accl; }
+  if (prof) { pc1 = clock64(); a.prof[6] += pc1 - pc0; pc0 = pc1; }
+  wk_sync();
+  for (int d = wk_tid(); d < p + 2; d += wk_threads()) {
+    const int jj = (d < p) ? d : (d == p ? kX64hPmax : kX64hPmax + 1);
+    double sum = 0.0;
+    for (int w = 0; w < nwarps; ++w) sum += wred[w * NA + jj];
+    red_out[d] = sum;
+  }
+  if (prof) { pc1 = clock64(); a.prof[7] += pc1 - pc0; }
+}
+
 // ---------------------------------------------------------------- wide p
 // p in (64, kWideMax]: a tile is kWideRows = 8 rows in the input's row-major
 // order followed by 16 bytes holding the 8 labels (+ 8 zero bytes): one TMA
@@ -973,6 +1128,11 @@ __device__ __noinline__ void logistic_cta_pass_wide(const LogisticArgs& a, const
 
 static __device__ __forceinline__ void logistic_cta_dispatch(const LogisticArgs& a, const double* theta, double* wred,
                                                              double* red_s) {
+  if (a.xh) {  // fp64 storage, p <= 64
+    if (a.p == 54) logistic_cta_pass_x64h<27>(a, theta, wred, red_s);
+    else logistic_cta_pass_x64h<0>(a, theta, wred, red_s);
+    return;
+  }
   if (a.wide) {
     if (a.xd) {  // fp64 X storage (always the fp64 policy)
       if (a.p <= 64) logistic_cta_pass_wide<true, 2, 0, true>(a, theta, wred, red_s);

@@ -664,6 +664,59 @@ def test_dense_many_chains_tf32_vs_fp64():
     assert np.nanmax(rhat) < 1.05
 
 
+def test_dense_tf32_decision_flips(oracle):
+    """Config-4 TF32 decisions counted against fp64 (north star: "acceptance
+    decisions checked against FP32"): 1008 transitions of
+    an fp64 run (16 chains x 63 post-warmup states) are replayed from the same
+    (q, key, step) by the TF32 tensor-core path and the fp64 SIMT path; the
+    integer decisions (depth, leapfrogs, divergence, per-tree direction /
+    count / stop, proposal) are compared.  Bound: <= 2% flips, each at a
+    near-tie of the oracle's decision margins (<= 5e-3: TF32 keeps 10
+    mantissa bits, the stated gradient tolerance is 2e-3 relative, so energy
+    errors of ~1e-3 move a multinomial / accept probability by about that
+    much; measured: 6 flips of 1008, margins 1.0e-4 .. 2.0e-3)."""
+    import json
+
+    t = ts()
+    D, C, W, S = 64, 16, 150, 64
+    A = _spd(D, 21, cond=30.0)
+    om = oracle.Model("dense_gaussian", D, dense_a=A.tolist())
+    m64 = t.dense_gaussian_model(A, precision="fp64")
+    m32 = t.dense_gaussian_model(A, precision="tf32")
+    cfg = t.RunConfig(model={}, num_chains=C, num_warmup=W, num_samples=S, seed=23)
+    keys = t.chain_keys(23, C)
+    r = t.run_device(m64, cfg, keys, 0)
+    samples = r.samples.cpu().numpy()
+    adapt = r.adapt.cpu().numpy()
+    flips, n = [], 0
+    for c in range(C):
+        step = float(adapt[c, 1])
+        scfg = t.SamplerConfig(step_size=step, mass=t.MassMatrix.identity(D))
+        for i in range(1, S):
+            q0 = samples[c, i - 1]
+            dkey = keys[c].fold(10 + W + i)
+            dec = {}
+            for prec, m in (("fp64", m64), ("tf32", m32)):
+                ug = t.models.potential_and_gradient(m.device_spec, q0[None, :])[0]
+                z = t.PhasePoint(q0, np.zeros(D), float(ug[0]), ug[1:].copy())
+                _, st, tr = t.nuts_transition_from(z, scfg, m, dkey, return_trace=True)
+                dec[prec] = (st.depth_reached, st.leapfrog_calls, int(st.diverged),
+                             tuple((j, gr, cc, stp) for j, cc, stp, gr, _ in tr.trees), (tr.proposal_tree, tr.proposal_leaf))
+            n += 1
+            if dec["tf32"] != dec["fp64"]:
+                margins = []
+                oracle.transition(oracle.Point(q0.tolist(), [0.0] * D, om.potential(q0.tolist()), om.gradient(q0.tolist())),
+                                  step, [1.0] * D, om, (dkey.hi, dkey.lo), margins=margins)
+                mrg = min((mm for tm in margins for mm in tm), key=lambda km: km[1], default=("none", math.inf))
+                flips.append({"chain": c, "draw": i, "kind": mrg[0], "min_margin": mrg[1],
+                              "tf32": dec["tf32"][:3], "fp64": dec["fp64"][:3]})
+    print("dense tf32 decision replay:", json.dumps({"replayed": n, "flips": len(flips), "flip_rate": len(flips) / n,
+                                                      "flip_log": flips}))
+    assert n == 1008
+    assert len(flips) <= 0.02 * n, flips
+    assert all(f["min_margin"] <= 5e-3 for f in flips), flips
+
+
 def test_dense_mass_reparametrisation():
     """Dense inverse mass M^-1 = Sigma: the sampler runs on x = L^-1 q and
     returns q; moments match Sigma."""
@@ -870,7 +923,7 @@ def test_dense_mass_adaptation_two_phase():
 # ----------------------------------------------------------------------------- fp64 X storage ("fp64x")
 
 
-@pytest.mark.parametrize("n,p", [(3000, 54), (1001, 7), (517, 100), (2000, 255)])
+@pytest.mark.parametrize("n,p", [(3000, 54), (1001, 7), (700, 63), (50, 1), (517, 100), (2000, 255)])
 def test_fp64x_non_fp32_exact_data(n, p, oracle):
     """Data that are not fp32-exact are stored in fp64 (the reference keeps
     fp64 X, models.py:43-64): precision "fp64" selects the fp64-storage pass

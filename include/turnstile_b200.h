@@ -208,6 +208,12 @@ int ts_gemm_tf32_probe(const float* a_dev, const float* xt_dev, float* gt_dev, i
  * words [n][2].  Replaces nothing in the reference; used by tests. */
 int ts_rng_probe(uint64_t key_hi, uint64_t key_lo, int kind, int n, double* out_dev, void* stream);
 
+/* Test probe: y = exp(x) (kind 0), log1p(x) (1) or log(x) (2) as the device
+ * engine evaluates them (csrc/ts_libm.cuh: glibc's exp and log1p bit for bit,
+ * log correctly rounded), the functions the reference calls through math at
+ * tree.py:131-156, 276, 410-416, sampler.py:127, adapt.py:44-57, 192. */
+int ts_libm_probe(int kind, const double* x_dev, double* y_dev, int64_t n, void* stream);
+
 /* Pooled sample covariance of n_rows draws (row-major n_rows x D fp64 in
  * device memory, e.g. the (C, S, D) samples of a many-chain warmup pooled
  * over chains): mean_dev[D] and cov_dev[D*D] with ddof = 1; regularize != 0

@@ -630,6 +630,19 @@ __global__ void k_rng_probe(uint64_t hi, uint64_t lo, int kind, int n, double* o
   }
 }
 
+// glibc-exact exp / log1p and the correctly rounded log of the engine (ts_libm.cuh)
+__global__ void k_libm_probe(int kind, const double* __restrict__ x, double* __restrict__ y, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = kind == 0 ? ts::lm_exp(x[i]) : (kind == 1 ? ts::lm_log1p(x[i]) : ts::lm_log(x[i]));
+}
+extern "C" int ts_libm_probe(int kind, const double* x_dev, double* y_dev, int64_t n, void* stream) {
+  if (!x_dev || !y_dev || n < 0 || kind < 0 || kind > 2) return set_err(TS_EINVAL, "bad libm probe arguments");
+  if (n == 0) return TS_OK;
+  k_libm_probe<<<592, 256, 0, (cudaStream_t)stream>>>(kind, x_dev, y_dev, n);
+  TS_CUDA(cudaGetLastError());
+  return TS_OK;
+}
+
 extern "C" int ts_rng_probe(uint64_t key_hi, uint64_t key_lo, int kind, int n, double* out_dev, void* stream) {
   if (!out_dev || n < 0 || kind < 0 || kind > 2) return set_err(TS_EINVAL, "bad rng probe arguments");
   k_rng_probe<<<1, 32, 0, (cudaStream_t)stream>>>(key_hi, key_lo, kind, n, out_dev);

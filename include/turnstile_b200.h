@@ -226,6 +226,13 @@ int ts_pooled_covariance(const double* x_dev, int64_t n_rows, int D, int regular
                          double* cov_dev, double* work_dev, void* stream);
 int64_t ts_pooled_covariance_workspace(int64_t n_rows, int D);
 
+/* Dense-mass reparametrisation: the run
+ * samples x = L^-1 q (M^-1 = L L^T); this maps every draw back,
+ * q_dev[r] = L x_dev[r] for r < rows (row-major [rows][dim], L lower
+ * triangular [dim][dim], fp64, not in place).  Replaces the reference's
+ * nothing (its mass is diagonal, integrator.py:21-31). */
+int ts_dense_transform(const double* l_dev, const double* x_dev, double* q_dev, int64_t rows, int dim, void* stream);
+
 /* Replaces diagnostics.ess (diagnostics.py:49-86) and diagnostics.split_rhat
  * (diagnostics.py:89-105) for samples already in device memory: samples_dev
  * (n_chains, n_draws, dim) fp64 C-contiguous -> ess_dev[dim], rhat_dev[dim]

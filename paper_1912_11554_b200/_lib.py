@@ -42,6 +42,7 @@ EXPORTS = (
     "ts_run_chains",
     "ts_rng_probe",
     "ts_libm_probe",
+    "ts_dense_transform",
     "ts_peer_mailbox_create",
     "ts_peer_mailbox_connect",
     "ts_logistic_partial_sums",
@@ -104,6 +105,7 @@ def _declare(lib):
     lib.ts_run_chains.argtypes = [_P, ctypes.POINTER(RunCfgC), _P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _I, _P]
     lib.ts_rng_probe.argtypes = [_U64, _U64, _I, _I, _P, _P]
     lib.ts_libm_probe.argtypes = [_I, _P, _P, ctypes.c_int64, _P]
+    lib.ts_dense_transform.argtypes = [_P, _P, _P, ctypes.c_int64, _I, _P]
     lib.ts_peer_mailbox_create.argtypes = [_P, _I, _I, _P]
     lib.ts_peer_mailbox_connect.argtypes = [_P, _P]
     lib.ts_logistic_partial_sums.argtypes = [_P, _P, _P, _P]

@@ -174,9 +174,12 @@ def run_device(model: TargetModel, config: RunConfig, keys: Sequence[RngKey], de
                                      _lib.ptr(samples), _lib.ptr(stats), _lib.ptr(adapt), _lib.ptr(status), _lib.ptr(evals),
                                      exec_mode_for(model, exec_mode), _lib.stream_ptr(torch)))
         t1.record()
-        if spec.reparam is not None:  # x -> q = L x (dense mass reparametrisation)
-            Lt = torch.from_numpy(np.ascontiguousarray(spec.reparam.T)).to(dev)
-            samples = torch.matmul(samples, Lt)
+        if spec.reparam is not None:  # x -> q = L x (dense mass reparametrisation), ts_dense_transform
+            Ld = torch.from_numpy(np.ascontiguousarray(spec.reparam)).to(dev)
+            q = torch.empty_like(samples)
+            _lib.check(lib.ts_dense_transform(_lib.ptr(Ld), _lib.ptr(samples), _lib.ptr(q), samples.numel() // D, D,
+                                              _lib.stream_ptr(torch)))
+            samples = q
         ms = None
         if sync:
             t1.synchronize()

@@ -322,19 +322,21 @@ struct Stats {
 __device__ __forceinline__ double kInf() { return __longlong_as_double(0x7ff0000000000000LL); }
 
 // tree._logaddexp (tree.py:131-137)
+template <bool EXACT>
 __device__ __forceinline__ double logaddexp_inner(double a, double b) {
   if (a == -kInf()) return b;
   if (b == -kInf()) return a;
   double hi = a, lo = b;
   if (!(a >= b)) { hi = b; lo = a; }
-  return __dadd_rn(hi, lm_log1p(lm_exp(__dsub_rn(lo, hi))));
+  return __dadd_rn(hi, x_log1p<EXACT>(x_exp<EXACT>(__dsub_rn(lo, hi))));
 }
 // numpy npy_logaddexp (used at sampler.py:129)
+template <bool EXACT>
 __device__ __forceinline__ double logaddexp_np(double x, double y) {
   if (x == y) return __dadd_rn(x, 0.693147180559945309417232121458176568);
   const double tmp = __dsub_rn(x, y);
-  if (tmp > 0) return __dadd_rn(x, lm_log1p(lm_exp(-tmp)));
-  if (tmp <= 0) return __dadd_rn(y, lm_log1p(lm_exp(tmp)));
+  if (tmp > 0) return __dadd_rn(x, x_log1p<EXACT>(x_exp<EXACT>(-tmp)));
+  if (tmp <= 0) return __dadd_rn(y, x_log1p<EXACT>(x_exp<EXACT>(tmp)));
   return tmp;
 }
 
@@ -579,8 +581,8 @@ struct Engine {
   // running = _merge(summaries[s], running, u)   (tree.py:140-156)
   __device__ void merge_slot(int s, double u) {
     const SlotScalars& L = ss[s];
-    const double lw = logaddexp_inner(L.lw, r_lw);
-    const double p_right = (r_lw == -kInf()) ? 0.0 : lm_exp(__dsub_rn(r_lw, lw));
+    const double lw = logaddexp_inner<Team::kExactMath>(L.lw, r_lw);
+    const double p_right = (r_lw == -kInf()) ? 0.0 : x_exp<Team::kExactMath>(__dsub_rn(r_lw, lw));
     if (!(u < p_right)) {
       copy_group(V_TPQ, slot_vec(s, 3), V_TPG, slot_vec(s, 4), V_TPG, slot_vec(s, 4));
       r_pU = L.pU; r_pH = L.pH; r_pidx = L.pidx;
@@ -750,14 +752,14 @@ struct Engine {
     const double thr = cfg.threshold;
     const int pc = __popcll(n);
     if (!(isfinite(delta) && delta <= thr)) {
-      const double metro = isfinite(delta) ? lm_exp(-delta) : 0.0;
+      const double metro = isfinite(delta) ? x_exp<Team::kExactMath>(-delta) : 0.0;
       ev_lw(-kInf());
       running_from_leaf((int)n, -kInf(), metro, h);
       merge_out(pc, draws);
       return kStopDiv;
     }
     const double lw = -h;
-    const double metro = delta > 0 ? lm_exp(-delta) : 1.0;
+    const double metro = delta > 0 ? x_exp<Team::kExactMath>(-delta) : 1.0;
     ev_lw(lw);
     if ((n & 1ULL) == 0) {
       const int slot = pc;
@@ -825,7 +827,7 @@ struct Engine {
       leaf_energy(h_ref, h, delta);
       const bool div = !isfinite(delta) || delta > thr;
       const double lw = div ? -kInf() : -h;
-      const double metro = !isfinite(delta) ? 0.0 : (delta > 0 ? lm_exp(-delta) : 1.0);
+      const double metro = !isfinite(delta) ? 0.0 : (delta > 0 ? x_exp<Team::kExactMath>(-delta) : 1.0);
       ev_lw(lw);
       running_from_leaf(0, lw, metro, h);
       stop = div ? kStopDiv : kStopNone;
@@ -1070,7 +1072,7 @@ struct Engine {
     }
     const double h1 = hamiltonian(cur_U, V_CR);
     const double delta = __dsub_rn(h1, h0);
-    const double p_accept = (isfinite(delta) && delta > 0) ? lm_exp(-delta) : (isfinite(delta) ? 1.0 : 0.0);
+    const double p_accept = (isfinite(delta) && delta > 0) ? x_exp<Team::kExactMath>(-delta) : (isfinite(delta) ? 1.0 : 0.0);
     Stream gen;
     gen.init(key_fold(key, 1));
     accepted = gen.next_double() < p_accept;
@@ -1134,12 +1136,12 @@ struct Engine {
         break;
       }
       const double u = gen.next_double();
-      const bool take = (t.lw >= lw) || (u < lm_exp(__dsub_rn(t.lw, lw)));
+      const bool take = (t.lw >= lw) || (u < x_exp<Team::kExactMath>(__dsub_rn(t.lw, lw)));
       if (take) {
         copy_group(V_PQ, V_TPQ, V_PG, V_TPG, V_PG, V_TPG); pU = t.pU; pH = t.pH; p_tree = j; p_leaf = t.pidx;
       }
       ev(kEvProposal, j, t.pidx, take ? 1 : 0);
-      lw = logaddexp_np(lw, t.lw);
+      lw = logaddexp_np<Team::kExactMath>(lw, t.lw);
       {
         double* rho = v(V_RHO);
         const double* ms = v(V_MSUM);
@@ -1180,7 +1182,7 @@ struct Engine {
     const double h1 = hamiltonian(cur_U, V_CR);
     if (!isfinite(h1)) return 0.0;
     const double x = __dsub_rn(h0, h1);
-    return lm_exp(x < 0.0 ? x : 0.0);
+    return x_exp<Team::kExactMath>(x < 0.0 ? x : 0.0);
   }
   // find_reasonable_step_size (adapt.py:172-204); z0 in Q0/G0/U0
   __device__ __noinline__ double find_step_size(Key key, double init, const double* inj, int64_t inj_ds) {
@@ -1248,14 +1250,14 @@ __device__ void run_chain(Engine<Team, Model>& E, Key ck, const RunCfg& rc, cons
     const double eps0 = E.find_step_size(key_fold(ck, 1), rc.base_step, nullptr, 0);
     if (writer && E.T.leader()) out.adapt[0] = eps0;
     // DualAveragingState.init (adapt.py:44-50)
-    const double mu = lm_log(__dmul_rn(10.0, eps0));
-    double log_eps = lm_log(eps0), log_eps_bar = 0.0, h_bar = 0.0;
+    const double mu = x_log<Team::kExactMath>(__dmul_rn(10.0, eps0));
+    double log_eps = x_log<Team::kExactMath>(eps0), log_eps_bar = 0.0, h_bar = 0.0;
     const double gamma = 0.05, t0 = 10.0, delta = rc.target_accept;
     int wcount = 0;
     E.fill(V_WMEAN, 0.0);
     E.fill(V_WM2, 0.0);
     for (int i = 0; i < W; ++i) {
-      E.cfg.step = lm_exp(log_eps);
+      E.cfg.step = x_exp<Team::kExactMath>(log_eps);
       if (writer && E.T.leader()) out.adapt[2 + i] = E.cfg.step;
       const Stats st = E.transition(key_fold(ck, 10 + (uint64_t)i), nullptr, 0);
       if (writer && E.T.leader()) {
@@ -1309,7 +1311,7 @@ __device__ void run_chain(Engine<Team, Model>& E, Key ck, const RunCfg& rc, cons
         E.refresh_mstd();
       }
     }
-    step = lm_exp(log_eps_bar);
+    step = x_exp<Team::kExactMath>(log_eps_bar);
   } else {
     step = rc.base_step;
     if (!rc.has_sampler) step = E.find_step_size(key_fold(ck, 1), 1.0, nullptr, 0);

@@ -184,3 +184,72 @@ extern "C" int64_t ts_pooled_covariance_workspace(int64_t n_rows, int D) {
   const int nt = (D + kTile - 1) / kTile;
   return (int64_t)kChunks * D + (int64_t)cov_splits(n_rows, D) * (nt * (nt + 1) / 2) * kTile * kTile;
 }
+
+// ---------------------------------------------------------------- dense mass: q = L x
+// Samples of the reparametrised dense-mass run come back as q = L x
+// (chains.run_device; L lower triangular, M^-1 = L L^T).  Q (rows x D) =
+// X (rows x D) . L^T: 64 x 64 output tiles per CTA (256 threads, 4 x 4 each),
+// k in chunks of 16 through shared memory, fp64 FMAs in k order; the upper
+// triangle of L (zeros) is skipped by the k range of each column block.
+namespace {
+constexpr int kTB = 64, kTK = 16;
+__global__ void __launch_bounds__(256) k_lower_transform(const double* __restrict__ L, const double* __restrict__ X,
+                                                         double* __restrict__ Q, int64_t rows, int D) {
+  __shared__ double xs[kTK][kTB + 1];  // [k][row]
+  __shared__ double ls[kTK][kTB + 1];  // [k][col]
+  const int64_t r0 = (int64_t)blockIdx.x * kTB;
+  const int c0 = blockIdx.y * kTB;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  double acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+  // columns c0 .. c0+63 of Q need L[c][k] for k <= c < c0 + 64
+  const int kend = (c0 + kTB < D) ? c0 + kTB : D;
+  for (int k0 = 0; k0 < kend; k0 += kTK) {
+    for (int i = threadIdx.x; i < kTK * kTB; i += 256) {
+      const int kk = i % kTK, rr = i / kTK;
+      const int64_t row = r0 + rr;
+      const int k = k0 + kk;
+      xs[kk][rr] = (row < rows && k < D) ? X[row * D + k] : 0.0;
+      const int col = c0 + rr;
+      ls[kk][rr] = (col < D && k < D && k <= col) ? L[(int64_t)col * D + k] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < kTK; ++kk) {
+      double a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) { a[i] = xs[kk][ty * 4 + i]; b[i] = ls[kk][tx * 4 + i]; }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = __fma_rn(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t row = r0 + ty * 4 + i;
+    if (row >= rows) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int col = c0 + tx * 4 + j;
+      if (col < D) Q[row * D + col] = acc[i][j];
+    }
+  }
+}
+}  // namespace
+
+extern "C" int ts_dense_transform(const double* l_dev, const double* x_dev, double* q_dev, int64_t rows, int dim,
+                                  void* stream) {
+  using ts_internal::set_err;
+  if (!l_dev || !x_dev || !q_dev || rows < 0 || dim < 1) return set_err(TS_EINVAL, "bad dense transform arguments");
+  if (x_dev == q_dev) return set_err(TS_EINVAL, "dense transform cannot run in place");
+  if (rows == 0) return TS_OK;
+  const dim3 grid((unsigned)((rows + kTB - 1) / kTB), (unsigned)((dim + kTB - 1) / kTB));
+  k_lower_transform<<<grid, 256, 0, (cudaStream_t)stream>>>(l_dev, x_dev, q_dev, rows, dim);
+  TS_CUDA(cudaGetLastError());
+  return TS_OK;
+}

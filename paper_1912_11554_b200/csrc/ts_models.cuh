@@ -59,7 +59,7 @@ __device__ double small_model_eval(const Team& T, const SmallModel& m, const Vec
     case kFunnel: {
       // U = v*v/18 + 0.5*(D-1)*v + 0.5*exp(-v)*ssq ; ssq = sum_{i>=1} q_i^2
       const double v = q[0];
-      const double inv_scale = lm_exp(-v);
+      const double inv_scale = x_exp<Team::kExactMath>(-v);
       double ssq = 0.0;
       for (int d = T.rank(); d < D; d += T.size()) {
         if (d == 0) continue;
@@ -82,7 +82,7 @@ __device__ double small_model_eval(const Team& T, const SmallModel& m, const Vec
       const double* y = m.params;
       const double* sg = m.params + J;
       const double mu = q[0], lt = q[ds];
-      const double tau = lm_exp(lt);
+      const double tau = x_exp<Team::kExactMath>(lt);
       const double s = __ddiv_rn(tau, 5.0);
       const double s2 = __dmul_rn(s, s);
       double ulik = 0.0, smu = 0.0, slt = 0.0;
@@ -105,7 +105,7 @@ __device__ double small_model_eval(const Team& T, const SmallModel& m, const Vec
         g[0] = __dsub_rn(__ddiv_rn(mu, 25.0), smu);
         g[ds] = __dsub_rn(__dsub_rn(__ddiv_rn(__dmul_rn(2.0, s2), __dadd_rn(1.0, s2)), 1.0), slt);
       }
-      const double prior = __dsub_rn(__dadd_rn(__ddiv_rn(__dmul_rn(mu, mu), 50.0), lm_log1p(s2)), lt);
+      const double prior = __dsub_rn(__dadd_rn(__ddiv_rn(__dmul_rn(mu, mu), 50.0), x_log1p<Team::kExactMath>(s2)), lt);
       return __dadd_rn(prior, ulik);
     }
     default:

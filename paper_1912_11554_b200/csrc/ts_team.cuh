@@ -38,6 +38,11 @@ struct VecStore {
 };
 
 struct ThreadTeam {
+  // exp / log1p / log with glibc's results (ts_libm.cuh): the thread team
+  // keeps the reference's operation order, so whole chains are bitwise the
+  // reference's; the warp / CTA teams reduce in another order anyway and use
+  // CUDA's functions (1 ulp, faster)
+  static constexpr bool kExactMath = true;
   static constexpr bool kBlock = false;
   static constexpr bool kUnitStride = false;  // chains interleaved in global memory
   static constexpr bool kWarp = false;
@@ -53,6 +58,7 @@ struct ThreadTeam {
 // reductions are shuffle trees to lane 0 plus a broadcast, so every lane
 // holds the bitwise-identical value and no CTA barrier is involved.
 struct WarpTeam {
+  static constexpr bool kExactMath = false;
   static constexpr bool kBlock = false;
   static constexpr bool kUnitStride = true;  // vectors contiguous in shared memory
   static constexpr bool kWarp = true;
@@ -78,6 +84,7 @@ struct WarpTeam {
 
 // Deterministic CTA-wide reduction.  `scratch` holds >= 2*32 doubles.
 struct BlockTeam {
+  static constexpr bool kExactMath = false;
   static constexpr bool kBlock = true;
   static constexpr bool kUnitStride = true;
   static constexpr bool kWarp = false;

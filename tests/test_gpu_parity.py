@@ -762,6 +762,23 @@ def test_dense_tf32_decision_flips(oracle):
     assert all(f["min_margin"] <= 5e-3 for f in flips), flips
 
 
+@pytest.mark.parametrize("rows,D", [(1, 1), (130, 100), (1000, 1000)])
+def test_dense_transform_matches_numpy(rows, D):
+    """ts_dense_transform (q = L x per draw, the dense-mass sample map) vs numpy."""
+    import torch
+
+    t = ts()
+    lib = t._lib.load_library()
+    rng = np.random.default_rng(rows + D)
+    L = np.tril(rng.standard_normal((D, D)))
+    x = rng.standard_normal((rows, D))
+    Ld, xd = torch.from_numpy(L).cuda(), torch.from_numpy(x).cuda()
+    qd = torch.empty_like(xd)
+    t._lib.check(lib.ts_dense_transform(Ld.data_ptr(), xd.data_ptr(), qd.data_ptr(), rows, D, 0))
+    ref = x @ L.T
+    assert close(qd.cpu().numpy(), ref, 1e-11, atol=1e-11 * np.abs(ref).max())
+
+
 def test_dense_mass_reparametrisation():
     """Dense inverse mass M^-1 = Sigma: the sampler runs on x = L^-1 q and
     returns q; moments match Sigma."""

@@ -509,6 +509,40 @@ def test_covtype_transitions_match_oracle(oracle):
         assert np.array_equal(z1.position, samples[i])  # the run's own draw
 
 
+@pytest.mark.parametrize("eps,max_depth", [(0.02, 10), (0.3, 10), (3.0, 6), (0.05, 1), (0.05, 2)])
+def test_logistic_trajectory_stops_match_oracle(eps, max_depth, oracle):
+    """Worker-run trajectories (LogisticW::serve_traj) under every way a
+    doubling ends: U-turns mid-tree (the speculative leaf is discarded),
+    divergences (large eps), the depth cap, depth-1/2 trees.  Per-tree
+    integers (direction, leapfrogs, stop kind), outer checks, proposal and
+    positions against the CPU oracle, and a second call with the same key
+    repeats the first bit for bit (the launch leaves no state behind)."""
+    t = ts()
+    from tests_data import logistic_data
+
+    x, y = logistic_data(3000, 54, 77)
+    m = t.logistic_regression_model(t.LogisticRegressionData(x, y), precision="fp64")
+    om = oracle.Model("logistic_regression", 55, x=x, y=y)
+    rng = np.random.default_rng(int(eps * 1000) + max_depth)
+    cfg = t.SamplerConfig(step_size=eps, mass=t.MassMatrix.identity(55), max_tree_depth=max_depth)
+    for case in range(6):
+        q0 = rng.standard_normal(55) * 0.1
+        U0, g0 = om.potential(q0.tolist()), om.gradient(q0.tolist())
+        z = t.PhasePoint(q0, np.zeros(55), U0, np.asarray(g0))
+        key = t.RngKey.from_seed(1000 + case)
+        z1, st, tr = t.nuts_transition_from(z, cfg, m, key, return_trace=True)
+        z2, st2, _ = t.nuts_transition_from(z, cfg, m, key, return_trace=True)
+        assert np.array_equal(z1.position, z2.position) and st == st2
+        oz, ost, dec = oracle.transition(oracle.Point(q0.tolist(), [0.0] * 55, U0, g0), eps, [1.0] * 55, om,
+                                         (key.hi, key.lo), max_depth=max_depth)
+        got = (st.depth_reached, st.leapfrog_calls, int(st.diverged),
+               tuple((j, gr, c, stp) for j, c, stp, gr, _ in tr.trees), (tr.proposal_tree, tr.proposal_leaf))
+        want = (ost.depth, ost.leapfrogs, int(ost.diverged),
+                tuple((j, d, c, tu + 2 * dv) for j, d, c, tu, dv, _ in dec["trees"]), tuple(dec["proposal"]))
+        assert got == want, (eps, max_depth, case, got, want)
+        assert close(z1.position, oz.q, 1e-10, atol=1e-12)
+
+
 @pytest.mark.parametrize("precision,rel", [("fp64", 1e-11), ("fp32", FP32_REL)])
 def test_covtype_shape_potential_gradient(precision, rel, oracle):
     """Full BASELINE config-2 size (581,012 x 54) against the C oracle."""

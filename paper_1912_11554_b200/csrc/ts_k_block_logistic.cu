@@ -27,6 +27,9 @@ int launch_block_logistic(const ts_model* m, int nslots, OpArgs& A, cudaStream_t
   mw.a.err = m->errw;
   mw.a.spin_ns = spin_limit_ns();
   if (const char* e = getenv("TS_FAULT_INJECT")) mw.a.fault = atoi(e);  // tests of the bounded waits only
+  // cross-CTA accumulator copies (8: fewer same-address atomics; TS_FX_COPIES=1/2/4/8 for A/B)
+  mw.a.fxc = kFxCopies;
+  if (const char* e = getenv("TS_FX_COPIES")) { const int c = atoi(e); mw.a.fxc = (c == 1 || c == 2 || c == 4) ? c : kFxCopies; }
   mw.a.llmode = 6;
   if (const char* e = getenv("TS_LLMODE")) mw.a.llmode = atoi(e);  // A/B of the fp32 log-likelihood precision
   // fp64 wide pass: half of the fp32->fp64 conversions on the integer pipe

@@ -94,6 +94,7 @@ struct LogisticArgs {
   int llmode;                      // FP32 narrow pass: log-likelihood term precision (logistic_cta_pass LL)
   int xd;                          // X stored as fp64 (wide layout, logistic_cta_pass_wide XD)
   const double* thd;  // FP64 narrow pass: theta as doubles [pmax + 1], zero-padded, 16-B aligned (smem, written by the driver)
+  int fxc;            // cross-CTA accumulator copies in use (1..kFxCopies)
   int xh;                          // X stored as fp64 in the 16-row half-row layout (p <= 64, logistic_cta_pass_x64h)
 };
 
@@ -1214,12 +1215,14 @@ static __device__ void logistic_eval_grid(const LogisticArgs& a, const double* t
   const int64_t bstride = 2 * (int64_t)P2 + 2;  // words of one set of totals (mailbox slots)
   const int64_t cstride = fx_copy_stride(p), bufw = fx_buf_words(p);
   unsigned long long* const curb = accb + (int64_t)(epoch % 3ULL) * bufw;  // this pass's buffer
-  unsigned long long* cur = curb + (int64_t)(a.cta % kFxCopies) * cstride;  // this CTA's copy
+  const int ncopy = a.fxc;  // copies in use (<= kFxCopies; buffers are sized for kFxCopies)
+  unsigned long long* cur = curb + (int64_t)(a.cta % ncopy) * cstride;  // this CTA's copy
   // total of word w over the copies (after the barrier)
   auto total = [&](int w) {
     unsigned long long v = 0;
 #pragma unroll
-    for (int c = 0; c < kFxCopies; ++c) v += __ldcg(curb + c * cstride + w);
+    for (int c = 0; c < kFxCopies; ++c)
+      if (c < ncopy) v += __ldcg(curb + c * cstride + w);
     return v;
   };
   if (a.wide) {  // the wide pass leaves exact fixed-point CTA totals in wred
@@ -1261,9 +1264,10 @@ static __device__ void logistic_eval_grid(const LogisticArgs& a, const double* t
   wk_sync();
   // buffer (epoch+2)%3 was last read before this barrier by every CTA and is
   // next accumulated after the following barrier: CTA 0 clears it now.
-  if (a.cta == 0) {
+  {  // every CTA clears its share (a CTA-0-only clear made CTA 0 the last to start the next pass)
     unsigned long long* nxt = accb + (int64_t)((epoch + 2) % 3ULL) * bufw;
-    for (int i = wk_tid(); i < bufw; i += wk_threads()) nxt[i] = 0ULL;
+    const int64_t used = (int64_t)ncopy * cstride;
+    for (int64_t i = (int64_t)a.cta * wk_threads() + wk_tid(); i < used; i += (int64_t)G * wk_threads()) nxt[i] = 0ULL;
   }
   epoch += 1;
   if (prof) { c1 = clock64(); a.prof[2] += c1 - c0; c0 = c1; }

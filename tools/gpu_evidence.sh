@@ -23,6 +23,4 @@ for prec in fp32 fp64; do
 done
 timeout 900 ncu --set full --clock-control none -k regex:k_dense_op --launch-skip 1 -c 1 -o /tmp/r2_dense -f env DENSE_ONLY_MASS=1 python tools/dense_bench.py tf32 1024 20 10 > gpurun_out/ncu_dense.log 2>&1; echo ncudense=$?
 python tools/ncu_summary.py /tmp/r2_dense.ncu-rep gpurun_out/r2_ncu_dense_raw.json > /dev/null
-timeout 900 ncu --set full --clock-control none -k regex:k_logistic_many -c 1 -o /tmp/r2_many -f python tools/lm_bench.py 256 20 10 > gpurun_out/ncu_many.log 2>&1; echo ncumany=$?
-python tools/ncu_summary.py /tmp/r2_many.ncu-rep gpurun_out/r2_ncu_many_raw.json > /dev/null
 ls -la gpurun_out

@@ -107,10 +107,11 @@ __host__ __device__ inline int64_t mail_words(int p, int world) {
 }
 
 // Cross-CTA accumulators (LogisticArgs::pbuf): 3 rotating buffers per rank;
-// a buffer holds kFxCopies copies of the (p+2) fixed-point pairs + flag, each
-// padded to its own 1-KB block; CTA c adds into copy c % kFxCopies (8x fewer
+// a buffer holds up to kFxCopies copies of the (p+2) fixed-point pairs + flag,
+// each padded to its own 1-KB block; CTA c adds into copy c % fxc (fewer
 // red.adds per address, spread over more L2 slices) and a reader sums the
-// copies (integers: the order does not matter).
+// copies (integers: the order does not matter).  fxc = 2 by default
+// (launch_block_logistic: the read-back grows with the copies).
 constexpr int kFxCopies = 8;
 __host__ __device__ inline int64_t fx_copy_stride(int p) { return (2 * (int64_t)(p + 2) + 2 + 127) / 128 * 128; }
 __host__ __device__ inline int64_t fx_buf_words(int p) { return kFxCopies * fx_copy_stride(p); }

@@ -239,8 +239,8 @@ struct DenseArgs {
   unsigned long long* prof;  // optional (TS_PROF): CTA-0 ns [snapshot+barrier, GEMM, release], steps, busy steps
   unsigned long long* posted;   // [Cpad] (zeroed before launch)
   unsigned long long* served;   // [Cpad]
-  unsigned long long* pending;  // [2][Cpad] request served by step s (slot s & 1; 0 = none)
-  unsigned long long* npend;    // [3] outstanding requests of step s (slot s % 3), [3..6) all-done flags
+  unsigned long long* pending;  // [Cpad] request served by the current step (0 = none)
+  unsigned long long* npend;    // [2] outstanding requests of the step, [2..4) all-done flags (rotating)
   unsigned int* err;            // sticky synchronisation-timeout flag of the model (SpinGuard)
   unsigned long long spin_ns;
 };
@@ -264,7 +264,7 @@ __device__ __forceinline__ void gemm_grid_barrier(unsigned long long* bar, unsig
 
 // SIMT fp64 tile (parity policy): thread = row m, 16 chains at a time, k in
 // order, multiply then add (oracle/turnstile_oracle.py restates it bit for bit)
-__device__ void dense_tile_fp64(const DenseArgs& a, int m0, int n0, const unsigned long long* pend) {
+__device__ void dense_tile_fp64(const DenseArgs& a, int m0, int n0) {
   const int m = m0 + (int)threadIdx.x;
   if (m >= a.D) return;
   const double* arow = a.a64 + (int64_t)m * a.D;
@@ -282,7 +282,7 @@ __device__ void dense_tile_fp64(const DenseArgs& a, int m0, int n0, const unsign
     }
 #pragma unroll
     for (int j = 0; j < 16; ++j)
-      if (j < nmax && __ldcg(pend + n0 + nb + j) != 0ULL) a.gt64[(int64_t)(n0 + nb + j) * a.D + m] = acc[j];
+      if (j < nmax && __ldcg(a.pending + n0 + nb + j) != 0ULL) a.gt64[(int64_t)(n0 + nb + j) * a.D + m] = acc[j];
   }
 }
 
@@ -310,38 +310,26 @@ __global__ void __launch_bounds__(128 + 32 * kDenseCW, 1)
     const bool prof = a.prof != nullptr && blockIdx.x == 0 && t == 0;
     unsigned long long tp0 = 0, tp1 = 0, busy = 0;
     if (prof) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tp0));
-    // One grid barrier per step: the snapshot of the requests served by step
-    // s+1 is taken right after this CTA's GEMM tiles of step s, before the
-    // barrier that ends step s, so that barrier both completes step s's
-    // gradients (release) and publishes step s+1's requests (GEMM).
-    // pending[] alternates between two slots (step s+1's is written while
-    // other CTAs still read step s's), the request counts / exit flags rotate
-    // over three (slot s+2 is cleared after barrier s-1: all its readers are
-    // past it, its writers not yet there).
-    unsigned long long mine = 0;  // request of my_chain served by the current step
-    auto snapshot = [&](int st, unsigned long long floor) -> unsigned long long {
-      unsigned long long m = 0;
+    for (int step = 0;; ++step) {
+      // snapshot: requests outstanding now are served by this step
+      unsigned long long mine = 0;
       if (t < a.cpc) {
         const unsigned long long p = ld_acquire_u64(a.posted + my_chain);
-        m = p > floor ? p : 0ULL;
-        a.pending[(int64_t)(st & 1) * a.Cpad + my_chain] = m;
-        if (m) atomicAdd(a.npend + (st % 3), 1ULL);
+        mine = p > srv ? p : 0ULL;
+        a.pending[my_chain] = mine;
+        if (mine) atomicAdd(a.npend + (step & 1), 1ULL);
       }
       // the exit decision must be the same in every CTA: CTA 0 samples the
       // finished-chain count BEFORE the barrier (chains keep finishing
       // asynchronously, so reading it after the barrier could differ per CTA)
       if (t == 0 && blockIdx.x == 0)
-        a.npend[3 + (st % 3)] = (*reinterpret_cast<volatile int*>(a.done) >= total) ? 1ULL : 0ULL;
-      return m;
-    };
-    mine = snapshot(0, srv);
-    gemm_grid_barrier(a.bar, epoch, a.err, a.spin_ns);
-    for (int step = 0;; ++step) {
+        a.npend[2 + (step & 1)] = (*reinterpret_cast<volatile int*>(a.done) >= total) ? 1ULL : 0ULL;
+      gemm_grid_barrier(a.bar, epoch, a.err, a.spin_ns);
       if (t == 0) {
-        const unsigned long long np = ld_relaxed_u64(a.npend + (step % 3));
-        const bool all_done = ld_relaxed_u64(a.npend + 3 + (step % 3)) != 0ULL;
+        const unsigned long long np = ld_relaxed_u64(a.npend + (step & 1));
+        const bool all_done = ld_relaxed_u64(a.npend + 2 + (step & 1)) != 0ULL;
         *flag = (np == 0ULL && all_done) ? 0 : (np ? 1 : 2);
-        if (blockIdx.x == 0) { a.npend[(step + 2) % 3] = 0ULL; a.npend[3 + (step + 2) % 3] = 0ULL; }
+        if (blockIdx.x == 0) a.npend[(step + 1) & 1] = 0ULL;  // next slot: last read before this barrier
       }
       asm volatile("bar.sync 4, 128;" ::: "memory");
       const int f = *flag;
@@ -351,19 +339,18 @@ __global__ void __launch_bounds__(128 + 32 * kDenseCW, 1)
         a.prof[0] += tp1 - tp0;
         tp0 = tp1;
       }
-      const unsigned long long* pend = a.pending + (int64_t)(step & 1) * a.Cpad;
       if (f == 1) {  // at least one request in the grid
         if (t == 0) asm volatile("fence.proxy.async.global;" ::: "memory");
         for (int tile = blockIdx.x; tile < mt * nt; tile += gridDim.x) {
           const int m0 = (tile % mt) * kUmmaBM, n0 = (tile / mt) * kUmmaBN;
           // skip N-tiles without outstanding requests (uniform over the 128 threads)
           int any = 0;
-          for (int j = t; j < kUmmaBN; j += 128) any |= __ldcg(pend + n0 + j) != 0ULL;
+          for (int j = t; j < kUmmaBN; j += 128) any |= __ldcg(a.pending + n0 + j) != 0ULL;
           any = gemm_sync_or(any);
           if (!any) continue;
-          if (a.fp64) dense_tile_fp64(a, m0, n0, pend);
+          if (a.fp64) dense_tile_fp64(a, m0, n0);
           else
-            g.tile(&tmA, &tmX, m0, n0, nkb, a.gt, a.D, a.D - m0 < kUmmaBM ? a.D - m0 : kUmmaBM, kUmmaBN, pend + n0);
+            g.tile(&tmA, &tmX, m0, n0, nkb, a.gt, a.D, a.D - m0 < kUmmaBM ? a.D - m0 : kUmmaBM, kUmmaBN, a.pending + n0);
         }
         busy += 1;
       }
@@ -372,14 +359,11 @@ __global__ void __launch_bounds__(128 + 32 * kDenseCW, 1)
         a.prof[1] += tp1 - tp0;
         tp0 = tp1;
       }
-      // requests for step s+1: new since the one this step serves
-      const unsigned long long next = snapshot(step + 1, mine > srv ? mine : srv);
-      gemm_grid_barrier(a.bar, epoch, a.err, a.spin_ns);  // step s's tiles written, step s+1's requests visible
+      gemm_grid_barrier(a.bar, epoch, a.err, a.spin_ns);  // all gradient tiles written
       if (t < a.cpc && mine) {
         srv = mine;
         st_release_gpu_u64(a.served + my_chain, mine);
       }
-      mine = next;
       if (prof) {
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tp1));
         a.prof[2] += tp1 - tp0;
@@ -469,7 +453,7 @@ static int launch_dense_chunk(const ts_model* m, int nslots, OpArgs& A, int C, i
   TS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 128 + 32 * kDenseCW, smem));
   if ((int64_t)occ * nsm < grid) return set_err(TS_EUNSUPPORTED, "dense model: too many chains for one co-resident grid");
   // workspaces (grown on demand, owned by the model)
-  const size_t need = (size_t)Cpad * D * (m->fp64 ? 16 : 8) + (size_t)C * nv * D * 8 + 64 + (size_t)Cpad * 32 + 64;  // + flags
+  const size_t need = (size_t)Cpad * D * (m->fp64 ? 16 : 8) + (size_t)C * nv * D * 8 + 64 + (size_t)Cpad * 24 + 64;  // + flags
   if (mm->dws_size < need) {
     if (mm->dws) cudaFree(mm->dws);
     mm->dws = nullptr;
@@ -497,7 +481,7 @@ static int launch_dense_chunk(const ts_model* m, int nslots, OpArgs& A, int C, i
   a.posted = reinterpret_cast<unsigned long long*>(p);
   a.served = a.posted + Cpad;
   a.pending = a.served + Cpad;
-  a.npend = a.pending + 2 * (size_t)Cpad;
+  a.npend = a.pending + Cpad;
   a.a64 = m->params;
   a.err = m->errw;
   a.spin_ns = spin_limit_ns();
@@ -511,7 +495,7 @@ static int launch_dense_chunk(const ts_model* m, int nslots, OpArgs& A, int C, i
     if (rc) return rc;
   }
   TS_CUDA(cudaMemsetAsync(mm->dws, 0, 64, st));
-  TS_CUDA(cudaMemsetAsync(a.posted, 0, ((size_t)Cpad * 4 + 6) * sizeof(unsigned long long), st));
+  TS_CUDA(cudaMemsetAsync(a.posted, 0, ((size_t)Cpad * 3 + 4) * sizeof(unsigned long long), st));
   const bool prof = getenv("TS_PROF") != nullptr;  // profiling aid: CTA-0 step phases to stderr
   if (prof) a.prof = reinterpret_cast<unsigned long long*>(mm->dws + 16);  // 5 words in the zeroed header
   int ns = nslots;
@@ -523,7 +507,7 @@ static int launch_dense_chunk(const ts_model* m, int nslots, OpArgs& A, int C, i
     TS_CUDA(cudaStreamSynchronize(st));
     const double n = h[3] ? (double)h[3] : 1.0;
     fprintf(stderr, "TS_PROF dense steps=%llu (with requests %llu) us/step: snapshot+barrier %.2f  GEMM %.2f  release barrier %.2f\n",
-            h[3], h[4], h[0] / n / 1e3, h[1] / n / 1e3, h[2] / n / 1e3);  // [0]: flag read after the barrier
+            h[3], h[4], h[0] / n / 1e3, h[1] / n / 1e3, h[2] / n / 1e3);
   }
   return TS_OK;
 }

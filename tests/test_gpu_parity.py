@@ -170,6 +170,30 @@ def test_wide_logistic_potential_gradient(p, precision, rel, oracle):
             assert close(got[1:], g, rel, atol=rel * max(1.0, np.abs(g).max())), (n, p, scale)
 
 
+@pytest.mark.parametrize("n", [1, 2, 31, 33])
+@pytest.mark.parametrize("p", [1, 3, 54, 64, 65])
+@pytest.mark.parametrize("precision", ["fp64", "fp32", "fp64x"])
+def test_logistic_ragged_shapes(n, p, precision, oracle):
+    """Ragged and boundary shapes of every logistic layout (a single row, a
+    partial 32-row tile, p at the narrow / wide boundary, odd p for the
+    half-row fp64x tiles): potential and gradient vs the oracle, and a short
+    run (trajectories, adaptation) that stays finite."""
+    t = ts()
+    rng = np.random.default_rng(n * 100 + p)
+    x = rng.standard_normal((n, p)).astype(np.float32).astype(np.float64)
+    y = (rng.random(n) < 0.5).astype(np.float64)
+    m = t.logistic_regression_model(t.LogisticRegressionData(x, y), precision=precision)
+    om = oracle.Model("logistic_regression", p + 1, x=x, y=y)
+    rel = FP32_REL if precision == "fp32" else FP64_REL
+    for q in (np.zeros(p + 1), rng.standard_normal(p + 1) * 0.3):
+        got = t.models.potential_and_gradient(m.device_spec, q[None, :])[0]
+        U, g = om.potential(q.tolist()), np.asarray(om.gradient(q.tolist()))
+        assert close(got[0], U, rel, atol=rel), (n, p, precision, got[0], U)
+        assert close(got[1:], g, rel, atol=rel * max(1.0, np.abs(g).max())), (n, p, precision)
+    r = t.run(t.RunConfig(model={}, num_chains=1, num_warmup=30, num_samples=20, seed=n + p), m)[0]
+    assert np.all(np.isfinite(r.samples)) and r.total_leapfrogs > 0
+
+
 def test_wide_tree_matches_oracle(oracle):
     t = ts()
     from tests_data import logistic_data

@@ -71,6 +71,29 @@ __global__ void k_retile_x64h(const double* __restrict__ x, const uint8_t* __res
   }
 }
 
+// Paired half-row layout (fp64 policy on fp32 X, p <= 64;
+// ts_logistic.cuh, logistic_cta_pass_pair): 32-row tiles of two 16-row
+// half-row blocks (groups of 4 floats), then the 32 labels in row order;
+// padding stays zero from the memset.
+__global__ void k_retile_pair(const float* __restrict__ x, const uint8_t* __restrict__ y, int64_t n, int p,
+                              int64_t ntiles, unsigned char* __restrict__ xt) {
+  const int H = x64h_half(p), G = pair_groups(p);
+  const int64_t tb = pair_tile_bytes(p);
+  const int64_t total = ntiles * 32 * (int64_t)p;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = i / p;
+    const int j = (int)(i % p);
+    const int64_t t = row >> 5;
+    const int rr = (int)(row & 31), b = rr >> 4, r = rr & 15;
+    const int h = j >= H ? 1 : 0;
+    const int k = j - h * H;
+    unsigned char* tile = xt + t * tb;
+    reinterpret_cast<float*>(tile + (int64_t)b * G * 512)[((k >> 2) * 32 + 16 * h + r) * 4 + (k & 3)] =
+        row < n ? x[row * p + j] : 0.f;
+    if (j == 0) tile[2 * G * 512 + rr] = row < n ? y[row] : 0;
+  }
+}
+
 // Wide p (64 < p <= 256): tiles of kWideRows = 8 rows, row-major, each
 // followed by 16 label bytes (8 labels + 8 zeros): 32p + 16 bytes per tile,
 // one TMA bulk copy (ts_logistic.cuh, logistic_cta_pass_wide).
@@ -224,16 +247,20 @@ extern "C" int ts_model_create(int kind, int dim, const double* params, int n_pa
       if (!m->pmax) return fail(TS_EUNSUPPORTED, "logistic feature count > 256 not supported on this path");
       m->xd = precision == TS_PREC_FP64X;  // X stored as fp64
       m->wide = n_feat > 64;
-      m->xh = m->xd && !m->wide;  // fp64 storage, p <= 64: 16-row half-row tiles
+      // p <= 64 in fp64 arithmetic: half-row tiles (1: X fp64, 16-row tiles;
+      // 2: X fp32, paired 32-row tiles)
+      m->xh = m->wide ? 0 : (m->xd ? 1 : (precision == TS_PREC_FP64 ? 2 : 0));
       if (m->xd) m->pmax = m->wide ? kWideMax : kX64hPmax;
+      if (m->xh) m->pmax = kX64hPmax;
       m->n_rows = n_rows;
       m->p = n_feat;
       // wide: whole groups of kWideGroup tiles (32 rows), padding rows zero with label 0
       m->ntiles = m->wide ? (n_rows + kWideRows * kWideGroup - 1) / (kWideRows * kWideGroup) * kWideGroup
-                          : (m->xh ? (n_rows + 15) / 16 : (n_rows + 31) / 32);
+                          : (m->xh == 1 ? (n_rows + 15) / 16 : (n_rows + 31) / 32);
       m->fp64 = precision == TS_PREC_FP64 || m->xd;
       const size_t xbytes = m->wide ? (size_t)m->ntiles * wide_tile_bytes(n_feat, m->xd ? 8 : 4)
-                                    : (m->xh ? (size_t)m->ntiles * x64h_tile_bytes(n_feat)
+                                    : (m->xh == 1 ? (size_t)m->ntiles * x64h_tile_bytes(n_feat)
+                                       : m->xh == 2 ? (size_t)m->ntiles * pair_tile_bytes(n_feat)
                                              : (size_t)m->ntiles * 32 * n_feat * sizeof(float));
       if (cudaMalloc((void**)&m->xt, xbytes) != cudaSuccess) return fail(TS_ECUDA, "cudaMalloc X failed");
       // wide tiles carry their labels; the separate label array is then unused
@@ -244,8 +271,12 @@ extern "C" int ts_model_create(int kind, int dim, const double* params, int n_pa
       // the barrier word doubles as the "X has fp32 subnormals" flag during re-tiling
       if (m->xh) {
         if (cudaMemset(m->xt, 0, xbytes) != cudaSuccess) return fail(TS_ECUDA, "memset X failed");
-        k_retile_x64h<<<1184, 256>>>(static_cast<const double*>(x_dev), y_dev, n_rows, n_feat, m->ntiles,
-                                     reinterpret_cast<unsigned char*>(m->xt));
+        if (m->xh == 1)
+          k_retile_x64h<<<1184, 256>>>(static_cast<const double*>(x_dev), y_dev, n_rows, n_feat, m->ntiles,
+                                       reinterpret_cast<unsigned char*>(m->xt));
+        else
+          k_retile_pair<<<1184, 256>>>(static_cast<const float*>(x_dev), y_dev, n_rows, n_feat, m->ntiles,
+                                       reinterpret_cast<unsigned char*>(m->xt));
       } else if (m->xd)
         k_retile_wide<double><<<1184, 256>>>(static_cast<const double*>(x_dev), y_dev, n_rows, n_feat, m->ntiles,
                                              reinterpret_cast<unsigned char*>(m->xt), reinterpret_cast<int*>(m->bar));

@@ -34,7 +34,7 @@ struct ts_model {
   int exact_cvt;             // X holds fp32 subnormals (fp64 pass uses F2F)
   int wide;                  // 64 < p <= 256, or X in fp64: 8-row row-major tiles (ts_logistic.cuh)
   int xd;                    // X stored as fp64 (TS_PREC_FP64X)
-  int xh;                    // fp64 storage with p <= 64: 16-row half-row tiles (logistic_cta_pass_x64h)
+  int xh;                    // p <= 64 half-row tiles: 1 fp64 X (logistic_cta_pass_x64h), 2 fp32 X paired (fp64 policy)
   double* slotws;            // wide: per-CTA NodeStore slot vectors (grown on demand)
   size_t slotws_size;        // doubles
   // row sharding across GPUs (ts_peer_mailbox_*)

@@ -68,7 +68,8 @@ int launch_block_logistic(const ts_model* m, int nslots, OpArgs& A, cudaStream_t
   TS_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
   TS_CUDA(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   const int stage_bytes = m->wide ? wide_stage_bytes(m->p, m->xd ? 8 : 4)
-                          : (m->xh ? x64h_stage_bytes(m->p) : (int)((128 * (int64_t)m->p + 32 + 127) / 128 * 128));
+                          : (m->xh == 1 ? x64h_stage_bytes(m->p)
+                             : m->xh == 2 ? pair_stage_bytes(m->p) : (int)((128 * (int64_t)m->p + 32 + 127) / 128 * 128));
   // Two stages per worker warp are enough bytes in flight to saturate HBM
   // and leave the rest of the L1/shared array to the engine's stack.
   const int rings = nwarps - 1;  // worker warps

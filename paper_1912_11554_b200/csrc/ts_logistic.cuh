@@ -95,7 +95,7 @@ struct LogisticArgs {
   int xd;                          // X stored as fp64 (wide layout, logistic_cta_pass_wide XD)
   const double* thd;  // FP64 narrow pass: theta as doubles [pmax + 1], zero-padded, 16-B aligned (smem, written by the driver)
   int fxc;            // cross-CTA accumulator copies in use (1..kFxCopies)
-  int xh;                          // X stored as fp64 in the 16-row half-row layout (p <= 64, logistic_cta_pass_x64h)
+  int xh;                          // p <= 64 half-row layouts: 1 X fp64 (logistic_cta_pass_x64h), 2 X fp32 paired (logistic_cta_pass_pair)
 };
 
 // Mailbox of one rank: kMailFlags words of flags (flag[src] = 1 + the last
@@ -837,6 +837,180 @@ __device__ __noinline__ void logistic_cta_pass_x64h(const LogisticArgs& a, const
   if (prof) { pc1 = clock64(); a.prof[7] += pc1 - pc0; }
 }
 
+// ------------------------------------------- fp64 policy on fp32 X, p <= 64
+// Paired half-row tiles (LogisticArgs::xh == 2): a 32-row tile holds two
+// 16-row blocks in the half-row layout above with groups of 4 floats (block
+// A = rows 0-15, B = rows 16-31), then the 32 labels in row order
+// (covtype: 7,200 B per 32 rows, +4.2% over 4 p 32 + 32).  Lane 16 h + r
+// forms half of eta for row r of both blocks (theta in 28 registers), one
+// shuffle per block joins the halves, and then lane L evaluates the
+// exp / log1p / division of tile row L alone -- each row's transcendental
+// work done once, not twice as with one block per stage -- and two
+// shuffles hand the residuals back to the half-row lanes for the gradient.
+// Against the 32-row layout (54 x, 55 accumulators, theta by LDS per row)
+// this halves the instructions per row.
+__host__ __device__ inline int pair_groups(int p) { return (x64h_half(p) + 3) / 4; }
+__host__ __device__ inline int64_t pair_tile_bytes(int p) { return 2 * (int64_t)pair_groups(p) * 512 + 32; }
+__host__ __device__ inline int pair_stage_bytes(int p) { return (int)((pair_tile_bytes(p) + 127) / 128 * 128); }
+
+template <int HE>
+__device__ __noinline__ void logistic_cta_pass_pair(const LogisticArgs& a, const double* __restrict__ theta_s,
+                                                    double* wred, double* red_out) {
+  extern __shared__ __align__(16) unsigned char ts_dyn_smem[];
+  constexpr int KX = HE > 0 ? ((HE + 3) / 4) * 4 : 32;  // x values per lane per block (whole groups)
+  constexpr int NA = kX64hPmax + 2;
+  const int lane = threadIdx.x & 31, warp = wk_warp(), nwarps = wk_nwarps();
+  const int p = a.p;
+  const int H = HE > 0 ? HE : x64h_half(p);
+  const int G = (H + 3) / 4;
+  const int h = lane >> 4, r = lane & 15;
+  const int f0 = h * H;
+  WarpPipe& pipe = a.pipe[warp];
+  const int count = pipe.count;
+  const bool prof = a.prof != nullptr && blockIdx.x == 0 && wk_tid() == 0;
+  long long pc0 = prof ? clock64() : 0, pc1;
+  const int nstage = a.nstage;
+  const int stage_bytes = a.stage_bytes;
+  const uint32_t ring_off = (uint32_t)(a.stages - ts_dyn_smem) + (uint32_t)(warp * nstage * stage_bytes);
+  uint64_t* const bars = a.mbar + warp * nstage;
+  const double* thd = reinterpret_cast<const double*>(ts_dyn_smem + (reinterpret_cast<const unsigned char*>(a.thd) - ts_dyn_smem));
+  // theta per half, 16-B aligned and zero past each half's features: thh[h][32]
+  // (after the driver's zero-padded copy in red_s); broadcast LDS.128 in the
+  // loop instead of 56 registers (which spilled)
+  double* thh = const_cast<double*>(thd) + 66;
+  for (int i = wk_tid(); i < 64; i += wk_threads()) {
+    const int hh = i >> 5, k = i & 31;
+    thh[i] = (k < H && hh * H + k < p) ? thd[hh * H + k] : 0.0;
+  }
+  wk_sync();
+  const uint32_t th_addr = smem_u32(thh + 32 * h);
+  const double thb = thd[kX64hPmax];
+  double acc[KX];
+#pragma unroll
+  for (int k = 0; k < KX; ++k) acc[k] = 0.0;
+  double accb = 0.0, accl = 0.0;
+  const int blk = G * 512;  // bytes per 16-row block
+  if (count > 0) {
+    const unsigned long long c0 = pipe.consumed;
+    unsigned long long issued = pipe.issued;
+    const int tfirst = pipe.first, tstride = nwarps;
+    const int nfull = (int)(a.n_rows >> 5), rem = (int)(a.n_rows & 31);
+    const uint32_t tb = (uint32_t)pair_tile_bytes(p);
+    const unsigned char* const xfirst = reinterpret_cast<const unsigned char*>(a.xt) + (int64_t)tfirst * tb;
+    const int64_t xstep = (int64_t)tstride * tb;
+    const int keep = pipe.keep;
+    const uint64_t pol = policy_evict_first(), pol_keep = policy_evict_last();
+    int ps = pipe.ps, pj = pipe.pj;
+    const unsigned char* pxs = xfirst + (int64_t)pj * xstep;
+    auto issue = [&]() {
+      if (lane == 0) {
+        uint64_t* bar = bars + ps;
+        unsigned char* dst = ts_dyn_smem + ring_off + (uint32_t)(ps * stage_bytes);
+        mbar_expect_tx(bar, tb);
+        bulk_g2s(dst, pxs, tb, bar, pj < keep ? pol_keep : pol);
+      }
+      if (++ps == nstage) ps = 0;
+      if (++pj == count) { pj = 0; pxs = xfirst; }
+      else pxs += xstep;
+    };
+    while (issued < c0 + (unsigned long long)nstage) { issue(); ++issued; }
+    int s = pipe.cs, tj = pipe.ctj;
+    uint32_t parity = (uint32_t)pipe.cpar;
+    if (prof) { pc1 = clock64(); a.prof[4] += pc1 - pc0; pc0 = pc1; }
+    for (int j = 0; j < count; ++j) {
+      mbar_wait(bars + s, parity);
+      const unsigned char* sb = ts_dyn_smem + ring_off + (uint32_t)(s * stage_bytes);
+      float xa[KX], xb[KX];
+#pragma unroll
+      for (int g = 0; g < KX / 4; ++g) {
+        if (HE > 0 || g < G) {
+          const float4 va = reinterpret_cast<const float4*>(sb)[g * 32 + lane];
+          const float4 vb = reinterpret_cast<const float4*>(sb + blk)[g * 32 + lane];
+          xa[4 * g] = va.x; xa[4 * g + 1] = va.y; xa[4 * g + 2] = va.z; xa[4 * g + 3] = va.w;
+          xb[4 * g] = vb.x; xb[4 * g + 1] = vb.y; xb[4 * g + 2] = vb.z; xb[4 * g + 3] = vb.w;
+        } else {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) { xa[4 * g + u] = 0.f; xb[4 * g + u] = 0.f; }
+        }
+      }
+      const double yv = (double)sb[2 * blk + lane];  // label of tile row `lane`
+      __syncwarp();
+      issue();
+      ++issued;
+      const int t = tfirst + tj * tstride;
+      const bool valid = lane < (t < nfull ? 32 : rem);
+      if (++s == nstage) { s = 0; parity ^= 1u; }
+      if (++tj == count) tj = 0;
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, b0 = 0.0, b1 = 0.0, b2 = 0.0, b3 = 0.0;
+#pragma unroll
+      for (int k = 0; k < KX; k += 4) {
+        double2 t01, t23;  // volatile loads: not hoisted into 56 registers
+        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(t01.x), "=d"(t01.y) : "r"(th_addr + 8u * k));
+        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(t23.x), "=d"(t23.y) : "r"(th_addr + 8u * (k + 2)));
+        a0 = __fma_rn((double)xa[k], t01.x, a0);
+        a1 = __fma_rn((double)xa[k + 1], t01.y, a1);
+        a2 = __fma_rn((double)xa[k + 2], t23.x, a2);
+        a3 = __fma_rn((double)xa[k + 3], t23.y, a3);
+        b0 = __fma_rn((double)xb[k], t01.x, b0);
+        b1 = __fma_rn((double)xb[k + 1], t01.y, b1);
+        b2 = __fma_rn((double)xb[k + 2], t23.x, b2);
+        b3 = __fma_rn((double)xb[k + 3], t23.y, b3);
+      }
+      const double pa = (a0 + a1) + (a2 + a3), pb = (b0 + b1) + (b2 + b3);
+      const double oa = __shfl_xor_sync(0xffffffffu, pa, 16), ob = __shfl_xor_sync(0xffffffffu, pb, 16);
+      // the same association in both halves: (lower + upper) + bias
+      const double eta_a = (h ? oa + pa : pa + oa) + thb, eta_b = (h ? ob + pb : pb + ob) + thb;
+      // lane L evaluates tile row L: block A's row L (L < 16), block B's row L - 16
+      const double eta = h ? eta_b : eta_a;
+      const double e = exp(-fabs(eta));
+      const double l = fmax(eta, 0.0) + log1p(e);
+      const double sig = __ddiv_rn(eta >= 0.0 ? 1.0 : e, 1.0 + e);
+      const double resid = valid ? yv - sig : 0.0;
+      accl += valid ? (yv * eta - l) : 0.0;
+      accb += resid;
+      const double ra = __shfl_sync(0xffffffffu, resid, r), rb = __shfl_sync(0xffffffffu, resid, 16 + r);
+#pragma unroll
+      for (int k = 0; k < KX; ++k) {
+        acc[k] = __fma_rn(ra, (double)xa[k], acc[k]);
+        acc[k] = __fma_rn(rb, (double)xb[k], acc[k]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) {
+      pipe.consumed = c0 + (unsigned long long)count;
+      pipe.issued = issued;
+      pipe.cs = s; pipe.cpar = (int)parity; pipe.ctj = tj;
+      pipe.ps = ps; pipe.pj = pj;
+    }
+    __syncwarp();
+  }
+  if (prof) { pc1 = clock64(); a.prof[5] += pc1 - pc0; pc0 = pc1; }
+  // gradient: sums over the 16 rows of each half (fixed shuffle tree), lane 0 / 16 write
+#pragma unroll
+  for (int k = 0; k < KX; ++k) {
+    double v = acc[k];
+#pragma unroll
+    for (int off = 8; off >= 1; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    if (r == 0 && k < H && f0 + k < p) wred[warp * NA + f0 + k] = v;
+  }
+  // residual and log-likelihood: one row per lane, sums over all 32 lanes
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    accb += __shfl_xor_sync(0xffffffffu, accb, off);
+    accl += __shfl_xor_sync(0xffffffffu, accl, off);
+  }
+  if (lane == 0) { wred[warp * NA + kX64hPmax] = accb; wred[warp * NA + kX64hPmax + 1] = accl; }
+  if (prof) { pc1 = clock64(); a.prof[6] += pc1 - pc0; pc0 = pc1; }
+  wk_sync();
+  for (int d = wk_tid(); d < p + 2; d += wk_threads()) {
+    const int jj = (d < p) ? d : (d == p ? kX64hPmax : kX64hPmax + 1);
+    double sum = 0.0;
+    for (int w = 0; w < nwarps; ++w) sum += wred[w * NA + jj];
+    red_out[d] = sum;
+  }
+  if (prof) { pc1 = clock64(); a.prof[7] += pc1 - pc0; }
+}
+
 // ---------------------------------------------------------------- wide p
 // p in (64, kWideMax]: a tile is kWideRows = 8 rows in the input's row-major
 // order followed by 16 bytes holding the 8 labels (+ 8 zero bytes): one TMA
@@ -1130,9 +1304,14 @@ __device__ __noinline__ void logistic_cta_pass_wide(const LogisticArgs& a, const
 
 static __device__ __forceinline__ void logistic_cta_dispatch(const LogisticArgs& a, const double* theta, double* wred,
                                                              double* red_s) {
-  if (a.xh) {  // fp64 storage, p <= 64
+  if (a.xh == 1) {  // fp64 storage, p <= 64
     if (a.p == 54) logistic_cta_pass_x64h<27>(a, theta, wred, red_s);
     else logistic_cta_pass_x64h<0>(a, theta, wred, red_s);
+    return;
+  }
+  if (a.xh == 2) {  // fp64 policy on fp32 X, p <= 64: paired half-row tiles
+    if (a.p == 54) logistic_cta_pass_pair<27>(a, theta, wred, red_s);
+    else logistic_cta_pass_pair<0>(a, theta, wred, red_s);
     return;
   }
   if (a.wide) {

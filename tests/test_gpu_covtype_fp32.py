@@ -162,11 +162,14 @@ def test_covtype_fp32_decision_replay(data, models, oracle):
 
 
 def _moments(chains, ts):
-    """Pooled mean/SD, per-dimension ESS (reference estimator) and split R-hat."""
+    """Pooled mean/SD, per-dimension ESS (reference estimator) of the draws and
+    of their squared deviations (the SD's Monte-Carlo error: NUTS draws are
+    antithetic for the mean, not for second moments), and split R-hat."""
     ess = ts.ess(chains)
     rhat = ts.split_rhat(chains)
     pooled = chains.reshape(-1, chains.shape[-1])
-    return pooled.mean(0), pooled.std(0, ddof=1), ess, rhat
+    mu = pooled.mean(0)
+    return mu, pooled.std(0, ddof=1), ess, ts.ess((chains - mu) ** 2), rhat
 
 
 def test_covtype_fp32_vs_fp64_posterior(models):
@@ -177,13 +180,13 @@ def test_covtype_fp32_vs_fp64_posterior(models):
     for prec in ("fp32", "fp64"):
         r = t.run(t.RunConfig(model={}, num_chains=4, num_warmup=1000, num_samples=1000, seed=77), models[prec])
         res[prec] = np.stack([c.samples for c in r])
-    m32, s32, e32, r32 = _moments(res["fp32"], t)
-    m64, s64, e64, r64 = _moments(res["fp64"], t)
+    m32, s32, e32, q32, r32 = _moments(res["fp32"], t)
+    m64, s64, e64, q64, r64 = _moments(res["fp64"], t)
     assert (r32 < 1.01).all() and (r64 < 1.01).all(), (r32.max(), r64.max())
     mcse_mean = np.sqrt(s32 ** 2 / e32 + s64 ** 2 / e64)
     z_mean = np.abs(m32 - m64) / mcse_mean
-    # SD of a near-Gaussian marginal: MCSE(sd) ~ sd / sqrt(2 ESS)
-    mcse_sd = np.sqrt(s32 ** 2 / (2 * e32) + s64 ** 2 / (2 * e64))
+    # SD of a near-Gaussian marginal: MCSE(sd) ~ sd / sqrt(2 ESS of the squared deviations)
+    mcse_sd = np.sqrt(s32 ** 2 / (2 * q32) + s64 ** 2 / (2 * q64))
     z_sd = np.abs(s32 - s64) / mcse_sd
     print(f"covtype fp32 vs fp64: max |dmean|/MCSE {z_mean.max():.2f}, max |dsd|/MCSE {z_sd.max():.2f}, "
           f"min ESS {min(e32.min(), e64.min()):.0f}, max R-hat {max(r32.max(), r64.max()):.4f}")

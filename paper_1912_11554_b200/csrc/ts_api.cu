@@ -561,7 +561,7 @@ extern "C" int ts_run_chains(const ts_model* m, const ts_run_cfg* rc, const uint
   // (allocated per call on the launch stream: no buffer shared across devices or threads)
   unsigned long long* prof_buf = nullptr;
   const bool prof = getenv("TS_PROF") != nullptr &&
-                    (m->kind == TS_LOGISTIC || (m->kind != TS_DENSE_GAUSS && exec_mode == TS_EXEC_WARP));
+                    (m->kind == TS_LOGISTIC || m->kind == TS_DENSE_GAUSS || exec_mode == TS_EXEC_WARP);
   if (prof) {
     TS_CUDA(cudaMallocAsync((void**)&prof_buf, kProfWords * sizeof(unsigned long long), st));
     TS_CUDA(cudaMemsetAsync(prof_buf, 0, kProfWords * sizeof(unsigned long long), st));
@@ -612,6 +612,13 @@ extern "C" int ts_run_chains(const ts_model* m, const ts_run_cfg* rc, const uint
         fprintf(stderr, "TS_PROF trajectories: driver %llu leaves, wait %.0f + bookkeeping %.0f cycles/leaf; workers %llu leaves, "
                 "gate wait %.0f + leaf work outside the pass %.0f cycles/leaf\n", h[22], h[20] / nl, h[21] / nl, h[19],
                 h[17] / nw, h[18] / nw);
+      }
+      if (m->kind == TS_DENSE_GAUSS && h[27]) {
+        const double nl = (double)h[27];
+        fprintf(stderr, "TS_PROF dense chain 0: %llu fused leaves, cycles/leaf: gradient wait %.0f, fused pass %.0f, "
+                "bookkeeping %.0f\n", h[27], h[24] / nl, (h[25] + h[28]) / nl, h[26] / nl);
+        fprintf(stderr, "TS_PROF dense chain 0 pass split: vector loop %.0f, post (fences + flag) %.0f, sums %.0f\n",
+                h[28] / nl, h[29] / nl, h[30] / nl);
       }
       if (m->kind == TS_LOGISTIC && m->many && h[24 + 8]) {
         const double nt = h[24 + 7] ? (double)h[24 + 7] : 1.0, nc = (double)h[24 + 8];

@@ -15,6 +15,7 @@
 // a ThreadTeam chain of a small model reproduces the reference bit for bit
 // up to the last-ulp behaviour of exp/log1p.
 #pragma once
+#include <stddef.h>
 #include <math.h>
 #include <stdint.h>
 #include "ts_rng.cuh"
@@ -46,6 +47,12 @@ __host__ __device__ inline int num_vecs(int nslots) { return V_SLOT0 + kSlotVecs
 constexpr int kTeamScratch = 64 + (kMaxSlots * 56 + 7) / 8;
 __device__ __forceinline__ int slot_vec(int s, int k) { return V_SLOT0 + kSlotVecs * s + k; }
 
+// Warp vector helpers for warp-owned large-D vectors in global memory (the
+// batched dense model).  Loads are ld.global.cg (L2 only): the vectors
+// stream through once per leaf and would otherwise evict the chain warps'
+// local memory (engine state) from L1 (ld.global.L1::no_allocate measured
+// slower: 8.06 -> 7.09 M chain-leapfrog/s).
+//
 // Warp copy of n2 double2 (lane-strided, 8 loads in flight per lane).  A
 // separate function: its registers stay out of the engine's allocation.
 static __device__ __noinline__ void warp_copy2(double2* __restrict__ a, const double2* __restrict__ b, int n2) {
@@ -53,7 +60,7 @@ static __device__ __noinline__ void warp_copy2(double2* __restrict__ a, const do
     double2 t[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u)
-      if (base + 32 * u < n2) t[u] = b[base + 32 * u];
+      if (base + 32 * u < n2) t[u] = __ldcg(b + base + 32 * u);
 #pragma unroll
     for (int u = 0; u < 8; ++u)
       if (base + 32 * u < n2) a[base + 32 * u] = t[u];
@@ -71,7 +78,7 @@ static __device__ __noinline__ void warp_drift2(double2* __restrict__ nq, double
     double2 tq[4], tr[4], tg[4], ti[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u)
-      if (base + 32 * u < n2) { tq[u] = q[base + 32 * u]; tr[u] = r[base + 32 * u]; tg[u] = g[base + 32 * u]; ti[u] = inv[base + 32 * u]; }
+      if (base + 32 * u < n2) { tq[u] = __ldcg(q + base + 32 * u); tr[u] = __ldcg(r + base + 32 * u); tg[u] = __ldcg(g + base + 32 * u); ti[u] = __ldcg(inv + base + 32 * u); }
 #pragma unroll
     for (int u = 0; u < 4; ++u)
       if (base + 32 * u < n2) {
@@ -93,7 +100,7 @@ static __device__ __noinline__ void warp_advance2(double2* __restrict__ q, doubl
     double2 tq[4], tr[4], tg[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u)
-      if (base + 32 * u < n2) { tq[u] = nq[base + 32 * u]; tr[u] = nr[base + 32 * u]; tg[u] = ng[base + 32 * u]; }
+      if (base + 32 * u < n2) { tq[u] = __ldcg(nq + base + 32 * u); tr[u] = __ldcg(nr + base + 32 * u); tg[u] = __ldcg(ng + base + 32 * u); }
 #pragma unroll
     for (int u = 0; u < 4; ++u)
       if (base + 32 * u < n2) {
@@ -111,7 +118,7 @@ static __device__ __noinline__ void warp_add2(double2* __restrict__ c, const dou
     double2 tc[8], tr[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u)
-      if (base + 32 * u < n2) { tc[u] = c[base + 32 * u]; tr[u] = r[base + 32 * u]; }
+      if (base + 32 * u < n2) { tc[u] = __ldcg(c + base + 32 * u); tr[u] = __ldcg(r + base + 32 * u); }
 #pragma unroll
     for (int u = 0; u < 8; ++u)
       if (base + 32 * u < n2) {
@@ -130,7 +137,7 @@ static __device__ __noinline__ double warp_kinetic2(const double2* __restrict__ 
     double2 tr[8], ti[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u)
-      if (base + 32 * u < n2) { tr[u] = r[base + 32 * u]; ti[u] = inv[base + 32 * u]; }
+      if (base + 32 * u < n2) { tr[u] = __ldcg(r + base + 32 * u); ti[u] = __ldcg(inv + base + 32 * u); }
 #pragma unroll
     for (int u = 0; u < 8; ++u)
       if (base + 32 * u < n2) {
@@ -151,8 +158,8 @@ static __device__ __noinline__ void warp_gen_uturn2(const double2* __restrict__ 
 #pragma unroll
     for (int u = 0; u < 4; ++u)
       if (base + 32 * u < n2) {
-        tc[u] = cum[base + 32 * u]; tf[u] = cf[base + 32 * u]; trf[u] = fr[base + 32 * u];
-        ti[u] = inv[base + 32 * u]; trr[u] = rr[base + 32 * u];
+        tc[u] = __ldcg(cum + base + 32 * u); tf[u] = __ldcg(cf + base + 32 * u); trf[u] = __ldcg(fr + base + 32 * u);
+        ti[u] = __ldcg(inv + base + 32 * u); trr[u] = __ldcg(rr + base + 32 * u);
       }
 #pragma unroll
     for (int u = 0; u < 4; ++u)
@@ -178,70 +185,118 @@ __device__ __forceinline__ bool al16(const void* p) { return (reinterpret_cast<u
 // which would re-read the vectors in another pass): 5 = even leaf into its
 // slot (q, r, cum, proposal q, proposal g -> st[0..4]), 2 = odd leaf into
 // the running proposal (st[0] = q, st[1] = g), 0 = none.
+// Operands of warp_leaf_fused, in shared memory (one record per chain warp,
+// written by the engine before the call): passed as one pointer instead of
+// 18 arguments, which spilled past the ABI's register arguments onto the
+// stack and were re-read from local memory every iteration.
+#ifndef TS_LEAF_INLINE
+#define TS_LEAF_INLINE __forceinline__
+#endif
+struct LeafVecs {
+  double2* q;
+  double2* r;
+  double2* g;
+  double2* nq;
+  double2* nr;
+  const void* grow;
+  const double2* inv;
+  double2* cum;
+  void* row;
+  double2* st[5];
+  double half, eps;
+  int n2;
+  int pad_;
+};
+// pointer field `off` (bytes) of a shared-memory record, re-read at every
+// use (volatile): short live ranges instead of 14 pointers held across the
+// loop, which the register allocator spilled to local memory
+template <class P>
+__device__ __forceinline__ P* lds_ptr(uint32_t rec, uint32_t off) {
+  uint64_t v;
+  asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(rec + off));
+  return reinterpret_cast<P*>(v);
+}
 template <bool F64ROW, int ST>
-static __device__ __noinline__ double warp_leaf_fused(double2* __restrict__ q, double2* __restrict__ r,
-                                                      double2* __restrict__ g, double2* __restrict__ nq,
-                                                      double2* __restrict__ nr, const void* __restrict__ grow,
-                                                      const double2* __restrict__ inv, double2* __restrict__ cum,
-                                                      void* __restrict__ row, double half, double eps, int n2,
-                                                      double& udot,
-                                                      double2* __restrict__ st0 = nullptr, double2* __restrict__ st1 = nullptr,
-                                                      double2* __restrict__ st2 = nullptr, double2* __restrict__ st3 = nullptr,
-                                                      double2* __restrict__ st4 = nullptr) {
+static __device__ TS_LEAF_INLINE double2 warp_leaf_fused(const LeafVecs* __restrict__ L) {
   // grow: the served gradient row (fp32 tf32-GEMM output, or doubles);
-  // udot: this lane's part of q . g (U = q'Aq / 2 = q . g / 2)
+  // returns this lane's (kinetic partial, q . g partial) (U = q'Aq / 2 = q . g / 2).
+  // Two elements per lane in flight, no predicated arrays, operand pointers
+  // re-read from the shared record at each use: the four-wide form with 18
+  // pointer arguments spilled its loads and pointers to local memory on
+  // every iteration (64 us per 1000-D leaf).  Per lane the elements are
+  // still visited in ascending order (the kinetic-energy / U partial sums
+  // keep warp_kinetic2's order).
+  const uint32_t rec = static_cast<uint32_t>(__cvta_generic_to_shared(L));
+  const double half = L->half, eps = L->eps;
+  const int n2 = L->n2;
+  constexpr uint32_t oQ = offsetof(LeafVecs, q), oR = offsetof(LeafVecs, r), oG = offsetof(LeafVecs, g),
+                     oNQ = offsetof(LeafVecs, nq), oNR = offsetof(LeafVecs, nr), oGR = offsetof(LeafVecs, grow),
+                     oINV = offsetof(LeafVecs, inv), oCUM = offsetof(LeafVecs, cum), oROW = offsetof(LeafVecs, row),
+                     oST = offsetof(LeafVecs, st);
   double kin = 0.0, ud = 0.0;
-  for (int base = (int)(threadIdx.x & 31); base < n2; base += 32 * 4) {
-    double2 tq[4], tr[4], tg[4], ti[4], tc[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-      if (base + 32 * u < n2) {
-        const int i = base + 32 * u;
-        tq[u] = nq[i]; tr[u] = nr[i]; ti[u] = inv[i]; tc[u] = cum[i];
-        if constexpr (F64ROW) {
-          tg[u] = __ldcg(reinterpret_cast<const double2*>(grow) + i);
-        } else {
-          const float2 f = __ldcg(reinterpret_cast<const float2*>(grow) + i);
-          tg[u] = make_double2((double)f.x, (double)f.y);
-        }
-      }
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-      if (base + 32 * u < n2) {
-        const int i = base + 32 * u;
-        double2 rr, rh, nqv, cv;
-        rr.x = __dsub_rn(tr[u].x, __dmul_rn(half, tg[u].x));
-        rr.y = __dsub_rn(tr[u].y, __dmul_rn(half, tg[u].y));
-        q[i] = tq[u];
-        g[i] = tg[u];
-        r[i] = rr;
-        ud = __dadd_rn(ud, __dmul_rn(tq[u].x, tg[u].x));
-        ud = __dadd_rn(ud, __dmul_rn(tq[u].y, tg[u].y));
-        cv.x = __dadd_rn(tc[u].x, rr.x);
-        cv.y = __dadd_rn(tc[u].y, rr.y);
-        cum[i] = cv;
-        if constexpr (ST == 5) { st0[i] = tq[u]; st1[i] = rr; st2[i] = cv; st3[i] = tq[u]; st4[i] = tg[u]; }
-        if constexpr (ST == 2) { st0[i] = tq[u]; st1[i] = tg[u]; }
-        kin = __dadd_rn(kin, __dmul_rn(__dmul_rn(__dmul_rn(0.5, rr.x), rr.x), ti[u].x));
-        kin = __dadd_rn(kin, __dmul_rn(__dmul_rn(__dmul_rn(0.5, rr.y), rr.y), ti[u].y));
-        rh.x = __dsub_rn(rr.x, __dmul_rn(half, tg[u].x));
-        rh.y = __dsub_rn(rr.y, __dmul_rn(half, tg[u].y));
-        nqv.x = __dadd_rn(tq[u].x, __dmul_rn(eps, __dmul_rn(ti[u].x, rh.x)));
-        nqv.y = __dadd_rn(tq[u].y, __dmul_rn(eps, __dmul_rn(ti[u].y, rh.y)));
-        nr[i] = rh;
-        nq[i] = nqv;
-        if constexpr (F64ROW) {
-          reinterpret_cast<double2*>(row)[i] = nqv;
-        } else {
-          uint32_t a, b;
-          asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(a) : "f"((float)nqv.x));
-          asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(b) : "f"((float)nqv.y));
-          reinterpret_cast<float2*>(row)[i] = make_float2(__uint_as_float(a), __uint_as_float(b));
-        }
-      }
+  auto load_g = [&](int i) -> double2 {
+    if constexpr (F64ROW) {
+      return __ldcg(lds_ptr<const double2>(rec, oGR) + i);
+    } else {
+      const float2 f = __ldcg(lds_ptr<const float2>(rec, oGR) + i);
+      return make_double2((double)f.x, (double)f.y);
+    }
+  };
+  auto body = [&](int i, double2 tq, double2 tr, double2 tg, double2 ti, double2 tc) {
+    double2 rr, rh, nqv, cv;
+    rr.x = __dsub_rn(tr.x, __dmul_rn(half, tg.x));
+    rr.y = __dsub_rn(tr.y, __dmul_rn(half, tg.y));
+    lds_ptr<double2>(rec, oQ)[i] = tq;
+    lds_ptr<double2>(rec, oG)[i] = tg;
+    lds_ptr<double2>(rec, oR)[i] = rr;
+    ud = __dadd_rn(ud, __dmul_rn(tq.x, tg.x));
+    ud = __dadd_rn(ud, __dmul_rn(tq.y, tg.y));
+    cv.x = __dadd_rn(tc.x, rr.x);
+    cv.y = __dadd_rn(tc.y, rr.y);
+    lds_ptr<double2>(rec, oCUM)[i] = cv;
+    if constexpr (ST == 5) {
+      lds_ptr<double2>(rec, oST)[i] = tq;
+      lds_ptr<double2>(rec, oST + 8)[i] = rr;
+      lds_ptr<double2>(rec, oST + 16)[i] = cv;
+      lds_ptr<double2>(rec, oST + 24)[i] = tq;
+      lds_ptr<double2>(rec, oST + 32)[i] = tg;
+    }
+    if constexpr (ST == 2) {
+      lds_ptr<double2>(rec, oST)[i] = tq;
+      lds_ptr<double2>(rec, oST + 8)[i] = tg;
+    }
+    kin = __dadd_rn(kin, __dmul_rn(__dmul_rn(__dmul_rn(0.5, rr.x), rr.x), ti.x));
+    kin = __dadd_rn(kin, __dmul_rn(__dmul_rn(__dmul_rn(0.5, rr.y), rr.y), ti.y));
+    rh.x = __dsub_rn(rr.x, __dmul_rn(half, tg.x));
+    rh.y = __dsub_rn(rr.y, __dmul_rn(half, tg.y));
+    nqv.x = __dadd_rn(tq.x, __dmul_rn(eps, __dmul_rn(ti.x, rh.x)));
+    nqv.y = __dadd_rn(tq.y, __dmul_rn(eps, __dmul_rn(ti.y, rh.y)));
+    lds_ptr<double2>(rec, oNR)[i] = rh;
+    lds_ptr<double2>(rec, oNQ)[i] = nqv;
+    if constexpr (F64ROW) {
+      lds_ptr<double2>(rec, oROW)[i] = nqv;
+    } else {
+      uint32_t a, b;
+      asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(a) : "f"((float)nqv.x));
+      asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(b) : "f"((float)nqv.y));
+      lds_ptr<float2>(rec, oROW)[i] = make_float2(__uint_as_float(a), __uint_as_float(b));
+    }
+  };
+  auto ld = [&](uint32_t off, int i) -> double2 { return __ldcg(lds_ptr<const double2>(rec, off) + i); };
+  int i = (int)(threadIdx.x & 31);
+  const int nfull = n2 & ~63;
+  for (; i < nfull; i += 64) {
+    const int j = i + 32;
+    const double2 q0 = ld(oNQ, i), r0 = ld(oNR, i), i0 = ld(oINV, i), c0 = ld(oCUM, i), g0 = load_g(i);
+    const double2 q1 = ld(oNQ, j), r1 = ld(oNR, j), i1 = ld(oINV, j), c1 = ld(oCUM, j), g1 = load_g(j);
+    body(i, q0, r0, g0, i0, c0);
+    body(j, q1, r1, g1, i1, c1);
   }
-  udot = ud;
-  return kin;
+  for (; i < n2; i += 32) {
+    const double2 q0 = ld(oNQ, i), r0 = ld(oNR, i), i0 = ld(oINV, i), c0 = ld(oCUM, i), g0 = load_g(i);
+    body(i, q0, r0, g0, i0, c0);
+  }
+  return make_double2(kin, ud);  // (kinetic-energy partial, this lane's part of q . g)
 }
 // up to 5 vector copies in one pass (k pairs), 2 x double2 per operand in flight
 static __device__ __noinline__ void warp_copy_multi(double2* __restrict__ d0, const double2* __restrict__ s0,
@@ -256,11 +311,11 @@ static __device__ __noinline__ void warp_copy_multi(double2* __restrict__ d0, co
     for (int u = 0; u < 2; ++u) {
       const int i = base + 32 * u;
       if (i < n2) {
-        t[0][u] = s0[i];
-        t[1][u] = s1[i];
-        t[2][u] = s2[i];
-        if (k > 3) t[3][u] = s3[i];
-        if (k > 4) t[4][u] = s4[i];
+        t[0][u] = __ldcg(s0 + i);
+        t[1][u] = __ldcg(s1 + i);
+        t[2][u] = __ldcg(s2 + i);
+        if (k > 3) t[3][u] = __ldcg(s3 + i);
+        if (k > 4) t[4][u] = __ldcg(s4 + i);
       }
     }
 #pragma unroll
@@ -372,6 +427,7 @@ struct Engine {
   unsigned long long* prof = nullptr;  // CTA 0 / thread 0 only (profiling builds of a run)
   long long prof_last = 0;
   long long prof_post = 0;
+  long long prof_w0 = 0, prof_w1 = 0;  // dense fused-leaf phase stamps ([24] wait, [25] pass, [26] bookkeeping, [27] leaves)
 
   // CTA/warp teams keep vectors contiguous in shared memory (unit component
   // stride, 32-bit offsets); thread teams interleave chains in global memory.
@@ -886,7 +942,9 @@ struct Engine {
           bool waited = false;
           if constexpr (Team::kWarp && Team::kUnitStride && Model::kVecOps) {
             if (fusable) {
+              if (prof != nullptr && T.leader()) prof_w0 = clock64();
               M.wait_poll();  // the fused pass reads the gradient row itself and forms U
+              if (prof != nullptr && T.leader()) { prof_w1 = clock64(); prof[24] += prof_w1 - prof_w0; prof[27] += 1; }
               n_evals += 1;
               waited = true;
             }
@@ -910,24 +968,28 @@ struct Engine {
               const double2* inv2 = reinterpret_cast<const double2*>(v(V_INV));
               double2* c2 = reinterpret_cast<double2*>(v(V_CUM));
               // leaf_book's NodeStore copies written by the same pass
-              double kin, ud = 0.0;
-              if ((n & 1ULL) == 0) {
-                const int sl = __popcll(n);
-                double2* st[5];
+              LeafVecs* lv = M.leaf_vecs();
+              if (T.leader()) {
+                lv->q = q2; lv->r = r2; lv->g = g2; lv->nq = nq2; lv->nr = nr2; lv->grow = ng2; lv->inv = inv2;
+                lv->cum = c2; lv->row = row; lv->half = half; lv->eps = eps; lv->n2 = D >> 1;
+                if ((n & 1ULL) == 0) {
+                  const int sl = __popcll(n);
 #pragma unroll
-                for (int k = 0; k < 5; ++k) st[k] = reinterpret_cast<double2*>(v(slot_vec(sl, k)));
-                kin = M.fp64 ? warp_leaf_fused<true, 5>(q2, r2, g2, nq2, nr2, ng2, inv2, c2, row, half, eps, D >> 1, ud,
-                                                         st[0], st[1], st[2], st[3], st[4])
-                             : warp_leaf_fused<false, 5>(q2, r2, g2, nq2, nr2, ng2, inv2, c2, row, half, eps, D >> 1, ud,
-                                                          st[0], st[1], st[2], st[3], st[4]);
-              } else {
-                double2* tpq = reinterpret_cast<double2*>(v(V_TPQ));
-                double2* tpg = reinterpret_cast<double2*>(v(V_TPG));
-                kin = M.fp64 ? warp_leaf_fused<true, 2>(q2, r2, g2, nq2, nr2, ng2, inv2, c2, row, half, eps, D >> 1, ud, tpq, tpg)
-                             : warp_leaf_fused<false, 2>(q2, r2, g2, nq2, nr2, ng2, inv2, c2, row, half, eps, D >> 1, ud, tpq, tpg);
+                  for (int k = 0; k < 5; ++k) lv->st[k] = reinterpret_cast<double2*>(v(slot_vec(sl, k)));
+                } else {
+                  lv->st[0] = reinterpret_cast<double2*>(v(V_TPQ));
+                  lv->st[1] = reinterpret_cast<double2*>(v(V_TPG));
+                }
               }
+              __syncwarp();
+              double2 ku;
+              if ((n & 1ULL) == 0) ku = M.fp64 ? warp_leaf_fused<true, 5>(lv) : warp_leaf_fused<false, 5>(lv);
+              else ku = M.fp64 ? warp_leaf_fused<true, 2>(lv) : warp_leaf_fused<false, 2>(lv);
+              const double kin = ku.x, ud = ku.y;
               T.sync();
+              if (prof != nullptr && T.leader()) { const long long c = clock64(); prof[28] += c - prof_w1; prof_w1 = c; }
               M.post_written(V_NQ, V_NG);
+              if (prof != nullptr && T.leader()) { const long long c = clock64(); prof[29] += c - prof_w1; prof[25] += c - prof_w1; prof_w1 = c; }
               {
                 const double uu = 0.5 * T.sum(ud);  // DenseW::wait's U, formed in the pass
                 cur_U = isfinite(uu) ? uu : kInf();
@@ -940,6 +1002,7 @@ struct Engine {
               }
               delta = __dsub_rn(h, h_ref);
               fused = true;
+              if (prof != nullptr && T.leader()) { prof_w0 = clock64(); prof[25] += prof_w0 - prof_w1; prof[30] += prof_w0 - prof_w1; }
             }
           }
           if (!fused) {
@@ -956,6 +1019,7 @@ struct Engine {
             leaf_energy(h_ref, h, delta);
           }
           stop = leaf_book(n, h, delta, draws, forward, fused);
+          if (fused && prof != nullptr && T.leader()) prof[26] += clock64() - prof_w0;
           if (stop != kStopNone) {
             if (spec) { (void)wait_eval(); n_wasted += 1; }
             break;

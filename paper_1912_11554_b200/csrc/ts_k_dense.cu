@@ -104,6 +104,8 @@ struct DenseW : NoTraj {
   unsigned long long spin_ns;
   VecStore S;
   int pq, pg;
+  LeafVecs* lv;  // this chain warp's fused-leaf operand record (shared memory)
+  __device__ LeafVecs* leaf_vecs() const { return lv; }
 
   __device__ void post(int q, int g) {
     pq = q;
@@ -292,6 +294,7 @@ __global__ void __launch_bounds__(128 + 32 * kDenseCW, 1)
   extern __shared__ __align__(1024) unsigned char dsm[];
   volatile int* flag = reinterpret_cast<volatile int*>(dsm + kUmmaSmemBytes);
   SlotScalars* ss_all = reinterpret_cast<SlotScalars*>(dsm + kUmmaSmemBytes + 64);
+  LeafVecs* lv_all = reinterpret_cast<LeafVecs*>(dsm + kUmmaSmemBytes + 64 + kDenseCW * kMaxSlots * sizeof(SlotScalars));
   const int warp = threadIdx.x >> 5;
   if (warp < 4) {
     // ---------------- GEMM warps
@@ -390,6 +393,7 @@ __global__ void __launch_bounds__(128 + 32 * kDenseCW, 1)
     M.chain = chain;
     M.err = a.err;
     M.spin_ns = a.spin_ns;
+    M.lv = lv_all + cw;
     Engine<WarpTeam, DenseW> E;
     E.D = a.D;
     E.S.base = a.ws + (int64_t)chain * a.nv * a.D;
@@ -397,7 +401,7 @@ __global__ void __launch_bounds__(128 + 32 * kDenseCW, 1)
     E.S.dstride = 1;
     M.S = E.S;
     E.M = M;
-    E.prof = nullptr;
+    E.prof = (A.prof != nullptr && chain == 0) ? A.prof : nullptr;  // TS_PROF: chain 0's leaf phases
     E.prof_last = 0;
     E.tr = nullptr;
     E.ss = ss_all + cw * kMaxSlots;
@@ -418,7 +422,7 @@ int launch_dense(const ts_model* m, int nslots, OpArgs& A, int n_chains, cudaStr
   int dev = 0, nsm = 0, occ = 0;
   TS_CUDA(cudaGetDevice(&dev));
   TS_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-  const size_t smem = kUmmaSmemBytes + 64 + kDenseCW * kMaxSlots * sizeof(SlotScalars);
+  const size_t smem = kUmmaSmemBytes + 64 + kDenseCW * (kMaxSlots * sizeof(SlotScalars) + sizeof(LeafVecs));
   TS_CUDA(cudaFuncSetAttribute(k_dense_op, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   TS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_dense_op, 128 + 32 * kDenseCW, smem));
   const int cap = occ * nsm * kDenseCW;
@@ -446,7 +450,7 @@ static int launch_dense_chunk(const ts_model* m, int nslots, OpArgs& A, int C, i
   int dev = 0, nsm = 0;
   TS_CUDA(cudaGetDevice(&dev));
   TS_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-  const size_t smem = kUmmaSmemBytes + 64 + kDenseCW * kMaxSlots * sizeof(SlotScalars);
+  const size_t smem = kUmmaSmemBytes + 64 + kDenseCW * (kMaxSlots * sizeof(SlotScalars) + sizeof(LeafVecs));
   auto kern = k_dense_op;
   TS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 0;

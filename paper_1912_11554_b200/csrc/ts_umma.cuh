@@ -25,7 +25,10 @@ namespace ts {
 constexpr int kUmmaBM = 128;
 constexpr int kUmmaBN = 64;  // chains per tile (128 measured slower: fewer CTAs share the step)
 constexpr int kUmmaBK = 32;  // fp32/tf32 elements per k-block = one 128-B swizzle row
-constexpr int kUmmaStages = 4;  // 2: 8.5 M, 4: 9.6 M, 8: 8.2 M chain-leapfrog/s (shared memory vs the chains' L1)
+#ifndef TS_UMMA_STAGES
+#define TS_UMMA_STAGES 4
+#endif
+constexpr int kUmmaStages = TS_UMMA_STAGES;  // 2: 8.5 M, 4: 9.6 M, 8: 8.2 M chain-leapfrog/s (shared memory vs the chains' L1)
 constexpr int kUmmaABytes = kUmmaBM * kUmmaBK * 4;  // 16 KB
 constexpr int kUmmaBBytes = kUmmaBN * kUmmaBK * 4;  // 8 KB
 constexpr int kUmmaStageBytes = kUmmaABytes + kUmmaBBytes;

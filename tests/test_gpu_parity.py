@@ -707,9 +707,12 @@ def test_dense_potential_gradient(D, oracle):
         assert np.allclose(o32[:, 0], 0.5 * np.einsum("kd,kd->k", q, g), rtol=2e-3)
 
 
-def test_dense_tree_fp64_matches_oracle(oracle):
+@pytest.mark.parametrize("D", [16, 160])
+def test_dense_tree_fp64_matches_oracle(D, oracle):
+    """D = 160 takes the batched model's fused leaf pass (D >= 128: kick,
+    prefix sum, energies, next drift, request row and NodeStore copies in one
+    vector loop); D = 16 the separate loops."""
     t = ts()
-    D = 16
     A = _spd(D, 3)
     om = oracle.Model("dense_gaussian", D, dense_a=A.tolist())
     m = t.dense_gaussian_model(A, precision="fp64")

@@ -68,83 +68,100 @@ static __device__ __noinline__ void warp_copy2(double2* __restrict__ a, const do
 }
 
 // Elementwise leaf updates for warp-owned large-D vectors: 16-byte accesses,
-// 4 x double2 per operand in flight per lane; per-component arithmetic is the
-// same as the scalar loops (so results are identical).
+// two double2 per operand in flight per lane in an unpredicated main loop
+// plus a tail (the earlier four / eight-wide predicated loops spilled their
+// arrays to local memory inside the loop); per-component arithmetic is the
+// same as the scalar loops (so results are identical), and per lane the
+// elements are visited in ascending order (reduction order unchanged).
+#define TS_WARP_LOOP2(N2, BODY)                               \
+  {                                                           \
+    int i_ = (int)(threadIdx.x & 31);                         \
+    const int nfull_ = (N2) & ~63;                            \
+    _Pragma("unroll 1") for (; i_ < nfull_; i_ += 64) { BODY(i_, i_ + 32) } \
+    _Pragma("unroll 1") for (; i_ < (N2); i_ += 32) { BODY(i_, -1) }        \
+  }
 static __device__ __noinline__ void warp_drift2(double2* __restrict__ nq, double2* __restrict__ nr,
                                                 const double2* __restrict__ q, const double2* __restrict__ r,
                                                 const double2* __restrict__ g, const double2* __restrict__ inv,
                                                 double half, double eps, int n2) {
-  for (int base = (int)(threadIdx.x & 31); base < n2; base += 32 * 4) {
-    double2 tq[4], tr[4], tg[4], ti[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-      if (base + 32 * u < n2) { tq[u] = __ldcg(q + base + 32 * u); tr[u] = __ldcg(r + base + 32 * u); tg[u] = __ldcg(g + base + 32 * u); ti[u] = __ldcg(inv + base + 32 * u); }
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-      if (base + 32 * u < n2) {
-        double2 rh, nqv;
-        rh.x = __dsub_rn(tr[u].x, __dmul_rn(half, tg[u].x));
-        rh.y = __dsub_rn(tr[u].y, __dmul_rn(half, tg[u].y));
-        nqv.x = __dadd_rn(tq[u].x, __dmul_rn(eps, __dmul_rn(ti[u].x, rh.x)));
-        nqv.y = __dadd_rn(tq[u].y, __dmul_rn(eps, __dmul_rn(ti[u].y, rh.y)));
-        nr[base + 32 * u] = rh;
-        nq[base + 32 * u] = nqv;
-      }
+  auto one = [&](int i, double2 tq, double2 tr, double2 tg, double2 ti) {
+    double2 rh, nqv;
+    rh.x = __dsub_rn(tr.x, __dmul_rn(half, tg.x));
+    rh.y = __dsub_rn(tr.y, __dmul_rn(half, tg.y));
+    nqv.x = __dadd_rn(tq.x, __dmul_rn(eps, __dmul_rn(ti.x, rh.x)));
+    nqv.y = __dadd_rn(tq.y, __dmul_rn(eps, __dmul_rn(ti.y, rh.y)));
+    nr[i] = rh;
+    nq[i] = nqv;
+  };
+#define TS_BODY(I, J)                                                                                          \
+  const double2 q0 = __ldcg(q + I), r0 = __ldcg(r + I), g0 = __ldcg(g + I), v0 = __ldcg(inv + I);            \
+  if (J >= 0) {                                                                                                \
+    const double2 q1 = __ldcg(q + J), r1 = __ldcg(r + J), g1 = __ldcg(g + J), v1 = __ldcg(inv + J);          \
+    one(I, q0, r0, g0, v0);                                                                                    \
+    one(J, q1, r1, g1, v1);                                                                                    \
+  } else {                                                                                                     \
+    one(I, q0, r0, g0, v0);                                                                                    \
   }
+  TS_WARP_LOOP2(n2, TS_BODY)
+#undef TS_BODY
 }
 static __device__ __noinline__ void warp_advance2(double2* __restrict__ q, double2* __restrict__ r,
                                                   double2* __restrict__ g, const double2* __restrict__ nq,
                                                   const double2* __restrict__ nr, const double2* __restrict__ ng,
                                                   double half, int n2) {
-  for (int base = (int)(threadIdx.x & 31); base < n2; base += 32 * 4) {
-    double2 tq[4], tr[4], tg[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-      if (base + 32 * u < n2) { tq[u] = __ldcg(nq + base + 32 * u); tr[u] = __ldcg(nr + base + 32 * u); tg[u] = __ldcg(ng + base + 32 * u); }
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-      if (base + 32 * u < n2) {
-        double2 rv;
-        rv.x = __dsub_rn(tr[u].x, __dmul_rn(half, tg[u].x));
-        rv.y = __dsub_rn(tr[u].y, __dmul_rn(half, tg[u].y));
-        q[base + 32 * u] = tq[u];
-        g[base + 32 * u] = tg[u];
-        r[base + 32 * u] = rv;
-      }
+  auto one = [&](int i, double2 tq, double2 tr, double2 tg) {
+    double2 rv;
+    rv.x = __dsub_rn(tr.x, __dmul_rn(half, tg.x));
+    rv.y = __dsub_rn(tr.y, __dmul_rn(half, tg.y));
+    q[i] = tq;
+    g[i] = tg;
+    r[i] = rv;
+  };
+#define TS_BODY(I, J)                                                                 \
+  const double2 q0 = __ldcg(nq + I), r0 = __ldcg(nr + I), g0 = __ldcg(ng + I);      \
+  if (J >= 0) {                                                                       \
+    const double2 q1 = __ldcg(nq + J), r1 = __ldcg(nr + J), g1 = __ldcg(ng + J);    \
+    one(I, q0, r0, g0);                                                               \
+    one(J, q1, r1, g1);                                                               \
+  } else {                                                                            \
+    one(I, q0, r0, g0);                                                               \
   }
+  TS_WARP_LOOP2(n2, TS_BODY)
+#undef TS_BODY
 }
 static __device__ __noinline__ void warp_add2(double2* __restrict__ c, const double2* __restrict__ r, int n2) {
-  for (int base = (int)(threadIdx.x & 31); base < n2; base += 32 * 8) {
-    double2 tc[8], tr[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u)
-      if (base + 32 * u < n2) { tc[u] = __ldcg(c + base + 32 * u); tr[u] = __ldcg(r + base + 32 * u); }
-#pragma unroll
-    for (int u = 0; u < 8; ++u)
-      if (base + 32 * u < n2) {
-        double2 o;
-        o.x = __dadd_rn(tc[u].x, tr[u].x);
-        o.y = __dadd_rn(tc[u].y, tr[u].y);
-        c[base + 32 * u] = o;
-      }
+  auto one = [&](int i, double2 tc, double2 tr) { c[i] = make_double2(__dadd_rn(tc.x, tr.x), __dadd_rn(tc.y, tr.y)); };
+#define TS_BODY(I, J)                                          \
+  const double2 c0 = __ldcg(c + I), r0 = __ldcg(r + I);       \
+  if (J >= 0) {                                                \
+    const double2 c1 = __ldcg(c + J), r1 = __ldcg(r + J);     \
+    one(I, c0, r0);                                            \
+    one(J, c1, r1);                                            \
+  } else {                                                     \
+    one(I, c0, r0);                                            \
   }
+  TS_WARP_LOOP2(n2, TS_BODY)
+#undef TS_BODY
 }
 // per-lane partial of kinetic_energy_impl over warp-owned vectors (lane's
 // components in order 2k, 2k+1 of each of its double2 slots)
 static __device__ __noinline__ double warp_kinetic2(const double2* __restrict__ r, const double2* __restrict__ inv, int n2) {
   double acc = 0.0;
-  for (int base = (int)(threadIdx.x & 31); base < n2; base += 32 * 8) {
-    double2 tr[8], ti[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u)
-      if (base + 32 * u < n2) { tr[u] = __ldcg(r + base + 32 * u); ti[u] = __ldcg(inv + base + 32 * u); }
-#pragma unroll
-    for (int u = 0; u < 8; ++u)
-      if (base + 32 * u < n2) {
-        acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(__dmul_rn(0.5, tr[u].x), tr[u].x), ti[u].x));
-        acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(__dmul_rn(0.5, tr[u].y), tr[u].y), ti[u].y));
-      }
+  auto one = [&](double2 tr, double2 ti) {
+    acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(__dmul_rn(0.5, tr.x), tr.x), ti.x));
+    acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(__dmul_rn(0.5, tr.y), tr.y), ti.y));
+  };
+#define TS_BODY(I, J)                                          \
+  const double2 r0 = __ldcg(r + I), v0 = __ldcg(inv + I);     \
+  if (J >= 0) {                                                \
+    const double2 r1 = __ldcg(r + J), v1 = __ldcg(inv + J);   \
+    one(r0, v0);                                               \
+    one(r1, v1);                                               \
+  } else {                                                     \
+    one(r0, v0);                                               \
   }
+  TS_WARP_LOOP2(n2, TS_BODY)
+#undef TS_BODY
   return acc;
 }
 // generalized U-turn dots of the running subtree with rho = (cum - cum_first) + r_first

@@ -87,6 +87,26 @@ __device__ __forceinline__ float tf32r(double x) {
   return __uint_as_float(v);
 }
 
+// Request-row write of one chain (warp), 4 components per lane and step, two
+// steps per iteration in an unpredicated main loop (a separate function: the
+// engine's registers stay out of the loop, which spilled to local memory
+// when inlined)
+static __device__ __noinline__ void dense_write_row_tf32(float4* __restrict__ row, const double2* __restrict__ q2, int n4) {
+  auto one = [&](int i) {
+    const double2 a = q2[2 * i], b = q2[2 * i + 1];
+    row[i] = make_float4(tf32r(a.x), tf32r(a.y), tf32r(b.x), tf32r(b.y));
+  };
+  int i = (int)(threadIdx.x & 31);
+#pragma unroll 1
+  for (; i + 32 < n4; i += 64) {
+    const double2 a0 = q2[2 * i], b0 = q2[2 * i + 1];
+    const double2 a1 = q2[2 * (i + 32)], b1 = q2[2 * (i + 32) + 1];
+    row[i] = make_float4(tf32r(a0.x), tf32r(a0.y), tf32r(b0.x), tf32r(b0.y));
+    row[i + 32] = make_float4(tf32r(a1.x), tf32r(a1.y), tf32r(b1.x), tf32r(b1.y));
+  }
+#pragma unroll 1
+  for (; i < n4; i += 32) one(i);
+}
 struct DenseW : NoTraj {
   static constexpr bool kAsync = true;
   static constexpr bool kVecOps = true;  // D ~ 1000 vectors in global memory
@@ -116,20 +136,7 @@ struct DenseW : NoTraj {
       double* row = xt64 + (int64_t)chain * D;
       for (int d = lane; d < D; d += 32) row[d] = qv[d];
     } else {
-      // 4 consecutive components per lane and iteration (16-B stores, 2 x
-      // 16-B loads), 4 iterations in flight (D % 4 == 0, checked at creation)
-      float4* row = reinterpret_cast<float4*>(xt + (int64_t)chain * D);
-      const double2* q2 = reinterpret_cast<const double2*>(qv);
-      const int n4 = D >> 2;
-      for (int base = lane; base < n4; base += 32 * 4) {
-        double2 a[4], b[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (base + 32 * u < n4) { a[u] = q2[2 * (base + 32 * u)]; b[u] = q2[2 * (base + 32 * u) + 1]; }
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (base + 32 * u < n4) row[base + 32 * u] = make_float4(tf32r(a[u].x), tf32r(a[u].y), tf32r(b[u].x), tf32r(b[u].y));
-      }
+      dense_write_row_tf32(reinterpret_cast<float4*>(xt + (int64_t)chain * D), reinterpret_cast<const double2*>(qv), D >> 2);
     }
     // the GEMM reads the row through the async (TMA) proxy in another CTA
     asm volatile("fence.proxy.async.global;" ::: "memory");

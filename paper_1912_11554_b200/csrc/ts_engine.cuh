@@ -315,37 +315,45 @@ static __device__ TS_LEAF_INLINE double2 warp_leaf_fused(const LeafVecs* __restr
   }
   return make_double2(kin, ud);  // (kinetic-energy partial, this lane's part of q . g)
 }
-// up to 5 vector copies in one pass (k pairs), 2 x double2 per operand in flight
+// K vector copies in one pass (K = 2, 3 or 5 pairs): U x double2 per operand
+// in flight per lane (4 for K <= 3, 2 for K = 5) in an unpredicated main
+// loop plus a one-element tail
+template <int K, int U>
 static __device__ __noinline__ void warp_copy_multi(double2* __restrict__ d0, const double2* __restrict__ s0,
                                                     double2* __restrict__ d1, const double2* __restrict__ s1,
                                                     double2* __restrict__ d2, const double2* __restrict__ s2,
                                                     double2* __restrict__ d3, const double2* __restrict__ s3,
-                                                    double2* __restrict__ d4, const double2* __restrict__ s4, int k,
-                                                    int n2) {
-  for (int base = (int)(threadIdx.x & 31); base < n2; base += 32 * 2) {
-    double2 t[5][2];
+                                                    double2* __restrict__ d4, const double2* __restrict__ s4, int n2) {
+  int i = (int)(threadIdx.x & 31);
+  const int nfull = n2 - n2 % (32 * U);
+#pragma unroll 1
+  for (; i < nfull; i += 32 * U) {
+    double2 t[K][U];
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int i = base + 32 * u;
-      if (i < n2) {
-        t[0][u] = __ldcg(s0 + i);
-        t[1][u] = __ldcg(s1 + i);
-        t[2][u] = __ldcg(s2 + i);
-        if (k > 3) t[3][u] = __ldcg(s3 + i);
-        if (k > 4) t[4][u] = __ldcg(s4 + i);
-      }
+    for (int u = 0; u < U; ++u) {
+      t[0][u] = __ldcg(s0 + i + 32 * u);
+      t[1][u] = __ldcg(s1 + i + 32 * u);
+      if constexpr (K > 2) t[2][u] = __ldcg(s2 + i + 32 * u);
+      if constexpr (K > 3) { t[3][u] = __ldcg(s3 + i + 32 * u); t[4][u] = __ldcg(s4 + i + 32 * u); }
     }
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int i = base + 32 * u;
-      if (i < n2) {
-        d0[i] = t[0][u];
-        d1[i] = t[1][u];
-        d2[i] = t[2][u];
-        if (k > 3) d3[i] = t[3][u];
-        if (k > 4) d4[i] = t[4][u];
-      }
+    for (int u = 0; u < U; ++u) {
+      d0[i + 32 * u] = t[0][u];
+      d1[i + 32 * u] = t[1][u];
+      if constexpr (K > 2) d2[i + 32 * u] = t[2][u];
+      if constexpr (K > 3) { d3[i + 32 * u] = t[3][u]; d4[i + 32 * u] = t[4][u]; }
     }
+  }
+#pragma unroll 1
+  for (; i < n2; i += 32) {
+    const double2 x0 = __ldcg(s0 + i), x1 = __ldcg(s1 + i);
+    double2 x2, x3, x4;
+    if constexpr (K > 2) x2 = __ldcg(s2 + i);
+    if constexpr (K > 3) { x3 = __ldcg(s3 + i); x4 = __ldcg(s4 + i); }
+    d0[i] = x0;
+    d1[i] = x1;
+    if constexpr (K > 2) d2[i] = x2;
+    if constexpr (K > 3) { d3[i] = x3; d4[i] = x4; }
   }
 }
 
@@ -497,18 +505,23 @@ struct Engine {
   __device__ void copy_group(int d0, int s0, int d1, int s1, int d2, int s2, int d3 = -1, int s3 = -1, int d4 = -1,
                              int s4 = -1) {
     if constexpr (Team::kWarp && Team::kUnitStride && Model::kVecOps) {
-      const int k = d3 < 0 ? 3 : 5;
+      // k = 2 when the third pair repeats the second (the proposal copies)
+      const int k = d3 >= 0 ? 5 : ((d2 == d1 && s2 == s1) ? 2 : 3);
       double* a[5] = {v(d0), v(d1), v(d2), k > 3 ? v(d3) : v(d0), k > 3 ? v(d4) : v(d0)};
       const double* b[5] = {v(s0), v(s1), v(s2), k > 3 ? v(s3) : v(s0), k > 3 ? v(s4) : v(s0)};
       bool ok = D >= 128 && (D & 1) == 0;
 #pragma unroll
       for (int i = 0; i < 5; ++i) ok = ok && al16(a[i]) && al16(b[i]);
       if (ok) {
-        warp_copy_multi(reinterpret_cast<double2*>(a[0]), reinterpret_cast<const double2*>(b[0]),
-                        reinterpret_cast<double2*>(a[1]), reinterpret_cast<const double2*>(b[1]),
-                        reinterpret_cast<double2*>(a[2]), reinterpret_cast<const double2*>(b[2]),
-                        reinterpret_cast<double2*>(a[3]), reinterpret_cast<const double2*>(b[3]),
-                        reinterpret_cast<double2*>(a[4]), reinterpret_cast<const double2*>(b[4]), k, D >> 1);
+        double2* A0 = reinterpret_cast<double2*>(a[0]); double2* A1 = reinterpret_cast<double2*>(a[1]);
+        double2* A2 = reinterpret_cast<double2*>(a[2]); double2* A3 = reinterpret_cast<double2*>(a[3]);
+        double2* A4 = reinterpret_cast<double2*>(a[4]);
+        const double2* B0 = reinterpret_cast<const double2*>(b[0]); const double2* B1 = reinterpret_cast<const double2*>(b[1]);
+        const double2* B2 = reinterpret_cast<const double2*>(b[2]); const double2* B3 = reinterpret_cast<const double2*>(b[3]);
+        const double2* B4 = reinterpret_cast<const double2*>(b[4]);
+        if (k == 2) warp_copy_multi<2, 4>(A0, B0, A1, B1, A1, B1, A1, B1, A1, B1, D >> 1);
+        else if (k == 3) warp_copy_multi<3, 4>(A0, B0, A1, B1, A2, B2, A2, B2, A2, B2, D >> 1);
+        else warp_copy_multi<5, 2>(A0, B0, A1, B1, A2, B2, A3, B3, A4, B4, D >> 1);
         return;
       }
     }

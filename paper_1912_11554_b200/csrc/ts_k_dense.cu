@@ -248,10 +248,12 @@ struct DenseArgs {
   unsigned long long* prof;  // optional (TS_PROF): CTA-0 ns [snapshot+barrier, GEMM, release], steps, busy steps
   unsigned long long* posted;   // [Cpad] (zeroed before launch)
   unsigned long long* served;   // [Cpad]
-  unsigned long long* pending;  // [Cpad] request served by the current step (0 = none)
-  unsigned long long* npend;    // [2] outstanding requests of the step, [2..4) all-done flags (rotating)
+  unsigned long long* pending;  // [2][Cpad] request served by the step of that parity (0 = none)
+  unsigned long long* npend;    // [4] outstanding requests of the step (step & 3), [4..6) all-done flags (step & 1)
   unsigned int* err;            // sticky synchronisation-timeout flag of the model (SpinGuard)
   unsigned long long spin_ns;
+  unsigned int* ncnt;           // [2][N-tiles] finished M-tiles of each N-tile per step parity (early release)
+  int early;                    // 1: the last M-tile of an N-tile releases its chains (no release barrier)
 };
 
 __device__ __forceinline__ void gemm_grid_barrier(unsigned long long* bar, unsigned long long& epoch, unsigned int* err,
@@ -273,7 +275,7 @@ __device__ __forceinline__ void gemm_grid_barrier(unsigned long long* bar, unsig
 
 // SIMT fp64 tile (parity policy): thread = row m, 16 chains at a time, k in
 // order, multiply then add (oracle/turnstile_oracle.py restates it bit for bit)
-__device__ void dense_tile_fp64(const DenseArgs& a, int m0, int n0) {
+__device__ void dense_tile_fp64(const DenseArgs& a, const unsigned long long* pend, int m0, int n0) {
   const int m = m0 + (int)threadIdx.x;
   if (m >= a.D) return;
   const double* arow = a.a64 + (int64_t)m * a.D;
@@ -291,7 +293,7 @@ __device__ void dense_tile_fp64(const DenseArgs& a, int m0, int n0) {
     }
 #pragma unroll
     for (int j = 0; j < 16; ++j)
-      if (j < nmax && __ldcg(a.pending + n0 + nb + j) != 0ULL) a.gt64[(int64_t)(n0 + nb + j) * a.D + m] = acc[j];
+      if (j < nmax && __ldcg(pend + n0 + nb + j) != 0ULL) a.gt64[(int64_t)(n0 + nb + j) * a.D + m] = acc[j];
   }
 }
 
@@ -326,20 +328,23 @@ __global__ void __launch_bounds__(128 + 32 * kDenseCW, 1)
       if (t < a.cpc) {
         const unsigned long long p = ld_acquire_u64(a.posted + my_chain);
         mine = p > srv ? p : 0ULL;
-        a.pending[my_chain] = mine;
-        if (mine) atomicAdd(a.npend + (step & 1), 1ULL);
+        a.pending[(step & 1) * a.Cpad + my_chain] = mine;
+        if (mine) atomicAdd(a.npend + (step & 3), 1ULL);
       }
       // the exit decision must be the same in every CTA: CTA 0 samples the
       // finished-chain count BEFORE the barrier (chains keep finishing
       // asynchronously, so reading it after the barrier could differ per CTA)
       if (t == 0 && blockIdx.x == 0)
-        a.npend[2 + (step & 1)] = (*reinterpret_cast<volatile int*>(a.done) >= total) ? 1ULL : 0ULL;
+        a.npend[4 + (step & 1)] = (*reinterpret_cast<volatile int*>(a.done) >= total) ? 1ULL : 0ULL;
       gemm_grid_barrier(a.bar, epoch, a.err, a.spin_ns);
       if (t == 0) {
-        const unsigned long long np = ld_relaxed_u64(a.npend + (step & 1));
-        const bool all_done = ld_relaxed_u64(a.npend + 2 + (step & 1)) != 0ULL;
+        const unsigned long long np = ld_relaxed_u64(a.npend + (step & 3));
+        const bool all_done = ld_relaxed_u64(a.npend + 4 + (step & 1)) != 0ULL;
         *flag = (np == 0ULL && all_done) ? 0 : (np ? 1 : 2);
-        if (blockIdx.x == 0) a.npend[(step + 1) & 1] = 0ULL;  // next slot: last read before this barrier
+        // slot of step + 2: last read after the barrier of step - 2, so every
+        // CTA is done with it; with the per-N-tile release a fast CTA can reach
+        // the next snapshot before CTA 0 gets here, hence four slots
+        if (blockIdx.x == 0) a.npend[(step + 2) & 3] = 0ULL;
       }
       asm volatile("bar.sync 4, 128;" ::: "memory");
       const int f = *flag;
@@ -349,18 +354,41 @@ __global__ void __launch_bounds__(128 + 32 * kDenseCW, 1)
         a.prof[0] += tp1 - tp0;
         tp0 = tp1;
       }
+      const unsigned long long* pend = a.pending + (step & 1) * a.Cpad;
       if (f == 1) {  // at least one request in the grid
         if (t == 0) asm volatile("fence.proxy.async.global;" ::: "memory");
         for (int tile = blockIdx.x; tile < mt * nt; tile += gridDim.x) {
           const int m0 = (tile % mt) * kUmmaBM, n0 = (tile / mt) * kUmmaBN;
           // skip N-tiles without outstanding requests (uniform over the 128 threads)
           int any = 0;
-          for (int j = t; j < kUmmaBN; j += 128) any |= __ldcg(a.pending + n0 + j) != 0ULL;
+          for (int j = t; j < kUmmaBN; j += 128) any |= __ldcg(pend + n0 + j) != 0ULL;
           any = gemm_sync_or(any);
           if (!any) continue;
-          if (a.fp64) dense_tile_fp64(a, m0, n0);
+          if (a.fp64) dense_tile_fp64(a, pend, m0, n0);
           else
-            g.tile(&tmA, &tmX, m0, n0, nkb, a.gt, a.D, a.D - m0 < kUmmaBM ? a.D - m0 : kUmmaBM, kUmmaBN, a.pending + n0);
+            g.tile(&tmA, &tmX, m0, n0, nkb, a.gt, a.D, a.D - m0 < kUmmaBM ? a.D - m0 : kUmmaBM, kUmmaBN, pend + n0);
+          if (a.early) {
+            // the CTA finishing the last M-tile of this N-tile releases its
+            // requested chains (every M-tile CTA fenced its gradient stores
+            // before counting; the counter is reset for step + 2)
+            asm volatile("bar.sync 4, 128;" ::: "memory");
+            __shared__ int last;
+            if (t == 0) {
+              __threadfence();
+              unsigned int* cnt = a.ncnt + (step & 1) * nt + tile / mt;
+              const unsigned int old = atomicAdd(cnt, 1u);
+              last = (old + 1u == (unsigned int)mt);
+              if (last) {
+                __threadfence();
+                *cnt = 0u;
+              }
+            }
+            asm volatile("bar.sync 4, 128;" ::: "memory");
+            if (last && t < kUmmaBN) {
+              const unsigned long long pv = __ldcg(pend + n0 + t);
+              if (pv != 0ULL) st_release_gpu_u64(a.served + n0 + t, pv);
+            }
+          }
         }
         busy += 1;
       }
@@ -369,10 +397,16 @@ __global__ void __launch_bounds__(128 + 32 * kDenseCW, 1)
         a.prof[1] += tp1 - tp0;
         tp0 = tp1;
       }
-      gemm_grid_barrier(a.bar, epoch, a.err, a.spin_ns);  // all gradient tiles written
-      if (t < a.cpc && mine) {
-        srv = mine;
-        st_release_gpu_u64(a.served + my_chain, mine);
+      if (a.early) {
+        // released per N-tile above; the next snapshot only needs this
+        // CTA's view of what it has served
+        if (t < a.cpc && mine) srv = mine;
+      } else {
+        gemm_grid_barrier(a.bar, epoch, a.err, a.spin_ns);  // all gradient tiles written
+        if (t < a.cpc && mine) {
+          srv = mine;
+          st_release_gpu_u64(a.served + my_chain, mine);
+        }
       }
       if (prof) {
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tp1));
@@ -464,7 +498,8 @@ static int launch_dense_chunk(const ts_model* m, int nslots, OpArgs& A, int C, i
   TS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 128 + 32 * kDenseCW, smem));
   if ((int64_t)occ * nsm < grid) return set_err(TS_EUNSUPPORTED, "dense model: too many chains for one co-resident grid");
   // workspaces (grown on demand, owned by the model)
-  const size_t need = (size_t)Cpad * D * (m->fp64 ? 16 : 8) + (size_t)C * nv * D * 8 + 64 + (size_t)Cpad * 24 + 64;  // + flags
+  const size_t need = (size_t)Cpad * D * (m->fp64 ? 16 : 8) + (size_t)C * nv * D * 8 + 64 + (size_t)Cpad * 32 + 64 +
+                     2 * (size_t)(Cpad / kUmmaBN) * sizeof(unsigned int) + 16;  // + flags, N-tile counters
   if (mm->dws_size < need) {
     if (mm->dws) cudaFree(mm->dws);
     mm->dws = nullptr;
@@ -492,7 +527,14 @@ static int launch_dense_chunk(const ts_model* m, int nslots, OpArgs& A, int C, i
   a.posted = reinterpret_cast<unsigned long long*>(p);
   a.served = a.posted + Cpad;
   a.pending = a.served + Cpad;
-  a.npend = a.pending + Cpad;
+  a.npend = a.pending + 2 * Cpad;
+  a.ncnt = reinterpret_cast<unsigned int*>(a.npend + 8);
+  // per-N-tile release instead of the release barrier: correct (same chains
+  // bit for bit) but slower, 9.33 -> 8.36 M chain-leapfrog/s: steps get
+  // shorter (23 vs 30 us) yet serve fewer requests each, and the gradient
+  // wait per leaf does not drop; TS_DENSE_EARLY=1 for A/B
+  a.early = 0;
+  if (const char* e = getenv("TS_DENSE_EARLY")) a.early = atoi(e) != 0;
   a.a64 = m->params;
   a.err = m->errw;
   a.spin_ns = spin_limit_ns();
@@ -506,7 +548,7 @@ static int launch_dense_chunk(const ts_model* m, int nslots, OpArgs& A, int C, i
     if (rc) return rc;
   }
   TS_CUDA(cudaMemsetAsync(mm->dws, 0, 64, st));
-  TS_CUDA(cudaMemsetAsync(a.posted, 0, ((size_t)Cpad * 3 + 4) * sizeof(unsigned long long), st));
+  TS_CUDA(cudaMemsetAsync(a.posted, 0, ((size_t)Cpad * 4 + 8) * sizeof(unsigned long long) + 2 * (size_t)(Cpad / kUmmaBN) * sizeof(unsigned int), st));
   const bool prof = getenv("TS_PROF") != nullptr;  // profiling aid: CTA-0 step phases to stderr
   if (prof) a.prof = reinterpret_cast<unsigned long long*>(mm->dws + 16);  // 5 words in the zeroed header
   int ns = nslots;

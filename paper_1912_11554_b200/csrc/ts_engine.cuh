@@ -233,6 +233,10 @@ __device__ __forceinline__ P* lds_ptr(uint32_t rec, uint32_t off) {
   asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(rec + off));
   return reinterpret_cast<P*>(v);
 }
+#ifndef TS_PF_DIST
+#define TS_PF_DIST 192  // double2 elements ahead (three iterations of the two-wide loop; 64 / 192 / none: 9.40 / 9.52 / 9.35 M)
+#endif
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 template <bool F64ROW, int ST>
 static __device__ TS_LEAF_INLINE double2 warp_leaf_fused(const LeafVecs* __restrict__ L) {
   // grow: the served gradient row (fp32 tf32-GEMM output, or doubles);
@@ -304,6 +308,16 @@ static __device__ TS_LEAF_INLINE double2 warp_leaf_fused(const LeafVecs* __restr
   const int nfull = n2 & ~63;
   for (; i < nfull; i += 64) {
     const int j = i + 32;
+#ifndef TS_NO_L2_PREFETCH
+    // the NodeStore workspaces exceed L2, so these streams come from DRAM:
+    // pull the elements of the iteration after next into L2 (no registers)
+    if (i + TS_PF_DIST < n2) {
+      prefetch_l2(lds_ptr<const double2>(rec, oNQ) + i + TS_PF_DIST);
+      prefetch_l2(lds_ptr<const double2>(rec, oNR) + i + TS_PF_DIST);
+      prefetch_l2(lds_ptr<const double2>(rec, oINV) + i + TS_PF_DIST);
+      prefetch_l2(lds_ptr<const double2>(rec, oCUM) + i + TS_PF_DIST);
+    }
+#endif
     const double2 q0 = ld(oNQ, i), r0 = ld(oNR, i), i0 = ld(oINV, i), c0 = ld(oCUM, i), g0 = load_g(i);
     const double2 q1 = ld(oNQ, j), r1 = ld(oNR, j), i1 = ld(oINV, j), c1 = ld(oCUM, j), g1 = load_g(j);
     body(i, q0, r0, g0, i0, c0);

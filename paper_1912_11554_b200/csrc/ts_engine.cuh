@@ -1034,11 +1034,14 @@ struct Engine {
               if (prof != nullptr && T.leader()) { const long long c = clock64(); prof[28] += c - prof_w1; prof_w1 = c; }
               M.post_written(V_NQ, V_NG);
               if (prof != nullptr && T.leader()) { const long long c = clock64(); prof[29] += c - prof_w1; prof[25] += c - prof_w1; prof_w1 = c; }
+              // both warp reductions in one interleaved shuffle tree (same
+              // tree order per value as T.sum)
+              double uds = ud, ke = kin;
+              T.sum2(uds, ke);
               {
-                const double uu = 0.5 * T.sum(ud);  // DenseW::wait's U, formed in the pass
+                const double uu = 0.5 * uds;  // DenseW::wait's U, formed in the pass
                 cur_U = isfinite(uu) ? uu : kInf();
               }
-              const double ke = T.sum(kin);
               if (!isfinite(cur_U)) h = kInf();
               else {
                 h = __dadd_rn(cur_U, ke);

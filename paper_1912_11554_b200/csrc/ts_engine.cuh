@@ -166,9 +166,9 @@ static __device__ __noinline__ double warp_kinetic2(const double2* __restrict__ 
 }
 // generalized U-turn dots of the running subtree with rho = (cum - cum_first) + r_first
 // formed on the fly: per-lane partials a = sum rho inv rl, b = sum rho inv rr
-static __device__ __noinline__ void warp_gen_uturn2(const double2* __restrict__ cum, const double2* __restrict__ cf,
+static __device__ __noinline__ double2 warp_gen_uturn2(const double2* __restrict__ cum, const double2* __restrict__ cf,
                                                     const double2* __restrict__ fr, const double2* __restrict__ inv,
-                                                    const double2* __restrict__ rr, int n2, double* ab) {
+                                                    const double2* __restrict__ rr, int n2) {
   double a = 0.0, b = 0.0;
   for (int base = (int)(threadIdx.x & 31); base < n2; base += 32 * 4) {
     double2 tc[4], tf[4], trf[4], ti[4], trr[4];
@@ -189,8 +189,7 @@ static __device__ __noinline__ void warp_gen_uturn2(const double2* __restrict__ 
         b = __dadd_rn(b, __dmul_rn(wy, trr[u].y));
       }
   }
-  ab[0] = a;
-  ab[1] = b;
+  return make_double2(a, b);  // (a, b) partials in registers (an array argument lived in local memory)
 }
 __device__ __forceinline__ bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 // One pass over a leaf for warp-owned large-D vectors (batched models):
@@ -712,11 +711,10 @@ struct Engine {
         const double* inv = v(V_INV);
         const double* cr = v(V_CR);
         if (D >= 128 && (D & 1) == 0 && al16(cum) && al16(cf) && al16(fr) && al16(inv) && al16(cr)) {
-          double ab[2];
-          warp_gen_uturn2(reinterpret_cast<const double2*>(cum), reinterpret_cast<const double2*>(cf),
-                          reinterpret_cast<const double2*>(fr), reinterpret_cast<const double2*>(inv),
-                          reinterpret_cast<const double2*>(cr), D >> 1, ab);
-          double a = ab[0], b = ab[1];
+          const double2 ab = warp_gen_uturn2(reinterpret_cast<const double2*>(cum), reinterpret_cast<const double2*>(cf),
+                                             reinterpret_cast<const double2*>(fr), reinterpret_cast<const double2*>(inv),
+                                             reinterpret_cast<const double2*>(cr), D >> 1);
+          double a = ab.x, b = ab.y;
           T.sum2(a, b);
           return a < 0.0 || b < 0.0;
         }
